@@ -1,0 +1,141 @@
+// common.cuh -- shared internals of libhf.so (graph object, error plumbing,
+// device helpers).  Nothing here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hf.h"
+
+namespace hf {
+
+// ---- error plumbing -------------------------------------------------------
+void set_error(const std::string &msg);
+const char *last_error();
+
+struct Fail {
+    hf_status st;
+};
+
+#define HF_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ::hf::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));        \
+            throw ::hf::Fail{e_ == cudaErrorMemoryAllocation ? HF_ERR_OOM : HF_ERR_CUDA}; \
+        }                                                                               \
+    } while (0)
+
+#define HF_CHECK_LAUNCH() HF_CUDA(cudaGetLastError())
+
+[[noreturn]] inline void fail(hf_status st, const std::string &msg) {
+    set_error(msg);
+    throw Fail{st};
+}
+
+// ---- device-side error bits (latched in hf_graph::d_err) ------------------
+enum : uint32_t {
+    ERR_PTR = 1u,        // fan-in ptr malformed
+    ERR_SRC = 2u,        // src out of range
+    ERR_NONFINITE = 4u,  // NaN / inf value
+    ERR_FO_PTR = 8u,     // fan-out ptr malformed / mismatch
+    ERR_FO_DST = 16u,    // fan-out dst out of range / not a transpose
+};
+
+// ---- stream-ordered scratch memory ----------------------------------------
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void alloc(size_t b, cudaStream_t st) {
+        release();
+        s = st;
+        bytes = b;
+        if (b) HF_CUDA(cudaMallocAsync(&p, b, st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// ---- the graph -------------------------------------------------------------
+struct Graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int32_t n = 0, m = 0;
+    int sms = 148;
+    // CSR fan-in (edge id = fan-in position), fan-out, per-edge data
+    DevBuf in_ptr, in_src, in_dst, delay;
+    DevBuf out_ptr, out_dst, out_eid;
+    // levelization
+    bool levelized = false;
+    int32_t L = -1;
+    DevBuf level, level_ptr, order;
+    std::vector<int32_t> h_level_ptr;
+    int32_t max_level_width = 0;
+    // batch workspace (at / rat when the caller does not want them), grows on demand
+    DevBuf ws_at, ws_rat;
+    // small device scalars: [0] error bits, [1..] scratch
+    DevBuf d_small;
+    uint32_t *d_err() const { return d_small.as<uint32_t>(); }
+    int32_t *d_scalars() const { return d_small.as<int32_t>() + 8; }   // 56 int32 scratch
+    // profiling
+    bool prof = false;
+    cudaEvent_t ev[6] = {};
+    float ms_lev = 0, ms_fwd = 0, ms_bwd = 0;
+    bool lev_timed = false, prop_timed = false;
+    int64_t launches = 0;
+};
+
+// ---- primitives (primitives.cu) --------------------------------------------
+// exclusive scan of int32 (out may alias in); writes the total to *total_d if non-null
+void scan_exclusive(const int32_t *in, int32_t *out, int64_t count, int32_t *total_d,
+                    cudaStream_t s, Graph &g);
+// stable LSD radix sort of (key, value) pairs, keys in [0, 2^key_bits); vals_in
+// NULL => values are 0..count-1.  Results in keys_out / vals_out.
+void radix_sort_pairs(const int32_t *keys_in, const int32_t *vals_in, int32_t *keys_out,
+                      int32_t *vals_out, int64_t count, int key_bits, cudaStream_t s,
+                      Graph &g);
+// ptr[k] = first index i with sorted_keys[i] >= k, for k in [0, nkeys]; ptr[nkeys] = count
+void keys_to_ptr(const int32_t *sorted_keys, int64_t count, int32_t nkeys, int32_t *ptr,
+                 cudaStream_t s, Graph &g);
+// row id of every CSR position: dst[e] = v for e in [ptr[v], ptr[v+1])
+void csr_row_ids(const int32_t *ptr, int32_t nrows, int32_t *row_of, cudaStream_t s,
+                 Graph &g);
+
+inline int bits_for(int64_t max_key) {
+    int b = 0;
+    while (b < 31 && (int64_t(1) << b) <= max_key) ++b;
+    return b;
+}
+inline int grid_for(int64_t work, int block, int sms, int per_sm = 8) {
+    int64_t gsz = (work + block - 1) / block;
+    int64_t cap = int64_t(sms) * per_sm;
+    if (gsz > cap) gsz = cap;
+    if (gsz < 1) gsz = 1;
+    return int(gsz);
+}
+
+// ---- device helpers --------------------------------------------------------
+// float <-> order-preserving int32 (reading R9): signed compare of the keys
+// orders all non-NaN floats; the map is an involution.
+__device__ __forceinline__ int32_t f2ord(float f) {
+    int32_t b = __float_as_int(f);
+    return b ^ ((b >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float ord2f(int32_t k) {
+    return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF));
+}
+__device__ __forceinline__ float canon0(float x) { return __fadd_rn(x, 0.0f); }  // -0 -> +0
+
+}  // namespace hf

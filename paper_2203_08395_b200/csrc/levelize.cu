@@ -1,0 +1,375 @@
+// levelize.cu -- hf_levelize: on-device Kahn levelization with chain contraction.
+// SURVEY.md §8(a) a2-a4; PAPER.md:689-690 ("no cycles"), 840-848 (join counters).
+//
+// level(v) = 0 for sources, else 1 + max level(pred) (reading R5).
+// Integer longest path, so it may be computed in any association order (exact):
+//  1. in-degree-1 nodes form in-trees hanging below "junctions" (in-degree != 1).
+//     Pointer jumping (Wyllie) gives every such node its junction root r(v) and
+//     its distance dist(v) in O(log depth) rounds -- this is what makes the 1M
+//     node chain (C2) cost 21 rounds instead of 1M frontier steps.
+//  2. Kahn over the junctions only, with atomic join counters cnt[j] = indeg(j)
+//     and a warp-aggregated frontier compaction: a contracted edge r(p) -> j
+//     carries weight dist(p)+1, and level(j) = max(level(r(p)) + dist(p) + 1)
+//     via atomicMax before the counter release.  The frontier expansion is
+//     edge-balanced inside each warp (shuffle prefix sum + binary search), so
+//     high-fan-out hubs do not serialise on one lane.
+//  3. level(v) = level(r(v)) + dist(v) for the in-degree-1 nodes.
+//  4. order = ids stably radix-sorted by level (ascending id inside a level),
+//     level_ptr from the run boundaries.
+// Nodes never resolved (on or below a cycle) are counted -> HF_ERR_CYCLE.
+// Both persistent loops run as cooperative kernels with a grid barrier.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace hf {
+
+namespace {
+
+struct GridBar {
+    unsigned count;
+    unsigned gen;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void grid_sync(GridBar *b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g0 = ld_acquire_u32(&b->gen);
+        __threadfence();
+        unsigned arrived = atomicAdd(&b->count, 1u);
+        if (arrived == gridDim.x - 1) {
+            atomicExch(&b->count, 0u);
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (ld_acquire_u32(&b->gen) == g0) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ long long ld_pd(const long long *p) {
+    return *reinterpret_cast<const volatile long long *>(p);
+}
+__device__ __forceinline__ void st_pd(long long *p, long long v) {
+    *reinterpret_cast<volatile long long *>(p) = v;
+}
+__device__ __forceinline__ long long mk_pd(int parent, int dist) {
+    return (long long)(((unsigned long long)(unsigned)dist << 32) | (unsigned)parent);
+}
+__device__ __forceinline__ int pd_parent(long long x) { return int(unsigned(x)); }
+__device__ __forceinline__ int pd_dist(long long x) { return int(x >> 32); }
+
+// warp-aggregated append of `item` when `pred` (all 32 lanes must call)
+__device__ __forceinline__ void warp_append(bool pred, int item, int *list, int *count) {
+    const int lane = threadIdx.x & 31;
+    unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = item;
+}
+
+// scalars: [0..2] active counts (rotating), [3..5] frontier counts (rotating),
+//          [6] unresolved count, [7] max level, [8] visited junctions
+enum { SC_ACT = 0, SC_FR = 3, SC_UNRES = 6, SC_MAXLV = 7, SC_VIS = 8 };
+
+__global__ void k_lev_init(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
+                           int32_t n, long long *__restrict__ pd, int32_t *__restrict__ cnt,
+                           int32_t *__restrict__ lev, int32_t *__restrict__ active,
+                           int32_t *__restrict__ frontier, int32_t *sc) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nround = (int64_t(n) + 31) / 32 * 32;   // warp-uniform trip count
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nround; v += stride) {
+        bool in = v < n;
+        int deg = 0;
+        if (in) {
+            int b = in_ptr[v];
+            deg = in_ptr[v + 1] - b;
+            pd[v] = deg == 1 ? mk_pd(in_src[b], 1) : mk_pd(int(v), 0);
+            cnt[v] = deg;
+            lev[v] = 0;
+        }
+        warp_append(in && deg == 1, int(v), active, sc + SC_ACT + 0);
+        warp_append(in && deg == 0, int(v), frontier, sc + SC_FR + 0);
+    }
+}
+
+// Pointer jumping over the active in-degree-1 nodes until each points at its
+// junction root (dist of a root is 0).  At most max_rounds rounds; nodes still
+// active afterwards lie on/below an in-degree-1 cycle.
+__global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act_a,
+                           int32_t *__restrict__ act_b, int32_t *sc, int max_rounds,
+                           GridBar *bar) {
+    const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    int32_t *lists[2] = {act_a, act_b};
+    for (int r = 0; r < max_rounds; ++r) {
+        volatile int32_t *vsc = sc;
+        int size = vsc[SC_ACT + r % 3];
+        if (size == 0) break;
+        if (tid == 0) vsc[SC_ACT + (r + 2) % 3] = 0;
+        const int32_t *in = lists[r & 1];
+        int32_t *out = lists[(r + 1) & 1];
+        const int64_t lim = (int64_t(size) + 31) / 32 * 32;
+        for (int64_t i = tid; i < lim; i += nthreads) {
+            bool keep = false;
+            int v = 0;
+            if (i < size) {
+                v = __ldcg(in + i);
+                long long x = ld_pd(pd + v);
+                long long y = ld_pd(pd + pd_parent(x));
+                if (pd_dist(y) != 0) {   // parent is not a root yet: jump
+                    st_pd(pd + v, mk_pd(pd_parent(y), pd_dist(x) + pd_dist(y)));
+                    keep = true;
+                }
+            }
+            warp_append(keep, v, out, sc + SC_ACT + (r + 1) % 3);
+        }
+        grid_sync(bar);
+    }
+}
+
+// Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w).
+__global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__restrict__ ceid,
+                           const int32_t *__restrict__ in_src, const int32_t *__restrict__ in_dst,
+                           const long long *__restrict__ pd, int32_t *__restrict__ cnt,
+                           int32_t *__restrict__ lev, int32_t *__restrict__ fr_a,
+                           int32_t *__restrict__ fr_b, int32_t *sc, GridBar *bar) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    int32_t *lists[2] = {fr_a, fr_b};
+    for (int r = 0;; ++r) {
+        volatile int32_t *vsc = sc;
+        int size = vsc[SC_FR + r % 3];
+        if (size == 0) break;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            vsc[SC_FR + (r + 2) % 3] = 0;
+            vsc[SC_VIS] += size;
+        }
+        const int32_t *in = lists[r & 1];
+        int32_t *out = lists[(r + 1) & 1];
+        for (int64_t base = wid * 32; base < size; base += nwarps * 32) {
+            int64_t i = base + lane;
+            int j = -1, deg = 0, start = 0, lj = 0;
+            if (i < size) {
+                j = __ldcg(in + i);
+                start = cptr[j];
+                deg = cptr[j + 1] - start;
+                lj = __ldcg(lev + j);
+            }
+            int incl = deg;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int excl = incl - deg;
+            int total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int eb = 0; eb < total; eb += 32) {
+                int idx = eb + lane;
+                int lo = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    int cand = lo + step;
+                    int ev = __shfl_sync(0xffffffffu, excl, cand & 31);
+                    if (cand < 32 && ev <= idx) lo = cand;
+                }
+                int o_excl = __shfl_sync(0xffffffffu, excl, lo);
+                int o_start = __shfl_sync(0xffffffffu, start, lo);
+                int o_lev = __shfl_sync(0xffffffffu, lj, lo);
+                bool ready = false;
+                int k = 0;
+                if (idx < total) {
+                    int e = ceid[o_start + (idx - o_excl)];
+                    k = in_dst[e];
+                    int p = in_src[e];
+                    int w = pd_dist(ld_pd(pd + p)) + 1;
+                    atomicMax(lev + k, o_lev + w);
+                    ready = atomicSub(cnt + k, 1) == 1;
+                }
+                warp_append(ready, k, out, sc + SC_FR + (r + 1) % 3);
+            }
+        }
+        grid_sync(bar);
+    }
+}
+
+// contracted-edge key of every fan-in edge e = (p -> j): r(p) if j is a junction
+// with indeg >= 2 and p resolved, else n (dropped)
+__global__ void k_lev_ckeys(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
+                            const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
+                            int32_t n, int32_t m, int32_t *__restrict__ keys) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int j = in_dst[e];
+        int deg = in_ptr[j + 1] - in_ptr[j];
+        int key = n;
+        if (deg >= 2) {
+            long long x = pd[in_src[e]];
+            int r = pd_parent(x);
+            if (pd_dist(x) == 0 || pd_dist(pd[r]) == 0) key = r;
+        }
+        keys[e] = key;
+    }
+}
+
+__global__ void k_lev_final(const long long *__restrict__ pd, const int32_t *__restrict__ cnt,
+                            const int32_t *__restrict__ lev, int32_t n,
+                            int32_t *__restrict__ level, int32_t *sc) {
+    int unres = 0, mx = -1;
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n;
+         v += int64_t(gridDim.x) * blockDim.x) {
+        long long x = pd[v];
+        int lv = -1;
+        if (pd_dist(x) == 0) {
+            if (cnt[v] == 0) lv = lev[v];
+        } else {
+            int r = pd_parent(x);
+            if (pd_dist(pd[r]) == 0 && cnt[r] == 0) lv = lev[r] + pd_dist(x);
+        }
+        level[v] = lv;
+        if (lv < 0) ++unres;
+        mx = max(mx, lv);
+    }
+    unres = __reduce_add_sync(0xffffffffu, unres);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (unres) atomicAdd(sc + SC_UNRES, unres);
+        atomicMax(sc + SC_MAXLV, mx);
+    }
+}
+
+__global__ void k_set_scalars(int32_t *sc) {
+    if (threadIdx.x < 16) sc[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sc[SC_MAXLV] = -1;
+}
+
+// Persistent cooperative grid: at most `cap` CTAs per SM (fewer CTAs = cheaper
+// grid barrier; the per-round work of these loops is small).
+int coop_grid(const void *func, int block, int sms, int cap = 2) {
+    int per_sm = 0;
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, block, 0));
+    if (per_sm < 1) fail(HF_ERR_CUDA, "cooperative kernel cannot be resident");
+    return std::min(per_sm, cap) * sms;
+}
+
+}  // namespace
+
+// Returns the number of never-ready nodes (0 on success); fills g.level/order/level_ptr.
+int64_t levelize_device(Graph &g) {
+    cudaStream_t s = g.stream;
+    const int32_t n = g.n, m = g.m;
+    g.levelized = false;
+    g.L = -1;
+    g.level.alloc(sizeof(int32_t) * int64_t(n > 0 ? n : 1), s);
+    g.order.alloc(sizeof(int32_t) * int64_t(n > 0 ? n : 1), s);
+    g.level_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    if (n == 0) {
+        HF_CUDA(cudaMemsetAsync(g.level_ptr.p, 0, sizeof(int32_t), s));
+        g.h_level_ptr.assign(1, 0);
+        g.L = 0;
+        g.max_level_width = 0;
+        g.levelized = true;
+        HF_CUDA(cudaStreamSynchronize(s));
+        return 0;
+    }
+    DevBuf pd, cnt, lev, la, lb, bar, keys, skeys, ceid, cptr;
+    pd.alloc(sizeof(long long) * n, s);
+    cnt.alloc(sizeof(int32_t) * n, s);
+    lev.alloc(sizeof(int32_t) * n, s);
+    la.alloc(sizeof(int32_t) * n, s);
+    lb.alloc(sizeof(int32_t) * n, s);
+    bar.alloc(sizeof(GridBar), s);
+    HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), s));
+    int32_t *sc = g.d_scalars();
+    k_set_scalars<<<1, 32, 0, s>>>(sc);
+    HF_CHECK_LAUNCH();
+    // frontier list F0 goes to `lb` (separate from the active list in `la`)
+    k_lev_init<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+        g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), n, pd.as<long long>(),
+        cnt.as<int32_t>(), lev.as<int32_t>(), la.as<int32_t>(), lb.as<int32_t>(), sc);
+    HF_CHECK_LAUNCH();
+    g.launches += 2;
+    {
+        // pointer jumping: lists la (active) / keys buffer as ping-pong partner
+        DevBuf act2;
+        act2.alloc(sizeof(int32_t) * n, s);
+        int max_rounds = bits_for(n) + 2;
+        const int block = 512;
+        int grid = coop_grid((const void *)k_lev_jump, block, g.sms);
+        long long *pdp = pd.as<long long>();
+        int32_t *a = la.as<int32_t>(), *b = act2.as<int32_t>();
+        GridBar *barp = bar.as<GridBar>();
+        void *args[] = {&pdp, &a, &b, &sc, &max_rounds, &barp};
+        HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_jump, grid, block, args, 0, s));
+        g.launches += 1;
+    }
+    // contracted fan-out of the junctions: stable sort of fan-in edges by root key
+    keys.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+    skeys.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+    ceid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+    cptr.alloc(sizeof(int32_t) * (int64_t(n) + 2), s);
+    if (m) {
+        k_lev_ckeys<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+            g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
+            pd.as<long long>(), n, m, keys.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+        radix_sort_pairs(keys.as<int32_t>(), nullptr, skeys.as<int32_t>(), ceid.as<int32_t>(), m,
+                         bits_for(n), s, g);
+    }
+    keys_to_ptr(skeys.as<int32_t>(), m, n + 1, cptr.as<int32_t>(), s, g);
+    {
+        const int block = 512;
+        int grid = coop_grid((const void *)k_lev_kahn, block, g.sms);
+        HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), s));
+        const int32_t *cp = cptr.as<int32_t>(), *ce = ceid.as<int32_t>();
+        const int32_t *isrc = g.in_src.as<int32_t>(), *idst = g.in_dst.as<int32_t>();
+        const long long *pdp = pd.as<long long>();
+        int32_t *cn = cnt.as<int32_t>(), *lv = lev.as<int32_t>();
+        int32_t *fa = lb.as<int32_t>(), *fb = la.as<int32_t>();
+        GridBar *barp = bar.as<GridBar>();
+        void *args[] = {&cp, &ce, &isrc, &idst, &pdp, &cn, &lv, &fa, &fb, &sc, &barp};
+        HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn, grid, block, args, 0, s));
+        g.launches += 1;
+    }
+    k_lev_final<<<grid_for(n, 256, g.sms), 256, 0, s>>>(pd.as<long long>(), cnt.as<int32_t>(),
+                                                        lev.as<int32_t>(), n,
+                                                        g.level.as<int32_t>(), sc);
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
+    int32_t h_sc[16];
+    HF_CUDA(cudaMemcpyAsync(h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaStreamSynchronize(s));
+    int64_t unresolved = h_sc[SC_UNRES];
+    if (unresolved) return unresolved;
+    const int32_t L = h_sc[SC_MAXLV] + 1;
+    // canonical order: ids stably sorted by level
+    skeys.alloc(sizeof(int32_t) * n, s);
+    radix_sort_pairs(g.level.as<int32_t>(), nullptr, skeys.as<int32_t>(), g.order.as<int32_t>(),
+                     n, bits_for(int64_t(L) - 1), s, g);
+    keys_to_ptr(skeys.as<int32_t>(), n, L, g.level_ptr.as<int32_t>(), s, g);
+    g.h_level_ptr.resize(size_t(L) + 1);
+    HF_CUDA(cudaMemcpyAsync(g.h_level_ptr.data(), g.level_ptr.p, sizeof(int32_t) * (L + 1),
+                            cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaStreamSynchronize(s));
+    int32_t w = 0;
+    for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
+    g.max_level_width = w;
+    g.L = L;
+    g.levelized = true;
+    return 0;
+}
+
+}  // namespace hf

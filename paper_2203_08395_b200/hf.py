@@ -1,0 +1,269 @@
+"""Thin ctypes binding of libhf.so (include/hf.h).  Argument marshalling only:
+every step of the path runs in the library's CUDA kernels.
+
+Each ``hf_*`` function here has the name of the C entry point it calls.  Arrays
+may be numpy arrays (host-pointer variant, synchronous) or CUDA torch tensors
+(``_d`` variant on the graph's stream); the two cannot be mixed in one call.
+There is no CPU fallback: if libhf.so is missing or fails to load, importing
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhf.so")
+
+HF_OK, HF_ERR_INVALID_ARG, HF_ERR_BAD_CSR, HF_ERR_CYCLE = 0, 1, 2, 3
+HF_ERR_NOT_LEVELIZED, HF_ERR_OOM, HF_ERR_CUDA, HF_ERR_NCCL = 4, 5, 6, 7
+HF_LAYOUT_SM, HF_LAYOUT_MS = 0, 1
+
+# every exported entry point of include/hf.h (checked by tests/test_abi.py)
+EXPORTS = [
+    "hf_last_error", "hf_status_string", "hf_version", "hf_graph_create", "hf_graph_create_d",
+    "hf_graph_destroy", "hf_graph_set_stream", "hf_graph_info", "hf_sync", "hf_levelize",
+    "hf_levelize_d", "hf_propagate_forward", "hf_propagate_forward_d", "hf_propagate_backward",
+    "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
+    "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
+]
+
+
+class HFError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        super().__init__(f"{_status_name(status)}: {message}")
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2203_08395_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P, i32, i64, f32, c_int = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float,
+                               ctypes.c_int)
+    sig = {
+        "hf_last_error": (ctypes.c_char_p, []),
+        "hf_status_string": (ctypes.c_char_p, [c_int]),
+        "hf_version": (c_int, []),
+        "hf_graph_create": (c_int, [i32, i32, P, P, P, P, P, c_int, P, P]),
+        "hf_graph_create_d": (c_int, [i32, i32, P, P, P, P, P, c_int, P, P]),
+        "hf_graph_destroy": (c_int, [P]),
+        "hf_graph_set_stream": (c_int, [P, P]),
+        "hf_graph_info": (c_int, [P, P, P, P]),
+        "hf_sync": (c_int, [P]),
+        "hf_levelize": (c_int, [P, P, P, P, P]),
+        "hf_levelize_d": (c_int, [P, P, P, P, P]),
+        "hf_propagate_forward": (c_int, [P, P, P]),
+        "hf_propagate_forward_d": (c_int, [P, P, P]),
+        "hf_propagate_backward": (c_int, [P, f32, P, P, P, P]),
+        "hf_propagate_backward_d": (c_int, [P, f32, P, P, P, P]),
+        "hf_run_batch": (c_int, [P, i32, P, c_int, P, P, P, P, P]),
+        "hf_run_batch_d": (c_int, [P, i32, P, c_int, P, P, P, P, P, P, P]),
+        "hf_nccl_unique_id": (c_int, [P]),
+        "hf_nccl_comm_init": (c_int, [P, c_int, c_int, c_int, P]),
+        "hf_nccl_comm_destroy": (c_int, [P]),
+        "hf_profile_enable": (c_int, [P, c_int]),
+        "hf_profile_read": (c_int, [P, P, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def _status_name(s: int) -> str:
+    return _lib.hf_status_string(s).decode()
+
+
+def _check(status: int):
+    if status != HF_OK:
+        raise HFError(status, _lib.hf_last_error().decode())
+
+
+def _is_torch(x) -> bool:
+    return x is not None and type(x).__module__.startswith("torch")
+
+
+def _ptr(x):
+    """Pointer of a numpy array / CUDA torch tensor (None -> NULL)."""
+    if x is None:
+        return None
+    if _is_torch(x):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if not x.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+def _np(x, dtype):
+    return None if x is None else np.ascontiguousarray(x, dtype=dtype)
+
+
+def _stream_of(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)   # torch.cuda.Stream
+
+
+class Graph:
+    """Owning handle of an hf_graph (destroyed with the object)."""
+
+    def __init__(self, handle: ctypes.c_void_p, n: int, m: int, device: int):
+        self._h = handle
+        self.n, self.m, self.device = n, m, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            hf_graph_destroy(self)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def num_levels(self) -> int:
+        return hf_graph_info(self)[2]
+
+
+def hf_graph_create(n, m, fanin_ptr, fanin_src, fanout_ptr=None, fanout_dst=None, delay=None,
+                    device: int = 0, stream=None) -> Graph:
+    out = ctypes.c_void_p()
+    if _is_torch(fanin_ptr):
+        st = _lib.hf_graph_create_d(n, m, _ptr(fanin_ptr), _ptr(fanin_src), _ptr(fanout_ptr),
+                                    _ptr(fanout_dst), _ptr(delay), device, _stream_of(stream),
+                                    ctypes.byref(out))
+    else:
+        a = [_np(fanin_ptr, np.int32), _np(fanin_src, np.int32), _np(fanout_ptr, np.int32),
+             _np(fanout_dst, np.int32), _np(delay, np.float32)]
+        st = _lib.hf_graph_create(n, m, *[_ptr(x) for x in a], device, _stream_of(stream),
+                                  ctypes.byref(out))
+    _check(st)
+    return Graph(out, n, m, device)
+
+
+def hf_graph_destroy(g: Graph):
+    _check(_lib.hf_graph_destroy(g.handle))
+
+
+def hf_graph_set_stream(g: Graph, stream):
+    _check(_lib.hf_graph_set_stream(g.handle, _stream_of(stream)))
+
+
+def hf_graph_info(g: Graph):
+    n, m, L = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(_lib.hf_graph_info(g.handle, ctypes.byref(n), ctypes.byref(m), ctypes.byref(L)))
+    return n.value, m.value, L.value
+
+
+def hf_sync(g: Graph):
+    _check(_lib.hf_sync(g.handle))
+
+
+def hf_levelize(g: Graph, level=None, level_ptr=None, order=None) -> int:
+    """Levelize; optional outputs are filled in place (numpy => host variant,
+    torch CUDA => device variant).  Returns L."""
+    L = ctypes.c_int32()
+    if any(_is_torch(x) for x in (level, level_ptr, order)):
+        _check(_lib.hf_levelize_d(g.handle, ctypes.byref(L), _ptr(level), _ptr(level_ptr),
+                                  _ptr(order)))
+    else:
+        _check(_lib.hf_levelize(g.handle, ctypes.byref(L), _ptr(level), _ptr(level_ptr),
+                                _ptr(order)))
+    return L.value
+
+
+def levelize_np(g: Graph):
+    """Convenience: (L, level, level_ptr, order) as numpy arrays."""
+    level = np.zeros(max(g.n, 1), np.int32)
+    lptr = np.zeros(g.n + 1, np.int32)
+    order = np.zeros(max(g.n, 1), np.int32)
+    L = hf_levelize(g, level, lptr, order)
+    return L, level[:g.n], lptr[:L + 1], order[:g.n]
+
+
+def hf_propagate_forward(g: Graph, at_src, at):
+    if _is_torch(at):
+        _check(_lib.hf_propagate_forward_d(g.handle, _ptr(at_src), _ptr(at)))
+    else:
+        a = _np(at_src, np.float32)
+        _check(_lib.hf_propagate_forward(g.handle, _ptr(a), _ptr(at)))
+
+
+def hf_propagate_backward(g: Graph, t_req: float, at, rat, slack=None, wns=None):
+    """wns: 1-element output (numpy float32 array or CUDA tensor) or None."""
+    if _is_torch(rat):
+        _check(_lib.hf_propagate_backward_d(g.handle, ctypes.c_float(t_req), _ptr(at), _ptr(rat),
+                                            _ptr(slack), _ptr(wns)))
+    else:
+        a = _np(at, np.float32)
+        _check(_lib.hf_propagate_backward(g.handle, ctypes.c_float(t_req), _ptr(a), _ptr(rat),
+                                          _ptr(slack), _ptr(wns)))
+
+
+def hf_run_batch(g: Graph, s_local: int, delays, layout: int, t_req, at_src, wns_local,
+                 nccl_comm=None, wns_all=None, at=None, rat=None):
+    if _is_torch(delays):
+        _check(_lib.hf_run_batch_d(g.handle, s_local, _ptr(delays), layout, _ptr(t_req),
+                                   _ptr(at_src), _ptr(wns_local), _ptr(at), _ptr(rat),
+                                   nccl_comm, _ptr(wns_all)))
+    else:
+        if at is not None or rat is not None:
+            raise ValueError("at/rat outputs are only available with device tensors")
+        d = _np(delays, np.float32)
+        t = _np(t_req, np.float32)
+        a = _np(at_src, np.float32)
+        _check(_lib.hf_run_batch(g.handle, s_local, _ptr(d), layout, _ptr(t), _ptr(a),
+                                 _ptr(wns_local), nccl_comm, _ptr(wns_all)))
+
+
+def hf_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.hf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def hf_nccl_comm_init(uid: bytes, rank: int, nranks: int, device: int) -> ctypes.c_void_p:
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    comm = ctypes.c_void_p()
+    _check(_lib.hf_nccl_comm_init(buf, rank, nranks, device, ctypes.byref(comm)))
+    return comm
+
+
+def hf_nccl_comm_destroy(comm):
+    _check(_lib.hf_nccl_comm_destroy(comm))
+
+
+def hf_profile_enable(g: Graph, on: bool = True):
+    _check(_lib.hf_profile_enable(g.handle, 1 if on else 0))
+
+
+def hf_profile_read(g: Graph):
+    """(ms_levelize, ms_forward, ms_backward, kernel_launches)"""
+    a, b, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+    k = ctypes.c_int64()
+    _check(_lib.hf_profile_read(g.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                ctypes.byref(k)))
+    return a.value, b.value, c.value, k.value
+
+
+def hf_version() -> int:
+    return _lib.hf_version()

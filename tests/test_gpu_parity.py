@@ -1,0 +1,331 @@
+"""GPU parity: libhf.so (through the C ABI) vs the CPU oracle, element by element.
+
+Bar (BASELINE.json:5): level / level_ptr / order exact; at, rat,
+slack, wns 0 ULP (compared as uint32 bit patterns).  Sizes span several tiles and
+ragged tails; full BASELINE sizes are covered with all outputs compared (the C
+oracle finishes them in seconds).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import hfgen
+import oracle
+from helpers import csr_from_edges, load_golden, mixed_delays, random_tiny_dag, reach_from_cycles
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+
+
+@pytest.fixture(scope="module")
+def hf():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2203_08395_b200 import build
+    build.build()
+    from paper_2203_08395_b200 import hf as _hf
+    return _hf
+
+
+def bits(x):
+    return np.ascontiguousarray(x, dtype=F32).view(np.uint32)
+
+
+def assert_bits_equal(a, b, what=""):
+    a, b = np.asarray(a, F32), np.asarray(b, F32)
+    assert a.shape == b.shape, what
+    nan = np.isnan(a) & np.isnan(b)
+    diff = (bits(a) != bits(b)) & ~nan
+    if diff.any():
+        i = np.argwhere(diff)[0]
+        raise AssertionError(f"{what}: {diff.sum()} mismatches, first at {tuple(i)}: "
+                             f"gpu={a[tuple(i)]!r} oracle={b[tuple(i)]!r}")
+
+
+def gpu_single(hf, g_in_ptr, g_in_src, n, m, delay, at_src, T, fanout=None):
+    kw = {}
+    if fanout is not None:
+        kw = dict(fanout_ptr=fanout[0], fanout_dst=fanout[1])
+    G = hf.hf_graph_create(n, m, g_in_ptr, g_in_src, delay=delay, **kw)
+    L, level, lptr, order = hf.levelize_np(G)
+    at = np.zeros(max(n, 1), F32)
+    hf.hf_propagate_forward(G, at_src, at)
+    rat = np.zeros(max(n, 1), F32)
+    slack = np.zeros(max(n, 1), F32)
+    wns = np.zeros(1, F32)
+    hf.hf_propagate_backward(G, T, at[:n], rat, slack, wns)
+    G.close()
+    return L, level, lptr, order, at[:n], rat[:n], slack[:n], wns[0]
+
+
+def check_single(hf, n, m, in_ptr, in_src, delay, at_src, T, fanout=None):
+    L, level, lptr, order, at, rat, slack, wns = gpu_single(hf, in_ptr, in_src, n, m, delay,
+                                                            at_src, T, fanout)
+    lv = oracle.levelize(n, m, in_ptr, in_src)
+    assert L == lv.num_levels
+    assert np.array_equal(level, lv.level)
+    assert np.array_equal(lptr, lv.level_ptr)
+    assert np.array_equal(order, lv.order)
+    at_o = oracle.forward(n, m, in_ptr, in_src, delay, at_src, lv)
+    assert_bits_equal(at, at_o, "at")
+    rat_o, slack_o, wns_o = oracle.backward(n, m, in_ptr, in_src, delay, T, at_o, lv)
+    assert_bits_equal(rat, rat_o, "rat")
+    assert_bits_equal(slack, slack_o, "slack")
+    assert_bits_equal(wns, wns_o, "wns")
+
+
+# ---- the paper's worked graphs ------------------------------------------------
+@pytest.mark.parametrize("fname", ["fig1_saxpy.txt", "fig5_dependency.txt"])
+def test_golden_graphs(hf, fname):
+    g = load_golden(fname)
+    in_ptr, in_src, _ = csr_from_edges(g["n"], g["edge"])
+    G = hf.hf_graph_create(g["n"], len(g["edge"]), in_ptr, in_src)
+    L, level, lptr, order = hf.levelize_np(G)
+    assert L == g["num_levels"]
+    assert level.tolist() == g["level"]
+    assert lptr.tolist() == g["level_ptr"]
+    assert order.tolist() == g["order"]
+
+
+# ---- configs at parity sizes and at full size ----------------------------------
+@pytest.mark.parametrize("name,scale", [
+    ("C1", 1.0), ("C3", 0.003), ("C3", 0.05), ("C2-random", 0.003), ("C5", 0.0005),
+    ("C5", 0.01),
+])
+def test_config_single(hf, name, scale):
+    g = hfgen.config(name, scale)
+    check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req)
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_config_single_full(hf, name):
+    g = hfgen.config(name)
+    check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req)
+
+
+@pytest.mark.parametrize("name", ["C2-chain", "C2-tree", "C2-random"])
+def test_c2_levelize_full(hf, name):
+    g = hfgen.config(name)
+    G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=np.ones(g.m, F32))
+    L, level, lptr, order = hf.levelize_np(G)
+    lv = oracle.levelize(g.n, g.m, g.in_ptr, g.in_src)
+    assert L == lv.num_levels
+    assert np.array_equal(level, lv.level)
+    assert np.array_equal(lptr, lv.level_ptr)
+    assert np.array_equal(order, lv.order)
+    if g.level_label is not None:
+        assert np.array_equal(level, g.level_label)
+    # unit-delay forward: at == level exactly (P3)
+    at = np.zeros(g.n, F32)
+    hf.hf_propagate_forward(G, np.zeros(g.n, F32), at)
+    assert np.array_equal(at, level.astype(F32))
+
+
+# ---- tiny random DAGs, mixed-sign / mixed-magnitude delays, multi-edges --------
+def test_tiny_random_dags(hf):
+    rng = np.random.default_rng(100)
+    for trial in range(150):
+        n, edges = random_tiny_dag(rng, nmax=12)
+        m = len(edges)
+        d = mixed_delays(rng, m)
+        in_ptr, in_src, perm = csr_from_edges(n, edges)
+        at_src = mixed_delays(rng, n)
+        T = float(mixed_delays(rng, 1)[0])
+        check_single(hf, n, m, in_ptr, in_src, d[perm], at_src, T)
+
+
+def test_cycles_reported_with_unready_count(hf):
+    rng = np.random.default_rng(5)
+    seen = 0
+    for trial in range(60):
+        n, edges = random_tiny_dag(rng, nmax=10)
+        if n < 2:
+            continue
+        edges.append((int(rng.integers(0, n)), int(rng.integers(0, n))))
+        bad = reach_from_cycles(n, edges)
+        in_ptr, in_src, _ = csr_from_edges(n, edges)
+        G = hf.hf_graph_create(n, len(edges), in_ptr, in_src)
+        if bad.any():
+            seen += 1
+            with pytest.raises(hf.HFError) as ei:
+                hf.levelize_np(G)
+            assert ei.value.status == hf.HF_ERR_CYCLE
+            assert f"{int(bad.sum())} nodes never become ready" in str(ei.value)
+            with pytest.raises(hf.HFError) as ei:
+                hf.hf_propagate_forward(G, None, np.zeros(n, F32))
+            assert ei.value.status == hf.HF_ERR_NOT_LEVELIZED
+        else:
+            hf.levelize_np(G)
+    assert seen > 10
+
+
+def test_cycle_in_large_graph(hf):
+    g = hfgen.config("C3", 0.01)
+    src, dst = g.edges()
+    # back edge from a deep node to a shallow ancestor region + a long pure chain cycle
+    deep = int(np.argmax(g.level_label))
+    shallow = int(np.argmin(g.level_label))
+    edges = list(zip(src.tolist(), dst.tolist())) + [(deep, shallow)]
+    in_ptr, in_src, _ = csr_from_edges(g.n, edges)
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.levelize(g.n, len(edges), in_ptr, in_src)
+    G = hf.hf_graph_create(g.n, len(edges), in_ptr, in_src)
+    with pytest.raises(hf.HFError) as ei:
+        hf.levelize_np(G)
+    assert f"{eo.value.unready} nodes never become ready" in str(ei.value)
+    # pure in-degree-1 ring (pointer jumping must stop)
+    ring = [(i, (i + 1) % 5000) for i in range(5000)] + [(5000, 5001)]
+    ip, isrc, _ = csr_from_edges(5002, ring)
+    G = hf.hf_graph_create(5002, len(ring), ip, isrc)
+    with pytest.raises(hf.HFError) as ei:
+        hf.levelize_np(G)
+    assert "5000 nodes never become ready" in str(ei.value)
+
+
+# ---- edge cases -------------------------------------------------------------------
+def test_empty_graph(hf):
+    G = hf.hf_graph_create(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32))
+    L, level, lptr, order = hf.levelize_np(G)
+    assert L == 0 and lptr.tolist() == [0]
+    wns = np.zeros(1, F32)
+    hf.hf_propagate_backward(G, 1.0, np.zeros(0, F32), np.zeros(1, F32), None, wns)
+    assert np.isposinf(wns[0])
+
+
+def test_isolated_nodes_and_negative_zero(hf):
+    n = 1000
+    in_ptr = np.zeros(n + 1, np.int32)
+    at_src = np.where(np.arange(n) % 2 == 0, -0.0, np.arange(n)).astype(F32)
+    check_single(hf, n, 0, in_ptr, np.zeros(0, np.int32), None, at_src, -0.0)
+
+
+def test_multi_edges_hub_denormals(hf):
+    rng = np.random.default_rng(3)
+    n = 12_000
+    edges = [(u, n - 1) for u in range(10_000)]                # 10k fan-in hub
+    edges += [(0, 10_001)] * 5                                    # multi-edges
+    edges += [(n - 1, 10_002 + k) for k in range(1000)]          # 1k fan-out
+    m = len(edges)
+    d = mixed_delays(rng, m)
+    d[::7] = np.float32(1e-40)                                     # denormals
+    d[1::11] = np.float32(-3e-39)
+    d[2::13] = np.float32(-0.0)
+    in_ptr, in_src, perm = csr_from_edges(n, edges)
+    at_src = (mixed_delays(rng, n) * np.float32(1e-38)).astype(F32)   # denormal range
+    check_single(hf, n, m, in_ptr, in_src, d[perm], at_src, 1e-38)
+
+
+def test_invalid_inputs(hf):
+    ip, isrc, _ = csr_from_edges(3, [(0, 1), (1, 2)])
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_graph_create(3, 2, ip, isrc, delay=np.array([1, np.nan], F32))
+    assert ei.value.status == hf.HF_ERR_INVALID_ARG
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_graph_create(3, 2, ip, np.array([0, 3], np.int32))
+    assert ei.value.status == hf.HF_ERR_BAD_CSR
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_graph_create(3, 2, np.array([0, 2, 1, 2], np.int32), isrc)
+    assert ei.value.status == hf.HF_ERR_BAD_CSR
+    G = hf.hf_graph_create(3, 2, ip, isrc)
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_propagate_forward(G, None, np.zeros(3, F32))
+    assert ei.value.status == hf.HF_ERR_NOT_LEVELIZED
+    hf.levelize_np(G)
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_run_batch(G, 2, np.array([[1, 2], [np.inf, 1]], F32), hf.HF_LAYOUT_MS,
+                        np.ones(2, F32), None, np.zeros(2, F32))
+    assert ei.value.status == hf.HF_ERR_INVALID_ARG
+
+
+def test_caller_fanout_validated(hf):
+    g = hfgen.config("C1", 0.2)
+    op, od, oe = oracle.fanout(g.n, g.m, g.in_ptr, g.in_src)
+    od2 = od.copy()
+    rng = np.random.default_rng(1)
+    for u in range(g.n):
+        rng.shuffle(od2[op[u]:op[u + 1]])
+    check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req, (op, od2))
+    od3 = od2.copy()
+    k = int(np.nonzero(np.diff(op))[0][3])
+    od3[op[k]] = (od3[op[k]] + 1) % g.n
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, op, od3, g.delay)
+    assert ei.value.status == hf.HF_ERR_BAD_CSR
+
+
+# ---- batched scenarios ---------------------------------------------------------------
+def gpu_batch_device(hf, g, D_ms, T, s_local, want_at_rat=True):
+    import torch
+    dev = torch.device("cuda:0")
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_levelize(G)
+    d = torch.from_numpy(np.ascontiguousarray(D_ms)).to(dev)
+    t = torch.from_numpy(np.asarray(T, F32)).to(dev)
+    a = torch.from_numpy(g.at_src).to(dev)
+    w = torch.empty(s_local, dtype=torch.float32, device=dev)
+    at = torch.empty(g.n * s_local, dtype=torch.float32, device=dev) if want_at_rat else None
+    rat = torch.empty(g.n * s_local, dtype=torch.float32, device=dev) if want_at_rat else None
+    hf.hf_run_batch(G, s_local, d, hf.HF_LAYOUT_MS, t, a, w, at=at, rat=rat)
+    hf.hf_sync(G)
+    out = (w.cpu().numpy(),
+           at.cpu().numpy().reshape(g.n, s_local) if want_at_rat else None,
+           rat.cpu().numpy().reshape(g.n, s_local) if want_at_rat else None)
+    G.close()
+    return out
+
+
+@pytest.mark.parametrize("S", [1, 2, 3, 8, 64])
+def test_batch_small(hf, S):
+    g = hfgen.config("C3", 0.004)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[::2] -= 3.5
+    w, at, rat = gpu_batch_device(hf, g, D, T, S)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                                 want_at_rat=True)
+    assert_bits_equal(at, ato, "at")
+    assert_bits_equal(rat, rato, "rat")
+    assert_bits_equal(w, wo, "wns")
+
+
+def test_batch_host_api_both_layouts(hf):
+    g = hfgen.config("C1")
+    S = 6
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4)
+    G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=g.delay)
+    hf.levelize_np(G)
+    for layout, arr in ((hf.HF_LAYOUT_MS, D), (hf.HF_LAYOUT_SM, np.ascontiguousarray(D.T))):
+        w = np.zeros(S, F32)
+        hf.hf_run_batch(G, S, arr, layout, T, g.at_src, w)
+        assert_bits_equal(w, wo, f"wns layout {layout}")
+
+
+def test_batch_full_c4_and_shard_invariance(hf):
+    """C4 at full size: all 64 worst slacks exact; at/rat exact for every scenario
+    of two sampled columns; sharding into G = 2, 4, 8 blocks is bit-identical."""
+    g = hfgen.config("C4")
+    S = 64
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    w, at, rat = gpu_batch_device(hf, g, D, T, S)
+    wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms",
+                      threads=os.cpu_count() or 1)
+    assert_bits_equal(w, wo, "wns")
+    for s in (0, 37):
+        _, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, np.ascontiguousarray(D[:, s:s + 1]),
+                                    T[s:s + 1], g.at_src, "ms", want_at_rat=True)
+        assert_bits_equal(at[:, s], ato[:, 0], f"at[:, {s}]")
+        assert_bits_equal(rat[:, s], rato[:, 0], f"rat[:, {s}]")
+    for G_ in (2, 4, 8):
+        parts = []
+        for r in range(G_):
+            lo, hi = r * S // G_, (r + 1) * S // G_
+            parts.append(gpu_batch_device(hf, g, np.ascontiguousarray(D[:, lo:hi]), T[lo:hi],
+                                          hi - lo, want_at_rat=False)[0])
+        assert_bits_equal(np.concatenate(parts), w, f"shards G={G_}")
