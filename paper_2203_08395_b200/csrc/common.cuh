@@ -83,8 +83,14 @@ struct Graph {
     DevBuf level, level_ptr, order;
     std::vector<int32_t> h_level_ptr;
     int32_t max_level_width = 0;
+    // level-ordered ("relabelled") CSR for the propagation passes: row i is node
+    // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
+    DevBuf lo_in_ptr, lo_in_src, lo_in_eid, lo_out_ptr, lo_out_dst, lo_out_eid;
+    // chunk schedule of the persistent propagation kernel (cached per `slots`)
+    DevBuf chunk_ptr;
+    int32_t chunk_slots = -1, total_chunks = 0;
     // batch workspace (at / rat when the caller does not want them), grows on demand
-    DevBuf ws_at, ws_rat;
+    DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // small device scalars: [0] error bits, [1..] scratch
     DevBuf d_small;
     uint32_t *d_err() const { return d_small.as<uint32_t>(); }

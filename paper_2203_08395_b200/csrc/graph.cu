@@ -46,11 +46,24 @@ __global__ void k_check_fanout(const int32_t *__restrict__ ptr, const int32_t *_
     if (bits) atomicOr(err, bits);
 }
 
-__global__ void k_gather(const int32_t *__restrict__ idx, const int32_t *__restrict__ from,
-                         int32_t *__restrict__ to, int64_t count) {
+__global__ void k_count_keys(const int32_t *__restrict__ keys, int64_t count,
+                             int32_t *__restrict__ cnt) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
          i += int64_t(gridDim.x) * blockDim.x)
-        to[i] = from[idx[i]];
+        atomicAdd(cnt + keys[i], 1);
+}
+
+__global__ void k_scatter_fanout(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                 int64_t m, const int32_t *__restrict__ out_ptr,
+                                 int32_t *__restrict__ cur, int32_t *__restrict__ out_dst,
+                                 int32_t *__restrict__ out_eid) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int u = src[e];
+        int k = out_ptr[u] + atomicAdd(cur + u, 1);
+        out_dst[k] = dst[e];
+        out_eid[k] = int(e);
+    }
 }
 
 __global__ void k_compare(const int32_t *__restrict__ a, const int32_t *__restrict__ b,
@@ -104,17 +117,25 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
                                            : "fan-in src out of range [0, n)");
     if (e & ERR_NONFINITE) fail(HF_ERR_INVALID_ARG, "delay contains NaN or inf");
 
-    // fan-out: stable sort of fan-in edges by source (key = src, value = edge id)
+    // fan-out: counting sort of the fan-in edges by source (atomic cursors; the
+    // order inside a fan-out row is irrelevant: min is exact and commutative)
     csr_row_ids(g.in_ptr.as<int32_t>(), n, g.in_dst.as<int32_t>(), s, g);
     {
-        DevBuf keys;
-        keys.alloc(sizeof(int32_t) * int64_t(m), s);
-        radix_sort_pairs(g.in_src.as<int32_t>(), nullptr, keys.as<int32_t>(),
-                         g.out_eid.as<int32_t>(), m, bits_for(int64_t(n) - 1), s, g);
-        keys_to_ptr(keys.as<int32_t>(), m, n, g.out_ptr.as<int32_t>(), s, g);
+        DevBuf cur;
+        cur.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        HF_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
         if (m) {
-            k_gather<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
-                g.out_eid.as<int32_t>(), g.in_dst.as<int32_t>(), g.out_dst.as<int32_t>(), m);
+            k_count_keys<<<grid_for(m, 256, g.sms), 256, 0, s>>>(g.in_src.as<int32_t>(), m,
+                                                               cur.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            g.launches += 1;
+        }
+        scan_exclusive(cur.as<int32_t>(), g.out_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+        HF_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
+        if (m) {
+            k_scatter_fanout<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+                g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(), m, g.out_ptr.as<int32_t>(),
+                cur.as<int32_t>(), g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
             g.launches += 1;
         }
@@ -150,14 +171,21 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
                          v1.as<int32_t>(), m, kb, s, g);   // by dst: (dst, src asc)
         radix_sort_pairs(v1.as<int32_t>(), k1.as<int32_t>(), k2.as<int32_t>(),
                          v2.as<int32_t>(), m, kb, s, g);   // by src: (src, dst asc)
-        // derived out rows are ascending in dst already (fan-in ids ascend with sink)
+        // canonical transpose of the fan-in: stable sort of edges (ascending id, so
+        // ascending sink) by source -> rows ascending in dst
+        DevBuf k3, v3, d3;
+        k3.alloc(sizeof(int32_t) * int64_t(m), s);
+        v3.alloc(sizeof(int32_t) * int64_t(m), s);
+        d3.alloc(sizeof(int32_t) * int64_t(m), s);
+        radix_sort_pairs(g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(), k3.as<int32_t>(),
+                         d3.as<int32_t>(), m, kb, s, g);
         int64_t cmp_n = int64_t(n) + 1;
         k_compare<<<grid_for(cmp_n, 256, g.sms), 256, 0, s>>>(
             cptr.as<int32_t>(), g.out_ptr.as<int32_t>(), cmp_n, g.d_err(), ERR_FO_PTR);
         HF_CHECK_LAUNCH();
         if (m) {
             k_compare<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
-                v2.as<int32_t>(), g.out_dst.as<int32_t>(), m, g.d_err(), ERR_FO_DST);
+                v2.as<int32_t>(), d3.as<int32_t>(), m, g.d_err(), ERR_FO_DST);
             HF_CHECK_LAUNCH();
         }
         g.launches += 2;

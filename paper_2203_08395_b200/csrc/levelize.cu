@@ -139,10 +139,10 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
     }
 }
 
-// Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w).
-__global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__restrict__ ceid,
-                           const int32_t *__restrict__ in_src, const int32_t *__restrict__ in_dst,
-                           const long long *__restrict__ pd, int32_t *__restrict__ cnt,
+// Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w) over the
+// contracted edges r -> j (cdst, cw), released by the atomic join counter cnt[j].
+__global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__restrict__ cdst,
+                           const int32_t *__restrict__ cw, int32_t *__restrict__ cnt,
                            int32_t *__restrict__ lev, int32_t *__restrict__ fr_a,
                            int32_t *__restrict__ fr_b, int32_t *sc, GridBar *bar) {
     const int lane = threadIdx.x & 31;
@@ -161,11 +161,11 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
         int32_t *out = lists[(r + 1) & 1];
         for (int64_t base = wid * 32; base < size; base += nwarps * 32) {
             int64_t i = base + lane;
-            int j = -1, deg = 0, start = 0, lj = 0;
+            int deg = 0, start = 0, lj = 0;
             if (i < size) {
-                j = __ldcg(in + i);
-                start = cptr[j];
-                deg = cptr[j + 1] - start;
+                int j = __ldcg(in + i);
+                start = __ldg(cptr + j);
+                deg = __ldg(cptr + j + 1) - start;
                 lj = __ldcg(lev + j);
             }
             int incl = deg;
@@ -176,6 +176,7 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
             }
             int excl = incl - deg;
             int total = __shfl_sync(0xffffffffu, incl, 31);
+            // edge-balanced expansion: lane idx handles the idx-th edge of the warp's rows
             for (int eb = 0; eb < total; eb += 32) {
                 int idx = eb + lane;
                 int lo = 0;
@@ -191,11 +192,9 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
                 bool ready = false;
                 int k = 0;
                 if (idx < total) {
-                    int e = ceid[o_start + (idx - o_excl)];
-                    k = in_dst[e];
-                    int p = in_src[e];
-                    int w = pd_dist(ld_pd(pd + p)) + 1;
-                    atomicMax(lev + k, o_lev + w);
+                    int c = o_start + (idx - o_excl);
+                    k = __ldg(cdst + c);
+                    atomicMax(lev + k, o_lev + __ldg(cw + c));
                     ready = atomicSub(cnt + k, 1) == 1;
                 }
                 warp_append(ready, k, out, sc + SC_FR + (r + 1) % 3);
@@ -205,22 +204,98 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
     }
 }
 
-// contracted-edge key of every fan-in edge e = (p -> j): r(p) if j is a junction
-// with indeg >= 2 and p resolved, else n (dropped)
-__global__ void k_lev_ckeys(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
-                            const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
-                            int32_t n, int32_t m, int32_t *__restrict__ keys) {
+// Contracted edges: every fan-in edge e = (p -> j) with j a junction of in-degree
+// >= 2 and p resolved becomes r(p) -> j with weight dist(p) + 1.  Counting sort by
+// r(p) (atomic cursors; order inside a row is irrelevant, max is commutative).
+__device__ __forceinline__ int contracted_root(const int32_t *in_ptr, const long long *pd,
+                                               int j, int p, int &w) {
+    if (in_ptr[j + 1] - in_ptr[j] < 2) return -1;
+    long long x = pd[p];
+    int r = pd_parent(x);
+    if (pd_dist(x) != 0 && pd_dist(pd[r]) != 0) return -1;   // p on/below a cycle
+    w = pd_dist(x) + 1;
+    return r;
+}
+
+__global__ void k_lev_ccount(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
+                             const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
+                             int32_t m, int32_t *__restrict__ ccnt) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
+        int w;
+        int r = contracted_root(in_ptr, pd, in_dst[e], in_src[e], w);
+        if (r >= 0) atomicAdd(ccnt + r, 1);
+    }
+}
+
+__global__ void k_lev_cscatter(const int32_t *__restrict__ in_ptr,
+                               const int32_t *__restrict__ in_src,
+                               const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
+                               int32_t m, const int32_t *__restrict__ cptr,
+                               int32_t *__restrict__ ccur, int32_t *__restrict__ cdst,
+                               int32_t *__restrict__ cw) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int w;
         int j = in_dst[e];
-        int deg = in_ptr[j + 1] - in_ptr[j];
-        int key = n;
-        if (deg >= 2) {
-            long long x = pd[in_src[e]];
-            int r = pd_parent(x);
-            if (pd_dist(x) == 0 || pd_dist(pd[r]) == 0) key = r;
+        int r = contracted_root(in_ptr, pd, j, in_src[e], w);
+        if (r >= 0) {
+            int k = cptr[r] + atomicAdd(ccur + r, 1);
+            cdst[k] = j;
+            cw[k] = w;
         }
-        keys[e] = key;
+    }
+}
+
+// Level-ordered CSR for the propagation passes: row i <-> node order[i].
+__global__ void k_relabel_deg(const int32_t *__restrict__ order, const int32_t *__restrict__ in_ptr,
+                              const int32_t *__restrict__ out_ptr, int32_t n,
+                              int32_t *__restrict__ din, int32_t *__restrict__ dout) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int v = order[i];
+        din[i] = in_ptr[v + 1] - in_ptr[v];
+        dout[i] = out_ptr[v + 1] - out_ptr[v];
+    }
+}
+
+// copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid;
+// eid_map == null -> the edge id is the source position itself
+__global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
+                               const int32_t *__restrict__ ptr, const int32_t *__restrict__ a,
+                               const int32_t *__restrict__ eid_map,
+                               const int32_t *__restrict__ nptr, int32_t *__restrict__ na,
+                               int32_t *__restrict__ neid) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps_total = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t wbase = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
+         wbase < n; wbase += nwarps_total * 32) {
+        int64_t i = wbase + lane;
+        int b = 0, e = 0, o = 0;
+        if (i < n) {
+            int v = order[i];
+            b = ptr[v];
+            e = ptr[v + 1];
+            o = nptr[i];
+        }
+        bool longrow = (e - b) >= 32;
+        if (!longrow)
+            for (int k = b; k < e; ++k) {
+                na[o + (k - b)] = a[k];
+                neid[o + (k - b)] = eid_map ? eid_map[k] : k;
+            }
+        unsigned lm = __ballot_sync(0xffffffffu, longrow);
+        while (lm) {
+            int srcl = __ffs(lm) - 1;
+            lm &= lm - 1;
+            int bb = __shfl_sync(0xffffffffu, b, srcl);
+            int ee = __shfl_sync(0xffffffffu, e, srcl);
+            int oo = __shfl_sync(0xffffffffu, o, srcl);
+            for (int k = bb + lane; k < ee; k += 32) {
+                na[oo + (k - bb)] = a[k];
+                neid[oo + (k - bb)] = eid_map ? eid_map[k] : k;
+            }
+        }
     }
 }
 
@@ -284,7 +359,7 @@ int64_t levelize_device(Graph &g) {
         HF_CUDA(cudaStreamSynchronize(s));
         return 0;
     }
-    DevBuf pd, cnt, lev, la, lb, bar, keys, skeys, ceid, cptr;
+    DevBuf pd, cnt, lev, la, lb, bar, skeys, cptr;
     pd.alloc(sizeof(long long) * n, s);
     cnt.alloc(sizeof(int32_t) * n, s);
     lev.alloc(sizeof(int32_t) * n, s);
@@ -306,8 +381,8 @@ int64_t levelize_device(Graph &g) {
         DevBuf act2;
         act2.alloc(sizeof(int32_t) * n, s);
         int max_rounds = bits_for(n) + 2;
-        const int block = 512;
-        int grid = coop_grid((const void *)k_lev_jump, block, g.sms);
+        const int block = 1024;
+        int grid = coop_grid((const void *)k_lev_jump, block, g.sms, 1);
         long long *pdp = pd.as<long long>();
         int32_t *a = la.as<int32_t>(), *b = act2.as<int32_t>();
         GridBar *barp = bar.as<GridBar>();
@@ -315,32 +390,39 @@ int64_t levelize_device(Graph &g) {
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_jump, grid, block, args, 0, s));
         g.launches += 1;
     }
-    // contracted fan-out of the junctions: stable sort of fan-in edges by root key
-    keys.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-    skeys.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-    ceid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-    cptr.alloc(sizeof(int32_t) * (int64_t(n) + 2), s);
+    // contracted fan-out of the junctions (counting sort by root)
+    DevBuf ccur, cdst, cw;
+    cptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    ccur.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    cdst.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+    cw.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+    HF_CUDA(cudaMemsetAsync(ccur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
     if (m) {
-        k_lev_ckeys<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+        k_lev_ccount<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
             g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
-            pd.as<long long>(), n, m, keys.as<int32_t>());
+            pd.as<long long>(), m, ccur.as<int32_t>());
         HF_CHECK_LAUNCH();
         g.launches += 1;
-        radix_sort_pairs(keys.as<int32_t>(), nullptr, skeys.as<int32_t>(), ceid.as<int32_t>(), m,
-                         bits_for(n), s, g);
     }
-    keys_to_ptr(skeys.as<int32_t>(), m, n + 1, cptr.as<int32_t>(), s, g);
+    scan_exclusive(ccur.as<int32_t>(), cptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    HF_CUDA(cudaMemsetAsync(ccur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
+    if (m) {
+        k_lev_cscatter<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+            g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
+            pd.as<long long>(), m, cptr.as<int32_t>(), ccur.as<int32_t>(), cdst.as<int32_t>(),
+            cw.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
     {
-        const int block = 512;
-        int grid = coop_grid((const void *)k_lev_kahn, block, g.sms);
+        const int block = 1024;
+        int grid = coop_grid((const void *)k_lev_kahn, block, g.sms, 1);
         HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), s));
-        const int32_t *cp = cptr.as<int32_t>(), *ce = ceid.as<int32_t>();
-        const int32_t *isrc = g.in_src.as<int32_t>(), *idst = g.in_dst.as<int32_t>();
-        const long long *pdp = pd.as<long long>();
+        const int32_t *cp = cptr.as<int32_t>(), *cd = cdst.as<int32_t>(), *cwp = cw.as<int32_t>();
         int32_t *cn = cnt.as<int32_t>(), *lv = lev.as<int32_t>();
         int32_t *fa = lb.as<int32_t>(), *fb = la.as<int32_t>();
         GridBar *barp = bar.as<GridBar>();
-        void *args[] = {&cp, &ce, &isrc, &idst, &pdp, &cn, &lv, &fa, &fb, &sc, &barp};
+        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &barp};
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn, grid, block, args, 0, s));
         g.launches += 1;
     }
@@ -367,6 +449,38 @@ int64_t levelize_device(Graph &g) {
     int32_t w = 0;
     for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
     g.max_level_width = w;
+    // relabel: level-ordered fan-in / fan-out CSR for the propagation passes (a4)
+    {
+        DevBuf din, dout;
+        din.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        dout.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        g.lo_in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        g.lo_out_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        g.lo_in_src.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+        g.lo_in_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+        g.lo_out_dst.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+        g.lo_out_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+        HF_CUDA(cudaMemsetAsync(din.as<int32_t>() + n, 0, sizeof(int32_t), s));
+        HF_CUDA(cudaMemsetAsync(dout.as<int32_t>() + n, 0, sizeof(int32_t), s));
+        k_relabel_deg<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            g.order.as<int32_t>(), g.in_ptr.as<int32_t>(), g.out_ptr.as<int32_t>(), n,
+            din.as<int32_t>(), dout.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        scan_exclusive(din.as<int32_t>(), g.lo_in_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+        scan_exclusive(dout.as<int32_t>(), g.lo_out_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s,
+                       g);
+        k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            g.order.as<int32_t>(), n, g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), nullptr,
+            g.lo_in_ptr.as<int32_t>(), g.lo_in_src.as<int32_t>(), g.lo_in_eid.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            g.order.as<int32_t>(), n, g.out_ptr.as<int32_t>(), g.out_dst.as<int32_t>(),
+            g.out_eid.as<int32_t>(), g.lo_out_ptr.as<int32_t>(), g.lo_out_dst.as<int32_t>(),
+            g.lo_out_eid.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 3;
+    }
+    g.chunk_slots = -1;   // chunk schedule depends on the levels
     g.L = L;
     g.levelized = true;
     return 0;
