@@ -86,9 +86,10 @@ struct Graph {
     // level-ordered ("relabelled") CSR for the propagation passes: row i is node
     // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
     DevBuf lo_in_ptr, lo_in_src, lo_in_eid, lo_out_ptr, lo_out_dst, lo_out_eid;
-    // chunk schedule of the persistent propagation kernel (cached per `slots`)
-    DevBuf chunk_ptr;
-    int32_t chunk_slots = -1, total_chunks = 0;
+    // chunk schedules of the persistent propagation kernels (per direction, cached
+    // per vslot target T): first position of every chunk, first chunk of every level
+    DevBuf sched_f_pos, sched_f_ptr, sched_b_pos, sched_b_ptr;
+    int32_t sched_f_C = 0, sched_f_T = -1, sched_b_C = 0, sched_b_T = -1;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // small device scalars: [0] error bits, [1..] scratch

@@ -480,7 +480,7 @@ int64_t levelize_device(Graph &g) {
         HF_CHECK_LAUNCH();
         g.launches += 3;
     }
-    g.chunk_slots = -1;   // chunk schedule depends on the levels
+    g.sched_f_T = g.sched_b_T = -1;   // chunk schedules depend on the levels
     g.L = L;
     g.levelized = true;
     return 0;

@@ -3,29 +3,33 @@
 // SURVEY.md §8(a) a5-a7; BASELINE.json:5.
 //
 // Data layout in HBM (scenario-minor): at[v*S + s], rat[v*S + s],
-// delays[e*S + s].  A node's S values are contiguous, so each fan-in/fan-out
-// edge touches S*4 contiguous bytes; a node is owned by LPN = S/V lanes, each
-// holding a V-wide vector (V = 4 -> LDG.128 / STG.128).  Pull-based: no float
-// atomics; every output is one fp32 max/min over fl(x +/- d) terms, which is
+// delays[e*S + s].  A node's S values are contiguous, so each edge touches S*4
+// contiguous bytes; a node-slice of Sg scenarios is owned by LPN = Sg/V lanes
+// holding V-wide vectors (V = 4 -> LDG.128 / STG.128).  Pull-based, no float
+// atomics: every output is one fp32 max/min over fl(x +/- d) terms, which is
 // order-independent (0 ULP against the oracle, reading R10).
 //
-// One persistent launch per pass (no per-level launches, no grid barrier):
-//   * the work is cut into chunks of `slots` consecutive nodes of one level, in
-//     level order (forward) or reverse level order (backward); CTAs claim chunks
-//     with an atomic ticket, so a CTA only ever waits on chunks with smaller
-//     tickets, which are held by running CTAs -> deadlock-free at any grid size;
-//   * a chunk of level k first PREFETCHES everything that does not depend on
-//     earlier levels (level-ordered CSR row, source ids, edge delays -- the bulk
-//     of the HBM traffic), THEN waits until level k-1 (k+1 backward) has
-//     published all its chunks (one acquire-poll of a per-level counter by one
-//     thread), then gathers at[u] / rat[v] from L2, reduces, stores, fences and
-//     bumps its level's counter (release).  Level k complete => all earlier
-//     levels complete, by induction;
-//   * a node whose degree exceeds the light-path limit is processed by the whole
-//     CTA (edges split across slots, shared-memory max/min reduction), so fan-in
-//     hubs (C5: 10k) and fan-out hubs (C3: ~700) do not serialise one lane;
-//   * backward keeps a per-lane running min of slack; one shared-memory reduction
-//     and one global atomicMin per scenario per CTA at the end give the WNS.
+// One persistent, warp-specialised launch per pass (no per-level launches, no
+// grid barrier):
+//   * Work = chunks of consecutive nodes of one level (level order forward,
+//     reverse level order backward), sized by "vslots" (a node of degree d needs
+//     ceil(d/PF) vslots of <= PF edges) so chunks are edge-balanced; hub nodes
+//     get a chunk of their own.  CTAs claim chunks with an atomic ticket; a chunk
+//     only waits on chunks with smaller tickets, held by running CTAs, so the
+//     schedule is deadlock-free at any grid size.
+//   * Producer warp: claims tickets up to NB chunks ahead, loads the chunk's
+//     level-ordered CSR rows, builds the vslot table and stages every edge's
+//     neighbour id and delay slice in shared memory with cp.async.bulk (TMA bulk
+//     copies, completion on an mbarrier).  None of this depends on earlier levels,
+//     so the HBM stream of delays runs ahead of the dependency front.
+//   * Consumer warps: wait for the stage (mbarrier), then for the previous level
+//     (one acquire-poll of its per-level chunk counter), gather at[u] / rat[v]
+//     from L2, reduce each vslot in registers, combine a node's vslots through
+//     shared memory, store, fence, and publish (release) the chunk.  Level k
+//     complete => all earlier levels complete, by induction.
+//   * Backward fuses slack = rat - at and keeps a per-lane running min; one
+//     shared-memory reduction and one global atomicMin per scenario per CTA give
+//     the worst slack.
 #include <algorithm>
 
 #include "common.cuh"
@@ -34,14 +38,17 @@ namespace hf {
 
 namespace {
 
-constexpr int BLOCK = 256;
-constexpr int PF = 4;   // edges per node prefetched into registers before the wait
+constexpr int NCW = 8;                     // consumer warps
+constexpr int NCT = NCW * 32;              // consumer threads
+constexpr int BLOCK = NCT + 32;            // + 1 producer warp
+constexpr int PF = 4;                      // edges per vslot
+constexpr int NB = 4;                      // pipeline stages
 
 template <int V> struct Vec {
     float x[V];
 };
 
-template <int V> __device__ __forceinline__ Vec<V> ldv_nc(const float *p) {   // read-only input
+template <int V> __device__ __forceinline__ Vec<V> ldv_g(const float *p) {   // read-only input
     Vec<V> r;
     if constexpr (V == 4) {
         float4 t = __ldg(reinterpret_cast<const float4 *>(p));
@@ -68,7 +75,29 @@ template <int V> __device__ __forceinline__ Vec<V> ldv_cg(const float *p) {
     }
     return r;
 }
-template <int V> __device__ __forceinline__ void stv(float *p, const Vec<V> &v) {
+template <int V> __device__ __forceinline__ Vec<V> ldv_s(const float *p) {   // shared
+    Vec<V> r;
+    if constexpr (V == 4) {
+        float4 t = *reinterpret_cast<const float4 *>(p);
+        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+    } else if constexpr (V == 2) {
+        float2 t = *reinterpret_cast<const float2 *>(p);
+        r.x[0] = t.x; r.x[1] = t.y;
+    } else {
+        r.x[0] = *p;
+    }
+    return r;
+}
+template <int V> __device__ __forceinline__ void stv_s(float *p, const Vec<V> &v) {
+    if constexpr (V == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
+    } else if constexpr (V == 2) {
+        *reinterpret_cast<float2 *>(p) = make_float2(v.x[0], v.x[1]);
+    } else {
+        *p = v.x[0];
+    }
+}
+template <int V> __device__ __forceinline__ void stv_g(float *p, const Vec<V> &v) {
     if constexpr (V == 4) {
         __stcg(reinterpret_cast<float4 *>(p), make_float4(v.x[0], v.x[1], v.x[2], v.x[3]));
     } else if constexpr (V == 2) {
@@ -78,10 +107,51 @@ template <int V> __device__ __forceinline__ void stv(float *p, const Vec<V> &v) 
     }
 }
 
+// ---- PTX helpers: acquire load, mbarrier, bulk copy, named barrier ----------
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {   // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
 }
 
 struct PassParams {
@@ -90,13 +160,12 @@ struct PassParams {
     const int32_t *nbr;        // [m] neighbour node id (fan-in src / fan-out dst)
     const int32_t *eid;        // [m] edge id (delay row)
     const int32_t *node_of;    // [n]
-    const int32_t *level_ptr;  // [L+1]
-    const int32_t *chunk_ptr;  // [L+1] chunks before level k (level order)
-    int32_t L;
-    int32_t total_chunks;
-    int32_t slots;             // nodes per chunk
-    int32_t lpn;               // lanes per node = S/V
-    int32_t S;                 // row stride of at/rat/delays (scenarios)
+    const int32_t *chunk_pos;  // [C+1] first position of every chunk (+ n)
+    const int32_t *chunk_ptr;  // [L+1] first chunk of every level
+    int32_t L, C, G;           // levels, chunks, scenario groups
+    int32_t T;                 // vslots per chunk target (= consumer slots)
+    int32_t ecap;              // staged edges per stage
+    int32_t S, Sg;             // row stride (scenarios), scenarios per group
     const float *d;            // [m][S]
     const float *src_val;      // forward: at_src [n] (or null); backward: t_req [S] (or null)
     float t_scalar;            // backward: T when t_req is null
@@ -104,10 +173,30 @@ struct PassParams {
     float *out;                // forward: at; backward: rat
     float *slack;              // backward, optional [n][S]
     int32_t *wns_ord;          // backward: [S] ordered-int mins
-    int32_t *done;             // [L] chunks published per level
+    int32_t *done;             // [G*L] chunks published per (group, level)
     int32_t *ticket;           // [1]
     uint32_t *err;
 };
+
+// per-stage shared-memory layout (offsets in bytes, computed identically on host)
+struct StageLayout {
+    int desc, node, rp, vb, vnode, nbr, d, bytes;
+};
+__host__ __device__ inline StageLayout stage_layout(int T, int ecap, int Sg) {
+    StageLayout L;
+    int o = 0;
+    L.desc = o;  o += 16 * 4;
+    L.node = o;  o += T * 4;
+    L.rp = o;    o += (T + 1) * 4;
+    L.vb = o;    o += (T + 1) * 4;
+    L.vnode = o; o += 2 * T * 4;
+    L.nbr = o;   o += ecap * 4;
+    o = (o + 15) & ~15;
+    L.d = o;     o += ecap * Sg * 4;
+    L.bytes = (o + 127) & ~127;
+    return L;
+}
+enum { D_T = 0, D_LV, D_G, D_POS, D_NN, D_RB, D_E, D_EST, D_NVS, D_HUB };
 
 template <bool FWD> __device__ __forceinline__ float combine(float best, float x) {
     return FWD ? fmaxf(best, x) : fminf(best, x);
@@ -115,208 +204,301 @@ template <bool FWD> __device__ __forceinline__ float combine(float best, float x
 template <bool FWD> __device__ __forceinline__ float relax(float a, float d) {
     return FWD ? __fadd_rn(a, d) : __fsub_rn(a, d);
 }
+template <bool FWD> __device__ __forceinline__ float ident() {
+    return __int_as_float(FWD ? 0xff800000 : 0x7f800000);   // -inf for max, +inf for min
+}
 
-template <int V, bool FWD, bool CHECK_D>
-__global__ void __launch_bounds__(BLOCK, 4) k_propagate(PassParams p) {
-    __shared__ int s_ticket;
-    __shared__ int s_heavy[BLOCK];
-    __shared__ int s_nheavy;
-    __shared__ float s_red[BLOCK * V];
-    extern __shared__ int32_t s_min[];   // backward: [S]
-
+template <int V, bool FWD, bool CHECK_D, bool BULK>
+__global__ void __launch_bounds__(BLOCK, 2) k_propagate(PassParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StageLayout SL = stage_layout(p.T, p.ecap, p.Sg);
+    const int lpn = p.Sg / V;                 // lanes per node slice
+    const int slots = NCT / lpn;              // vslots handled per round
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NB * SL.bytes);
+    uint64_t *empty = full + NB;
+    float *s_part = reinterpret_cast<float *>(smem + NB * SL.bytes + 2 * NB * 8);   // [2T][Sg]
+    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + 2 * p.T * p.Sg);           // [S]
     const int tid = threadIdx.x;
-    const int slot = tid / p.lpn;
-    const int lane = tid - slot * p.lpn;
-    const bool has_slot = slot < p.slots;
-    const int64_t col = int64_t(lane) * V;   // first scenario of this lane
-    const int light_max = 8 * PF;
+
+    if (tid == 0) {
+        for (int s = 0; s < NB; ++s) {
+            mbar_init(full + s, 32);
+            mbar_init(empty + s, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (!FWD)
+        for (int s = tid; s < p.S; s += BLOCK) s_min[s] = 0x7f800000;
+    __syncthreads();
+
+    if (tid >= NCT) {
+        // ============================ producer warp ============================
+        const int lane = tid - NCT;
+        int lv = FWD ? 0 : p.L - 1;
+        for (int i = 0;; ++i) {
+            const int st = i % NB;
+            mbar_wait(empty + st, ((i / NB) & 1) ^ 1);
+            unsigned char *sb = smem + st * SL.bytes;
+            int32_t *desc = reinterpret_cast<int32_t *>(sb + SL.desc);
+            int t = 0;
+            if (lane == 0) t = atomicAdd(p.ticket, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= p.C * p.G) {
+                if (lane == 0) desc[D_T] = -1;
+                mbar_arrive(full + st);
+                break;
+            }
+            const int g = t % p.G;
+            const int rank = FWD ? t / p.G : p.C - 1 - t / p.G;
+            if (FWD) {
+                while (__ldg(p.chunk_ptr + lv + 1) <= rank) ++lv;
+            } else {
+                while (__ldg(p.chunk_ptr + lv) > rank) --lv;
+            }
+            const int pos = __ldg(p.chunk_pos + rank);
+            const int nn = __ldg(p.chunk_pos + rank + 1) - pos;
+            int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
+            int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
+            int32_t *s_vb = reinterpret_cast<int32_t *>(sb + SL.vb);
+            int32_t *s_vnode = reinterpret_cast<int32_t *>(sb + SL.vnode);
+            int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
+            float *s_d = reinterpret_cast<float *>(sb + SL.d);
+            const int rb = __ldg(p.row_ptr + pos);
+            const int E = __ldg(p.row_ptr + pos + nn) - rb;
+            const bool hub = nn == 1 && (E + PF - 1) / PF > p.T;
+            // rows + vslot prefix (nodes are <= T)
+            int carry = 0;
+            for (int j0 = 0; j0 < nn; j0 += 32) {
+                const int j = j0 + lane;
+                int nv = 0;
+                if (j < nn) {
+                    s_node[j] = __ldg(p.node_of + pos + j);
+                    const int a = __ldg(p.row_ptr + pos + j) - rb;
+                    const int b = __ldg(p.row_ptr + pos + j + 1) - rb;
+                    s_rp[j] = a;
+                    nv = hub ? 0 : max(1, (b - a + PF - 1) / PF);
+                }
+                int incl = nv;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (j < nn) s_vb[j] = carry + incl - nv;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            const int nvs = hub ? 0 : carry;
+            if (lane == 0) {
+                s_rp[nn] = E;
+                s_vb[nn] = nvs;
+            }
+            __syncwarp();
+            if (!hub)
+                for (int j = lane; j < nn; j += 32)
+                    for (int v = s_vb[j]; v < s_vb[j + 1]; ++v) s_vnode[v] = j;
+            // stage neighbours + delay slices of the first est edges
+            const int est = min(E, p.ecap);
+            const int64_t col0 = int64_t(g) * p.Sg;
+            for (int e = lane; e < est; e += 32) {
+                s_nbr[e] = __ldg(p.nbr + rb + e);
+                const float *src = p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col0;
+                if (BULK) {
+                    bulk_g2s(s_d + int64_t(e) * p.Sg, src, uint32_t(p.Sg) * 4u, full + st);
+                } else {
+                    for (int c = 0; c < p.Sg; ++c) s_d[int64_t(e) * p.Sg + c] = __ldg(src + c);
+                }
+            }
+            if (lane == 0) {
+                desc[D_T] = t;
+                desc[D_LV] = lv;
+                desc[D_G] = g;
+                desc[D_POS] = pos;
+                desc[D_NN] = nn;
+                desc[D_RB] = rb;
+                desc[D_E] = E;
+                desc[D_EST] = est;
+                desc[D_NVS] = nvs;
+                desc[D_HUB] = hub;
+            }
+            __syncwarp();
+            if (BULK && lane == 0)
+                mbar_arrive_tx(full + st, uint32_t(est) * uint32_t(p.Sg) * 4u);
+            else
+                mbar_arrive(full + st);
+        }
+        return;
+    }
+
+    // ============================== consumer warps ==============================
+    const int slot = tid / lpn;
+    const int lane = tid - slot * lpn;
+    const bool has_slot = slot < slots;
     bool bad = false;
     Vec<V> run_min;
 #pragma unroll
-    for (int k = 0; k < V; ++k) run_min.x[k] = __int_as_float(0x7f800000);
-    if (!FWD) {
-        for (int s = tid; s < p.S; s += BLOCK) s_min[s] = 0x7f800000;
-    }
-    int lv = FWD ? 0 : p.L - 1;   // level cursor (monotone in ticket order)
+    for (int k = 0; k < V; ++k) run_min.x[k] = ident<false>();
 
-    for (;;) {
-        if (tid == 0) s_ticket = atomicAdd(p.ticket, 1);
-        if (tid == 0) s_nheavy = 0;
-        __syncthreads();
-        const int t = s_ticket;
-        if (t >= p.total_chunks) break;
-        // ticket -> (level, chunk in level); forward walks levels up, backward down
-        int rank;   // position of the chunk in level-order enumeration
-        if (FWD) {
-            rank = t;
-            while (__ldg(p.chunk_ptr + lv + 1) <= rank) ++lv;
-        } else {
-            rank = p.total_chunks - 1 - t;
-            while (__ldg(p.chunk_ptr + lv) > rank) --lv;
-        }
-        const int lbeg = __ldg(p.level_ptr + lv), lend = __ldg(p.level_ptr + lv + 1);
-        const int pos = lbeg + (rank - __ldg(p.chunk_ptr + lv)) * p.slots + slot;
-        const bool valid = has_slot && pos < lend;
+    for (int i = 0;; ++i) {
+        const int st = i % NB;
+        mbar_wait(full + st, (i / NB) & 1);
+        unsigned char *sb = smem + st * SL.bytes;
+        const int32_t *desc = reinterpret_cast<const int32_t *>(sb + SL.desc);
+        if (desc[D_T] < 0) break;
+        const int lv = desc[D_LV], g = desc[D_G], nn = desc[D_NN], rb = desc[D_RB];
+        const int E = desc[D_E], est = desc[D_EST], nvs = desc[D_NVS];
+        const bool hub = desc[D_HUB] != 0;
+        const int32_t *s_node = reinterpret_cast<const int32_t *>(sb + SL.node);
+        const int32_t *s_rp = reinterpret_cast<const int32_t *>(sb + SL.rp);
+        const int32_t *s_vb = reinterpret_cast<const int32_t *>(sb + SL.vb);
+        const int32_t *s_vnode = reinterpret_cast<const int32_t *>(sb + SL.vnode);
+        const int32_t *s_nbr = reinterpret_cast<const int32_t *>(sb + SL.nbr);
+        const float *s_d = reinterpret_cast<const float *>(sb + SL.d);
+        const int64_t col = int64_t(g) * p.Sg + int64_t(lane) * V;   // scenario of lane
+        const int scol = lane * V;                                     // column in stage
 
-        // ---- prefetch: independent of earlier levels ----------------------------
-        int node = 0, rb = 0, deg = 0;
-        int nb[PF];
-        Vec<V> dv[PF];
-        if (valid) {
-            node = __ldg(p.node_of + pos);
-            rb = __ldg(p.row_ptr + pos);
-            deg = __ldg(p.row_ptr + pos + 1) - rb;
-#pragma unroll
-            for (int k = 0; k < PF; ++k) {
-                if (k < deg && deg <= light_max) {
-                    nb[k] = __ldg(p.nbr + rb + k);
-                    dv[k] = ldv_nc<V>(p.d + int64_t(__ldg(p.eid + rb + k)) * p.S + col);
-                }
-            }
-        }
-        Vec<V> seed;   // value for degree-0 nodes
-        if (valid && deg == 0) {
-            if (FWD) {
-                float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
-#pragma unroll
-                for (int k = 0; k < V; ++k) seed.x[k] = a0;
-            } else {
-#pragma unroll
-                for (int k = 0; k < V; ++k)
-                    seed.x[k] = canon0(p.src_val ? __ldg(p.src_val + col + k) : p.t_scalar);
-            }
-        }
-
-        // ---- wait for the previous level (in pass order) to be published --------
+        // ---- wait until the previous level (pass order) of this group is published
         const int dep = FWD ? lv - 1 : lv + 1;
         if (tid == 0 && dep >= 0 && dep < p.L) {
             const int need = __ldg(p.chunk_ptr + dep + 1) - __ldg(p.chunk_ptr + dep);
-            if (ld_acquire(p.done + dep) < need) {
-                while (ld_acquire(p.done + dep) < need) __nanosleep(20);
-            }
+            const int *cnt = p.done + g * p.L + dep;
+            if (ld_acquire(cnt) < need)
+                while (ld_acquire(cnt) < need) __nanosleep(20);
         }
-        __syncthreads();
+        consumer_sync();
 
-        // ---- light nodes: this slot's lanes reduce the node's edges --------------
-        if (valid && deg > light_max && lane == 0) s_heavy[atomicAdd(&s_nheavy, 1)] = pos;
-        if (valid && deg <= light_max) {
-            Vec<V> best = seed;
-            if (deg > 0) {
+        // ---- partial max/min of every vslot (<= PF edges) or hub strip ----------
+        auto edge_val = [&](int e, Vec<V> &acc, bool first) {
+            int u;
+            Vec<V> dd;
+            if (e < est) {
+                u = s_nbr[e];
+                dd = ldv_s<V>(s_d + int64_t(e) * p.Sg + scol);
+            } else {
+                u = __ldg(p.nbr + rb + e);
+                dd = ldv_g<V>(p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col);
+            }
+            Vec<V> a = ldv_cg<V>(p.out + int64_t(u) * p.S + col);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                float d1 = dd.x[j];
+                if (CHECK_D) {
+                    bad |= !isfinite(d1);
+                    d1 = canon0(d1);
+                }
+                const float x = relax<FWD>(a.x[j], d1);
+                acc.x[j] = first ? x : combine<FWD>(acc.x[j], x);
+            }
+        };
+        if (!hub) {
+            for (int vs = slot; has_slot && vs < nvs; vs += slots) {
+                const int j = s_vnode[vs];
+                const int eb = s_rp[j] + (vs - s_vb[j]) * PF;
+                const int ee = min(s_rp[j + 1], eb + PF);
+                Vec<V> acc;
+#pragma unroll
+                for (int k = 0; k < V; ++k) acc.x[k] = ident<FWD>();
+                // independent gathers of up to PF edges (one L2 round trip)
+                Vec<V> a[PF];
+                Vec<V> dd[PF];
 #pragma unroll
                 for (int k = 0; k < PF; ++k) {
-                    if (k < deg) {
-                        Vec<V> a = ldv_cg<V>(p.out + int64_t(nb[k]) * p.S + col);
+                    const int e = eb + k;
+                    if (e < ee) {
+                        int u;
+                        if (e < est) {
+                            u = s_nbr[e];
+                            dd[k] = ldv_s<V>(s_d + int64_t(e) * p.Sg + scol);
+                        } else {
+                            u = __ldg(p.nbr + rb + e);
+                            dd[k] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col);
+                        }
+                        a[k] = ldv_cg<V>(p.out + int64_t(u) * p.S + col);
+                    }
+                }
 #pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            float dd = dv[k].x[j];
+                for (int k = 0; k < PF; ++k) {
+                    if (eb + k < ee) {
+#pragma unroll
+                        for (int j2 = 0; j2 < V; ++j2) {
+                            float d1 = dd[k].x[j2];
                             if (CHECK_D) {
-                                bad |= !isfinite(dd);
-                                dd = canon0(dd);
+                                bad |= !isfinite(d1);
+                                d1 = canon0(d1);
                             }
-                            float x = relax<FWD>(a.x[j], dd);
-                            best.x[j] = k == 0 ? x : combine<FWD>(best.x[j], x);
+                            acc.x[j2] = combine<FWD>(acc.x[j2], relax<FWD>(a[k].x[j2], d1));
                         }
                     }
                 }
-                for (int k = PF; k < deg; ++k) {
-                    const int e = rb + k;
-                    Vec<V> a = ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + e)) * p.S + col);
-                    Vec<V> dd = ldv_nc<V>(p.d + int64_t(__ldg(p.eid + e)) * p.S + col);
+                stv_s<V>(s_part + int64_t(vs) * p.Sg + scol, acc);
+            }
+        } else if (has_slot) {
+            Vec<V> acc;
 #pragma unroll
-                    for (int j = 0; j < V; ++j) {
-                        float d1 = dd.x[j];
-                        if (CHECK_D) {
-                            bad |= !isfinite(d1);
-                            d1 = canon0(d1);
-                        }
-                        best.x[j] = combine<FWD>(best.x[j], relax<FWD>(a.x[j], d1));
-                    }
+            for (int k = 0; k < V; ++k) acc.x[k] = ident<FWD>();
+            for (int e = slot; e < E; e += slots) edge_val(e, acc, false);
+            stv_s<V>(s_part + int64_t(slot) * p.Sg + scol, acc);
+        }
+        consumer_sync();
+
+        // ---- combine each node's vslots, store, fused slack (backward) ----------
+        const int nodes_here = hub ? 1 : nn;
+        for (int j = slot; has_slot && j < nodes_here; j += slots) {
+            const int node = s_node[j];
+            Vec<V> best;
+            const bool leaf = s_rp[j + 1] == s_rp[j];
+            if (leaf) {
+                if (FWD) {
+                    const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+#pragma unroll
+                    for (int k = 0; k < V; ++k) best.x[k] = a0;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k)
+                        best.x[k] = canon0(p.src_val ? __ldg(p.src_val + col + k) : p.t_scalar);
+                }
+            } else {
+                const int v0 = hub ? 0 : s_vb[j];
+                const int v1 = hub ? min(slots, E) : s_vb[j + 1];
+                best = ldv_s<V>(s_part + int64_t(v0) * p.Sg + scol);
+                for (int v = v0 + 1; v < v1; ++v) {
+                    Vec<V> q = ldv_s<V>(s_part + int64_t(v) * p.Sg + scol);
+#pragma unroll
+                    for (int k = 0; k < V; ++k) best.x[k] = combine<FWD>(best.x[k], q.x[k]);
                 }
             }
-            stv<V>(p.out + int64_t(node) * p.S + col, best);
+            stv_g<V>(p.out + int64_t(node) * p.S + col, best);
             if (!FWD) {
                 Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
                 Vec<V> sl;
 #pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
-                    run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
+                for (int k = 0; k < V; ++k) {
+                    sl.x[k] = __fsub_rn(best.x[k], a.x[k]);
+                    run_min.x[k] = fminf(run_min.x[k], sl.x[k]);
                 }
-                if (p.slack) stv<V>(p.slack + int64_t(node) * p.S + col, sl);
+                if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
             }
         }
-        __syncthreads();
-
-        // ---- heavy nodes (degree > light_max): the whole CTA splits the edges ----
-        const int nheavy = s_nheavy;
-        for (int h = 0; h < nheavy; ++h) {
-            const int hp = s_heavy[h];
-            const int hnode = __ldg(p.node_of + hp);
-            const int hb = __ldg(p.row_ptr + hp), he = __ldg(p.row_ptr + hp + 1);
-            Vec<V> part;
-            bool any = false;
-            if (has_slot) {
-                for (int e = hb + slot; e < he; e += p.slots) {
-                    Vec<V> a = ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + e)) * p.S + col);
-                    Vec<V> dd = ldv_nc<V>(p.d + int64_t(__ldg(p.eid + e)) * p.S + col);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) {
-                        float d1 = dd.x[j];
-                        if (CHECK_D) {
-                            bad |= !isfinite(d1);
-                            d1 = canon0(d1);
-                        }
-                        float x = relax<FWD>(a.x[j], d1);
-                        part.x[j] = any ? combine<FWD>(part.x[j], x) : x;
-                    }
-                    any = true;
-                }
-            }
-            // slots with no edge contribute the identity
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                s_red[tid * V + j] = any ? part.x[j]
-                                         : __int_as_float(FWD ? 0xff800000 : 0x7f800000);
-            __syncthreads();
-            if (slot == 0 && has_slot) {
-                Vec<V> best;
-#pragma unroll
-                for (int j = 0; j < V; ++j) best.x[j] = s_red[tid * V + j];
-                for (int sl2 = 1; sl2 < p.slots; ++sl2)
-#pragma unroll
-                    for (int j = 0; j < V; ++j)
-                        best.x[j] = combine<FWD>(best.x[j], s_red[(sl2 * p.lpn + lane) * V + j]);
-                stv<V>(p.out + int64_t(hnode) * p.S + col, best);
-                if (!FWD) {
-                    Vec<V> a = ldv_cg<V>(p.other + int64_t(hnode) * p.S + col);
-                    Vec<V> sl;
-#pragma unroll
-                    for (int j = 0; j < V; ++j) {
-                        sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
-                        run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
-                    }
-                    if (p.slack) stv<V>(p.slack + int64_t(hnode) * p.S + col, sl);
-                }
-            }
-            __syncthreads();
-        }
-
-        // ---- publish this chunk ------------------------------------------------------
+        // ---- publish: stores visible at gpu scope, then bump the level counter --
         __threadfence();
-        __syncthreads();
-        if (tid == 0) atomicAdd(p.done + lv, 1);
+        consumer_sync();
+        if (tid == 0) {
+            atomicAdd(p.done + g * p.L + lv, 1);
+            mbar_arrive(empty + st);
+        }
     }
 
-    if (CHECK_D && __syncthreads_or(bad) && tid == 0) atomicOr(p.err, ERR_NONFINITE);
+    if (CHECK_D && bad) atomicOr(p.err, ERR_NONFINITE);
     if (!FWD) {
+        // backward runs with one scenario group (G == 1), so lane owns scenarios
+        // lane*V .. lane*V+V-1 in every chunk
         if (has_slot) {
 #pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (col + j < p.S && run_min.x[j] != __int_as_float(0x7f800000))
-                    atomicMin(s_min + col + j, f2ord(run_min.x[j]));
+            for (int k = 0; k < V; ++k)
+                if (run_min.x[k] != ident<false>())
+                    atomicMin(s_min + lane * V + k, f2ord(run_min.x[k]));
         }
-        __syncthreads();
-        for (int s = tid; s < p.S; s += BLOCK)
+        asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
+        for (int s = tid; s < p.S; s += NCT)
             if (s_min[s] != 0x7f800000) atomicMin(p.wns_ord + s, s_min[s]);
     }
 }
@@ -338,85 +520,161 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
         if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
 }
 
-int pick_vec(int32_t S, std::initializer_list<const void *> ptrs) {
+// ---- chunk schedule (per direction and T), cached in the graph ---------------
+__global__ void k_chunk_nv(const int32_t *__restrict__ row_ptr, int32_t n, int32_t *__restrict__ nv) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int d = row_ptr[i + 1] - row_ptr[i];
+        nv[i] = max(1, (d + PF - 1) / PF);
+    }
+}
+
+__global__ void k_chunk_flags(const int32_t *__restrict__ order, const int32_t *__restrict__ level,
+                              const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ nv,
+                              const int32_t *__restrict__ P, int32_t n, int32_t T,
+                              int32_t *__restrict__ flag) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int ls = level_ptr[level[order[i]]];
+        int f = 1;
+        if (i > ls) {
+            const int c = (P[i] - P[ls]) / T, cp = (P[i - 1] - P[ls]) / T;
+            f = (c != cp) || nv[i] > T || nv[i - 1] > T;
+        }
+        flag[i] = f;
+    }
+}
+
+__global__ void k_chunk_scatter(const int32_t *__restrict__ flag, const int32_t *__restrict__ F,
+                                int32_t n, int32_t *__restrict__ chunk_pos) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (flag[i]) chunk_pos[F[i]] = int(i);
+    if (blockIdx.x == 0 && threadIdx.x == 0) chunk_pos[F[n]] = n;
+}
+
+__global__ void k_chunk_levels(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ F,
+                               int32_t L, int32_t *__restrict__ chunk_ptr) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= L; k += gridDim.x * blockDim.x)
+        chunk_ptr[k] = F[level_ptr[k]];
+}
+
+void build_schedule(Graph &g, const int32_t *row_ptr, int T, DevBuf &pos_buf, DevBuf &ptr_buf,
+                    int32_t &C) {
+    cudaStream_t s = g.stream;
+    const int32_t n = g.n;
+    DevBuf nv, P, flag, F;
+    nv.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    P.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    F.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    HF_CUDA(cudaMemsetAsync(nv.as<int32_t>() + n, 0, sizeof(int32_t), s));
+    HF_CUDA(cudaMemsetAsync(flag.as<int32_t>() + n, 0, sizeof(int32_t), s));
+    k_chunk_nv<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, nv.as<int32_t>());
+    HF_CHECK_LAUNCH();
+    scan_exclusive(nv.as<int32_t>(), P.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    k_chunk_flags<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+        g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), nv.as<int32_t>(),
+        P.as<int32_t>(), n, T, flag.as<int32_t>());
+    HF_CHECK_LAUNCH();
+    scan_exclusive(flag.as<int32_t>(), F.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    int32_t h_C = 0;
+    HF_CUDA(cudaMemcpyAsync(&h_C, F.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaStreamSynchronize(s));
+    C = h_C;
+    pos_buf.alloc(sizeof(int32_t) * (int64_t(C) + 1), s);
+    ptr_buf.alloc(sizeof(int32_t) * (int64_t(g.L) + 1), s);
+    k_chunk_scatter<<<grid_for(n, 256, g.sms), 256, 0, s>>>(flag.as<int32_t>(), F.as<int32_t>(),
+                                                            n, pos_buf.as<int32_t>());
+    HF_CHECK_LAUNCH();
+    k_chunk_levels<<<grid_for(int64_t(g.L) + 1, 256, g.sms), 256, 0, s>>>(
+        g.level_ptr.as<int32_t>(), F.as<int32_t>(), g.L, ptr_buf.as<int32_t>());
+    HF_CHECK_LAUNCH();
+    g.launches += 5;
+}
+
+int pick_vec(int32_t Sg, std::initializer_list<const void *> ptrs) {
     auto aligned = [&](int bytes) {
         for (const void *q : ptrs)
             if (q && (reinterpret_cast<uintptr_t>(q) % bytes)) return false;
         return true;
     };
-    if (S % 4 == 0 && aligned(16)) return 4;
-    if (S % 2 == 0 && aligned(8)) return 2;
+    if (Sg % 4 == 0 && aligned(16)) return 4;
+    if (Sg % 2 == 0 && aligned(8)) return 2;
     return 1;
-}
-
-// chunk_ptr for `slots` nodes per chunk, cached in the graph
-void ensure_chunks(Graph &g, int slots) {
-    if (g.chunk_slots == slots && g.chunk_ptr.p) return;
-    std::vector<int32_t> cp(size_t(g.L) + 1, 0);
-    for (int32_t k = 0; k < g.L; ++k) {
-        int32_t w = g.h_level_ptr[k + 1] - g.h_level_ptr[k];
-        cp[k + 1] = cp[k] + (w + slots - 1) / slots;
-    }
-    g.chunk_ptr.alloc(sizeof(int32_t) * cp.size(), g.stream);
-    HF_CUDA(cudaMemcpyAsync(g.chunk_ptr.p, cp.data(), sizeof(int32_t) * cp.size(),
-                            cudaMemcpyHostToDevice, g.stream));
-    HF_CUDA(cudaStreamSynchronize(g.stream));   // cp is a host temporary
-    g.chunk_slots = slots;
-    g.total_chunks = cp.back();
-}
-
-template <int V, bool FWD, bool CHECK_D> int grid_of(Graph &g, size_t smem) {
-    int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_propagate<V, FWD, CHECK_D>,
-                                                          BLOCK, smem));
-    if (per_sm < 1) per_sm = 1;
-    return std::max(1, std::min(per_sm * g.sms, g.total_chunks));
-}
-
-template <int V, bool FWD, bool CHECK_D> void launch(Graph &g, PassParams &p) {
-    size_t smem = FWD ? 0 : sizeof(int32_t) * size_t(p.S);
-    if (smem > 48 * 1024)
-        HF_CUDA(cudaFuncSetAttribute(k_propagate<V, FWD, CHECK_D>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int grid = grid_of<V, FWD, CHECK_D>(g, smem);
-    k_propagate<V, FWD, CHECK_D><<<grid, BLOCK, smem, g.stream>>>(p);
-    HF_CHECK_LAUNCH();
-    g.launches += 1;
-}
-
-template <int V, bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d) {
-    const int lpn = p.S / V;
-    p.lpn = lpn;
-    p.slots = BLOCK / lpn;
-    ensure_chunks(g, p.slots);
-    p.chunk_ptr = g.chunk_ptr.as<int32_t>();
-    p.total_chunks = g.total_chunks;
-    p.level_ptr = g.level_ptr.as<int32_t>();
-    p.L = g.L;
-    // per-pass counters: done[L] + ticket
-    g.ws_sync.alloc(sizeof(int32_t) * (size_t(g.L) + 1), g.stream);
-    HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(g.L) + 1), g.stream));
-    p.done = g.ws_sync.as<int32_t>();
-    p.ticket = p.done + g.L;
-    p.err = g.d_err();
-    if (check_d) launch<V, FWD, true>(g, p);
-    else launch<V, FWD, false>(g, p);
-}
-
-template <bool FWD> void dispatch(Graph &g, PassParams &p, bool check_d, int V) {
-    if (V == 4) run_pass<4, FWD>(g, p, check_d);
-    else if (V == 2) run_pass<2, FWD>(g, p, check_d);
-    else run_pass<1, FWD>(g, p, check_d);
 }
 
 void prof_record(Graph &g, int idx) {
     if (g.prof) HF_CUDA(cudaEventRecord(g.ev[idx], g.stream));
 }
 
-void check_S(int32_t S, int V) {
-    if (S / V > BLOCK)
-        fail(HF_ERR_INVALID_ARG, "too many scenarios in one call (S/V must be <= 256: S <= 1024 "
-                                 "with 16-byte aligned buffers)");
+template <int V, bool FWD, bool CHECK_D, bool BULK>
+void launch(Graph &g, PassParams &p, size_t smem) {
+    auto kern = k_propagate<V, FWD, CHECK_D, BULK>;
+    HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
+    if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
+    const int grid = std::max(1, std::min(per_sm * g.sms, p.C * p.G));
+    kern<<<grid, BLOCK, smem, g.stream>>>(p);
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
+}
+
+template <bool FWD>
+void run_pass(Graph &g, PassParams &p, bool check_d, int V, bool bulk) {
+    const int lpn = p.Sg / V;
+    const int T = NCT / lpn;
+    p.T = T;
+    // chunk schedule (cached per direction and T)
+    DevBuf &pos = FWD ? g.sched_f_pos : g.sched_b_pos;
+    DevBuf &ptr = FWD ? g.sched_f_ptr : g.sched_b_ptr;
+    int32_t &C = FWD ? g.sched_f_C : g.sched_b_C;
+    int32_t &Tc = FWD ? g.sched_f_T : g.sched_b_T;
+    if (Tc != T || !pos.p) {
+        build_schedule(g, p.row_ptr, T, pos, ptr, C);
+        Tc = T;
+    }
+    p.chunk_pos = pos.as<int32_t>();
+    p.chunk_ptr = ptr.as<int32_t>();
+    p.C = C;
+    p.L = g.L;
+    p.ecap = std::min(2 * T * PF, std::max(64, 16384 / (4 * p.Sg)));
+    const StageLayout SL = stage_layout(T, p.ecap, p.Sg);
+    size_t smem = size_t(NB) * SL.bytes + 2 * NB * 8 + sizeof(float) * 2 * T * p.Sg +
+                  (FWD ? 0 : sizeof(int32_t) * p.S);
+    // per-pass counters: done[G*L] + ticket
+    g.ws_sync.alloc(sizeof(int32_t) * (size_t(p.G) * g.L + 1), g.stream);
+    HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(p.G) * g.L + 1), g.stream));
+    p.done = g.ws_sync.as<int32_t>();
+    p.ticket = p.done + size_t(p.G) * g.L;
+    p.err = g.d_err();
+#define HF_LAUNCH(VV)                                                                       \
+    do {                                                                                    \
+        if (check_d && bulk) launch<VV, FWD, true, true>(g, p, smem);                       \
+        else if (check_d) launch<VV, FWD, true, false>(g, p, smem);                         \
+        else if (bulk) launch<VV, FWD, false, true>(g, p, smem);                            \
+        else launch<VV, FWD, false, false>(g, p, smem);                                     \
+    } while (0)
+    if (V == 4) HF_LAUNCH(4);
+    else if (V == 2) HF_LAUNCH(2);
+    else HF_LAUNCH(1);
+#undef HF_LAUNCH
+}
+
+// scenario groups: Sg = S / G with Sg / V <= NCT
+void choose_groups(int32_t S, const std::initializer_list<const void *> &ptrs, int &G, int &Sg,
+                   int &V) {
+    G = 1;
+    while (true) {
+        if (S % G == 0) {
+            Sg = S / G;
+            V = pick_vec(Sg, ptrs);
+            if (Sg / V <= NCT) break;
+        }
+        ++G;
+        if (G > S) fail(HF_ERR_INVALID_ARG, "cannot split scenarios into groups");
+    }
 }
 
 }  // namespace
@@ -425,18 +683,21 @@ void check_S(int32_t S, int V) {
 void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                     float *at) {
     if (g.n == 0) return;
-    int V = pick_vec(S, {d, at});
-    check_S(S, V);
     PassParams p{};
+    int G, Sg, V;
+    choose_groups(S, {d, at}, G, Sg, V);
     p.row_ptr = g.lo_in_ptr.as<int32_t>();
     p.nbr = g.lo_in_src.as<int32_t>();
     p.eid = g.lo_in_eid.as<int32_t>();
     p.node_of = g.order.as<int32_t>();
     p.S = S;
+    p.Sg = Sg;
+    p.G = G;
     p.d = d;
     p.src_val = at_src;
     p.out = at;
-    dispatch<true>(g, p, check_d, V);
+    const bool bulk = (Sg % 4 == 0) && (reinterpret_cast<uintptr_t>(d) % 16 == 0) && S % 4 == 0;
+    run_pass<true>(g, p, check_d, V, bulk);
 }
 
 // Backward over all levels + slack + wns (ordered ints, decoded into wns_f[S]).
@@ -454,14 +715,17 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         g.launches += 1;
     }
     if (g.n > 0) {
-        int V = pick_vec(S, {d, at, rat, slack});
-        check_S(S, V);
         PassParams p{};
+        int G, Sg, V;
+        choose_groups(S, {d, at, rat, slack}, G, Sg, V);
+        if (G > 1) fail(HF_ERR_INVALID_ARG, "backward: more than 1024 scenarios per call");
         p.row_ptr = g.lo_out_ptr.as<int32_t>();
         p.nbr = g.lo_out_dst.as<int32_t>();
         p.eid = g.lo_out_eid.as<int32_t>();
         p.node_of = g.order.as<int32_t>();
         p.S = S;
+        p.Sg = Sg;
+        p.G = G;
         p.d = d;
         p.src_val = t_arr;
         p.t_scalar = t_scalar;
@@ -469,7 +733,8 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         p.out = rat;
         p.slack = slack;
         p.wns_ord = ord;
-        dispatch<false>(g, p, false, V);
+        const bool bulk = (Sg % 4 == 0) && (reinterpret_cast<uintptr_t>(d) % 16 == 0) && S % 4 == 0;
+        run_pass<false>(g, p, false, V, bulk);
     }
     if (wns_f) {
         k_ord_to_float<<<1, 256, 0, s>>>(ord, wns_f, S);
