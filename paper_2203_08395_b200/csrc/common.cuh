@@ -68,6 +68,14 @@ struct DevBuf {
     template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
+// ---- piece schedule of one propagation direction (propagate.cu) ------------
+struct PieceSched {
+    DevBuf pieces;   // int4 {pos_begin, pos_end, edge_begin, edge_end}, level-major
+    DevBuf off;      // [L+1] first piece of every level
+    DevBuf cta_pc, cta_lv, cta_off;   // the same pieces dealt to CTAs, pass order
+    int32_t key = -1;                 // (piece weight, CTAs) the schedule was built for
+};
+
 // ---- the graph -------------------------------------------------------------
 struct Graph {
     int device = 0;
@@ -85,11 +93,12 @@ struct Graph {
     int32_t max_level_width = 0;
     // level-ordered ("relabelled") CSR for the propagation passes: row i is node
     // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
-    DevBuf lo_in_ptr, lo_in_src, lo_in_eid, lo_out_ptr, lo_out_dst, lo_out_eid;
-    // chunk schedules of the persistent propagation kernels (per direction, cached
-    // per vslot target T): first position of every chunk, first chunk of every level
-    DevBuf sched_f_pos, sched_f_ptr, sched_b_pos, sched_b_ptr;
-    int32_t sched_f_C = 0, sched_f_T = -1, sched_b_C = 0, sched_b_T = -1;
+    // Within a level, rows are in ascending degree (per direction): node ids
+    // lo_in_node / lo_out_node.
+    DevBuf lo_in_node, lo_in_ptr, lo_in_src, lo_in_eid;
+    DevBuf lo_out_node, lo_out_ptr, lo_out_dst, lo_out_eid;
+    // piece schedules of the persistent propagation kernels (per direction)
+    PieceSched ps_f, ps_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // small device scalars: [0] error bits, [1..] scratch

@@ -4,33 +4,41 @@
 //
 // Data layout in HBM (scenario-minor): at[v*S + s], rat[v*S + s],
 // delays[e*S + s].  A node's S values are contiguous, so each edge touches S*4
-// contiguous bytes; a node-slice of Sg scenarios is owned by LPN = Sg/V lanes
-// holding V-wide vectors (V = 4 -> LDG.128 / STG.128).  Pull-based, no float
-// atomics: every output is one fp32 max/min over fl(x +/- d) terms, which is
-// order-independent (0 ULP against the oracle, reading R10).
+// contiguous bytes; a node row is owned by LPN = S/V lanes holding V-wide
+// vectors (V = 4 -> LDG.128 / STG.128).  Pull-based, no float atomics: every
+// output is one fp32 max/min over fl(x +/- d) terms, which is order-independent
+// (0 ULP against the oracle, reading R10).
 //
-// One persistent, warp-specialised launch per pass (no per-level launches, no
-// grid barrier):
-//   * Work = chunks of consecutive nodes of one level (level order forward,
-//     reverse level order backward), sized by "vslots" (a node of degree d needs
-//     ceil(d/PF) vslots of <= PF edges) so chunks are edge-balanced; hub nodes
-//     get a chunk of their own.  CTAs claim chunks with an atomic ticket; a chunk
-//     only waits on chunks with smaller tickets, held by running CTAs, so the
-//     schedule is deadlock-free at any grid size.
-//   * Producer warp: claims tickets up to NB chunks ahead, loads the chunk's
-//     level-ordered CSR rows, builds the vslot table and stages every edge's
-//     neighbour id and delay slice in shared memory with cp.async.bulk (TMA bulk
-//     copies, completion on an mbarrier).  None of this depends on earlier levels,
-//     so the HBM stream of delays runs ahead of the dependency front.
-//   * Consumer warps: wait for the stage (mbarrier), then for the previous level
-//     (one acquire-poll of its per-level chunk counter), gather at[u] / rat[v]
-//     from L2, reduce each vslot in registers, combine a node's vslots through
-//     shared memory, store, fence, and publish (release) the chunk.  Level k
-//     complete => all earlier levels complete, by induction.
-//   * Backward fuses slack = rat - at and keeps a per-lane running min; one
+// One persistent launch per pass (cooperative launch, one CTA per SM; no
+// per-level launches, no grid barrier):
+//   * every level is cut into weight-balanced PIECES (weight = edges + nodes);
+//     piece j of a level belongs to CTA j mod P, and a CTA walks its pieces in
+//     pass order (levels ascending forward, descending backward);
+//   * STAGING: a piece's level-ordered rows, neighbour ids, edge ids and delay
+//     slices are copied into shared memory with cp.async by all threads -- rows
+//     two pieces ahead, delays one piece ahead of the piece being computed
+//     (3-slot ring).  None of this depends on earlier levels, so the HBM stream
+//     of delays runs ahead of the dependency front;
+//   * DEPENDENCY: before computing a piece of level k the CTA waits until level
+//     k-1 (k+1 backward) has published all its pieces: one acquire-poll of a
+//     per-level counter by one thread.  Level k complete => every earlier level
+//     complete, by induction; a CTA only waits on earlier levels whose pieces
+//     belong to co-resident CTAs, so the schedule cannot deadlock;
+//   * COMPUTE: edge-parallel gathers of at[u] / rat[v] from L2 (all edge-lane
+//     items issue their loads at once), x = fl(a +/- d) written in place over the
+//     staged delay, then each node's owner lanes reduce their row from shared
+//     memory; rows longer than HUB_DEG are reduced by the whole CTA (strided
+//     partials, shared-memory combine).  Stores, gpu-scope fence, one atomicAdd
+//     publishes the piece;
+//   * backward fuses slack = rat - at and keeps a per-lane running min; one
 //     shared-memory reduction and one global atomicMin per scenario per CTA give
 //     the worst slack.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -38,11 +46,10 @@ namespace hf {
 
 namespace {
 
-constexpr int NCW = 8;                     // consumer warps
-constexpr int NCT = NCW * 32;              // consumer threads
-constexpr int BLOCK = NCT + 32;            // + 1 producer warp
-constexpr int PF = 4;                      // edges per vslot
-constexpr int NB = 4;                      // pipeline stages
+constexpr int NT = 512;        // threads per CTA (one CTA per SM)
+constexpr int NBUF = 4;        // staging ring slots
+constexpr int HUB_DEG = 64;    // rows longer than this are reduced by the whole CTA
+constexpr int MAX_HUBS = 256;  // long rows per piece (piece weight bounds this)
 
 template <int V> struct Vec {
     float x[V];
@@ -75,7 +82,7 @@ template <int V> __device__ __forceinline__ Vec<V> ldv_cg(const float *p) {
     }
     return r;
 }
-template <int V> __device__ __forceinline__ Vec<V> ldv_s(const float *p) {   // shared
+template <int V> __device__ __forceinline__ Vec<V> ldv_s(const float *p) {
     Vec<V> r;
     if constexpr (V == 4) {
         float4 t = *reinterpret_cast<const float4 *>(p);
@@ -107,7 +114,6 @@ template <int V> __device__ __forceinline__ void stv_g(float *p, const Vec<V> &v
     }
 }
 
-// ---- PTX helpers: acquire load, mbarrier, bulk copy, named barrier ----------
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -116,43 +122,17 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void consumer_sync() {   // named barrier 1: consumer warps only
-    asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
-}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 struct PassParams {
     // level-ordered CSR of this direction: row i <-> node node_of[i]
@@ -160,12 +140,15 @@ struct PassParams {
     const int32_t *nbr;        // [m] neighbour node id (fan-in src / fan-out dst)
     const int32_t *eid;        // [m] edge id (delay row)
     const int32_t *node_of;    // [n]
-    const int32_t *chunk_pos;  // [C+1] first position of every chunk (+ n)
-    const int32_t *chunk_ptr;  // [L+1] first chunk of every level
-    int32_t L, C, G;           // levels, chunks, scenario groups
-    int32_t T;                 // vslots per chunk target (= consumer slots)
-    int32_t ecap;              // staged edges per stage
-    int32_t S, Sg;             // row stride (scenarios), scenarios per group
+    const int4 *cta_pc;        // per-CTA piece sequence (pass order): {pos_begin, pos_end,
+                               // edge_begin, edge_end}
+    const int32_t *cta_lv;     // level of each entry of cta_pc
+    const int32_t *cta_off;    // [P+1] first entry of every CTA
+    const int32_t *piece_off;  // [L+1] first piece of every level (pieces per level)
+    int32_t L;
+    int32_t ncap, ecap;        // staged rows / edges per ring slot
+    int32_t split;             // rows longer than this are cut into part pieces
+    int32_t S;                 // scenarios (row stride of at / rat / delays)
     const float *d;            // [m][S]
     const float *src_val;      // forward: at_src [n] (or null); backward: t_req [S] (or null)
     float t_scalar;            // backward: T when t_req is null
@@ -173,30 +156,37 @@ struct PassParams {
     float *out;                // forward: at; backward: rat
     float *slack;              // backward, optional [n][S]
     int32_t *wns_ord;          // backward: [S] ordered-int mins
-    int32_t *done;             // [G*L] chunks published per (group, level)
-    int32_t *ticket;           // [1]
+    int32_t *done;             // [L] pieces published per level
     uint32_t *err;
+    // optional timeline (HF_TRACE=1): per piece {level<<8|slot, cta, t_top, t_ready,
+    // t_computed, t_published, edges, rows} in globaltimer ns
+    unsigned long long *trace;
+    int32_t *trace_n;
+    int32_t trace_cap;
 };
 
-// per-stage shared-memory layout (offsets in bytes, computed identically on host)
-struct StageLayout {
-    int desc, node, rp, vb, vnode, nbr, d, bytes;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ring-slot layout in shared memory (bytes)
+struct SlotLayout {
+    int node, rp, nbr, eid, d, bytes;
 };
-__host__ __device__ inline StageLayout stage_layout(int T, int ecap, int Sg) {
-    StageLayout L;
+__host__ __device__ inline SlotLayout slot_layout(int ncap, int ecap, int S) {
+    SlotLayout L;
     int o = 0;
-    L.desc = o;  o += 16 * 4;
-    L.node = o;  o += T * 4;
-    L.rp = o;    o += (T + 1) * 4;
-    L.vb = o;    o += (T + 1) * 4;
-    L.vnode = o; o += 2 * T * 4;
-    L.nbr = o;   o += ecap * 4;
+    L.node = o; o += ncap * 4;
+    L.rp = o;   o += (ncap + 1) * 4;
+    L.nbr = o;  o += ecap * 4;
+    L.eid = o;  o += ecap * 4;
     o = (o + 15) & ~15;
-    L.d = o;     o += ecap * Sg * 4;
+    L.d = o;    o += ecap * S * 4;
     L.bytes = (o + 127) & ~127;
     return L;
 }
-enum { D_T = 0, D_LV, D_G, D_POS, D_NN, D_RB, D_E, D_EST, D_NVS, D_HUB };
 
 template <bool FWD> __device__ __forceinline__ float combine(float best, float x) {
     return FWD ? fmaxf(best, x) : fminf(best, x);
@@ -208,297 +198,443 @@ template <bool FWD> __device__ __forceinline__ float ident() {
     return __int_as_float(FWD ? 0xff800000 : 0x7f800000);   // -inf for max, +inf for min
 }
 
-template <int V, bool FWD, bool CHECK_D, bool BULK>
-__global__ void __launch_bounds__(BLOCK, 2) k_propagate(PassParams p) {
+// combine v into *addr with max (forward) / min (backward); exact, order-free
+template <bool FWD> __device__ __forceinline__ void atomic_combine(float *addr, float v) {
+    int *ai = reinterpret_cast<int *>(addr);
+    int old = __ldcg(ai);
+    for (;;) {
+        const float nv = combine<FWD>(__int_as_float(old), v);
+        if (__float_as_int(nv) == old) return;
+        const int prev = atomicCAS(ai, old, __float_as_int(nv));
+        if (prev == old) return;
+        old = prev;
+    }
+}
+
+__device__ __forceinline__ int pieces_in(const PassParams &p, int k) {
+    return __ldg(p.piece_off + k + 1) - __ldg(p.piece_off + k);
+}
+
+template <int V, bool FWD, bool CHECK_D, bool VEC16>
+__global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const StageLayout SL = stage_layout(p.T, p.ecap, p.Sg);
-    const int lpn = p.Sg / V;                 // lanes per node slice
-    const int slots = NCT / lpn;              // vslots handled per round
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NB * SL.bytes);
-    uint64_t *empty = full + NB;
-    float *s_part = reinterpret_cast<float *>(smem + NB * SL.bytes + 2 * NB * 8);   // [2T][Sg]
-    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + 2 * p.T * p.Sg);           // [S]
+    const SlotLayout SL = slot_layout(p.ncap, p.ecap, p.S);
+    float *s_part = reinterpret_cast<float *>(smem + NBUF * SL.bytes);       // [NT*V]
+    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + NT * V);           // [S]
+    __shared__ int s_meta[NBUF][5];   // level, pos_begin, rows, edge_begin, edges
+    __shared__ int s_nhub;
+    __shared__ int s_hub[MAX_HUBS];
+
     const int tid = threadIdx.x;
-
-    if (tid == 0) {
-        for (int s = 0; s < NB; ++s) {
-            mbar_init(full + s, 32);
-            mbar_init(empty + s, 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (!FWD)
-        for (int s = tid; s < p.S; s += BLOCK) s_min[s] = 0x7f800000;
-    __syncthreads();
-
-    if (tid >= NCT) {
-        // ============================ producer warp ============================
-        const int lane = tid - NCT;
-        int lv = FWD ? 0 : p.L - 1;
-        for (int i = 0;; ++i) {
-            const int st = i % NB;
-            mbar_wait(empty + st, ((i / NB) & 1) ^ 1);
-            unsigned char *sb = smem + st * SL.bytes;
-            int32_t *desc = reinterpret_cast<int32_t *>(sb + SL.desc);
-            int t = 0;
-            if (lane == 0) t = atomicAdd(p.ticket, 1);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            if (t >= p.C * p.G) {
-                if (lane == 0) desc[D_T] = -1;
-                mbar_arrive(full + st);
-                break;
-            }
-            const int g = t % p.G;
-            const int rank = FWD ? t / p.G : p.C - 1 - t / p.G;
-            if (FWD) {
-                while (__ldg(p.chunk_ptr + lv + 1) <= rank) ++lv;
-            } else {
-                while (__ldg(p.chunk_ptr + lv) > rank) --lv;
-            }
-            const int pos = __ldg(p.chunk_pos + rank);
-            const int nn = __ldg(p.chunk_pos + rank + 1) - pos;
-            int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
-            int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
-            int32_t *s_vb = reinterpret_cast<int32_t *>(sb + SL.vb);
-            int32_t *s_vnode = reinterpret_cast<int32_t *>(sb + SL.vnode);
-            int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
-            float *s_d = reinterpret_cast<float *>(sb + SL.d);
-            const int rb = __ldg(p.row_ptr + pos);
-            const int E = __ldg(p.row_ptr + pos + nn) - rb;
-            const bool hub = nn == 1 && (E + PF - 1) / PF > p.T;
-            // rows + vslot prefix (nodes are <= T)
-            int carry = 0;
-            for (int j0 = 0; j0 < nn; j0 += 32) {
-                const int j = j0 + lane;
-                int nv = 0;
-                if (j < nn) {
-                    s_node[j] = __ldg(p.node_of + pos + j);
-                    const int a = __ldg(p.row_ptr + pos + j) - rb;
-                    const int b = __ldg(p.row_ptr + pos + j + 1) - rb;
-                    s_rp[j] = a;
-                    nv = hub ? 0 : max(1, (b - a + PF - 1) / PF);
-                }
-                int incl = nv;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (j < nn) s_vb[j] = carry + incl - nv;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            const int nvs = hub ? 0 : carry;
-            if (lane == 0) {
-                s_rp[nn] = E;
-                s_vb[nn] = nvs;
-            }
-            __syncwarp();
-            if (!hub)
-                for (int j = lane; j < nn; j += 32)
-                    for (int v = s_vb[j]; v < s_vb[j + 1]; ++v) s_vnode[v] = j;
-            // stage neighbours + delay slices of the first est edges
-            const int est = min(E, p.ecap);
-            const int64_t col0 = int64_t(g) * p.Sg;
-            for (int e = lane; e < est; e += 32) {
-                s_nbr[e] = __ldg(p.nbr + rb + e);
-                const float *src = p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col0;
-                if (BULK) {
-                    bulk_g2s(s_d + int64_t(e) * p.Sg, src, uint32_t(p.Sg) * 4u, full + st);
-                } else {
-                    for (int c = 0; c < p.Sg; ++c) s_d[int64_t(e) * p.Sg + c] = __ldg(src + c);
-                }
-            }
-            if (lane == 0) {
-                desc[D_T] = t;
-                desc[D_LV] = lv;
-                desc[D_G] = g;
-                desc[D_POS] = pos;
-                desc[D_NN] = nn;
-                desc[D_RB] = rb;
-                desc[D_E] = E;
-                desc[D_EST] = est;
-                desc[D_NVS] = nvs;
-                desc[D_HUB] = hub;
-            }
-            __syncwarp();
-            if (BULK && lane == 0)
-                mbar_arrive_tx(full + st, uint32_t(est) * uint32_t(p.Sg) * 4u);
-            else
-                mbar_arrive(full + st);
-        }
-        return;
-    }
-
-    // ============================== consumer warps ==============================
-    const int slot = tid / lpn;
-    const int lane = tid - slot * lpn;
-    const bool has_slot = slot < slots;
+    const int P = gridDim.x, b = blockIdx.x;
+    const int lpn = p.S / V;                       // lanes per node row
+    const int active = (NT / lpn) * lpn;           // threads with a fixed lane
+    const int slots = active / lpn;                // rows handled side by side
+    const int lane = tid % lpn;
+    const int64_t col = int64_t(lane) * V;
     bool bad = false;
     Vec<V> run_min;
 #pragma unroll
     for (int k = 0; k < V; ++k) run_min.x[k] = ident<false>();
+    if (!FWD)
+        for (int s = tid; s < p.S; s += NT) s_min[s] = 0x7f800000;
 
-    for (int i = 0;; ++i) {
-        const int st = i % NB;
-        mbar_wait(full + st, (i / NB) & 1);
-        unsigned char *sb = smem + st * SL.bytes;
-        const int32_t *desc = reinterpret_cast<const int32_t *>(sb + SL.desc);
-        if (desc[D_T] < 0) break;
-        const int lv = desc[D_LV], g = desc[D_G], nn = desc[D_NN], rb = desc[D_RB];
-        const int E = desc[D_E], est = desc[D_EST], nvs = desc[D_NVS];
-        const bool hub = desc[D_HUB] != 0;
+    // ---- staging ------------------------------------------------------------------
+    const int seq0 = __ldg(p.cta_off + b), nseq = __ldg(p.cta_off + b + 1) - seq0;
+    auto stage_rows = [&](int slot, int4 pc, int lvl) {  // phase 1: rows and ids (async)
+        unsigned char *sb = smem + slot * SL.bytes;
+        const int nn = pc.y - pc.x, E = pc.w - pc.z;
+        const int nst = min(nn, p.ncap), est = min(E, p.ecap);
+        if (tid == 0) {
+            s_meta[slot][0] = lvl;
+            s_meta[slot][1] = pc.x;
+            s_meta[slot][2] = nn;
+            s_meta[slot][3] = pc.z;
+            s_meta[slot][4] = E;
+        }
+        int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
+        int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
+        int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
+        int32_t *s_eid = reinterpret_cast<int32_t *>(sb + SL.eid);
+        for (int i = tid; i < nst; i += NT) cp_async4(s_node + i, p.node_of + pc.x + i);
+        for (int i = tid; i <= nst; i += NT) cp_async4(s_rp + i, p.row_ptr + pc.x + i);
+        for (int e = tid; e < est; e += NT) {
+            cp_async4(s_nbr + e, p.nbr + pc.z + e);
+            cp_async4(s_eid + e, p.eid + pc.z + e);
+        }
+    };
+    auto stage_delays = [&](int slot) {                  // phase 2: needs the staged eids
+        unsigned char *sb = smem + slot * SL.bytes;
+        const int est = min(s_meta[slot][4], p.ecap);
+        const int32_t *s_eid = reinterpret_cast<const int32_t *>(sb + SL.eid);
+        float *s_d = reinterpret_cast<float *>(sb + SL.d);
+        if (VEC16) {
+            const int gpr = p.S / 4;                       // 16-byte granules per row
+            if ((gpr & (gpr - 1)) == 0 && gpr <= NT) {     // fixed column per thread
+                const int c = tid & (gpr - 1), estep = NT / gpr;
+                for (int e = tid / gpr; e < est; e += estep)
+                    cp_async16(s_d + int64_t(e) * p.S + 4 * c,
+                               p.d + int64_t(s_eid[e]) * p.S + 4 * c);
+            } else {
+                for (int q = tid; q < est * gpr; q += NT) {
+                    const int e = q / gpr, c = q - e * gpr;
+                    cp_async16(s_d + int64_t(e) * p.S + 4 * c,
+                               p.d + int64_t(s_eid[e]) * p.S + 4 * c);
+                }
+            }
+        } else {
+            for (int q = tid; q < est * p.S; q += NT) {
+                const int e = q / p.S, c = q - e * p.S;
+                cp_async4(s_d + int64_t(e) * p.S + c, p.d + int64_t(s_eid[e]) * p.S + c);
+            }
+        }
+    };
+
+    // ---- prologue: groups {rows(0)}, {delays(0), rows(1)}, {delays(1), rows(2)} -----
+    // In steady state iteration t commits {delays(t+2), rows(t+3)}: delays are in
+    // flight for a whole iteration before the piece is computed.
+    if (nseq > 0) stage_rows(0, __ldg(p.cta_pc + seq0), __ldg(p.cta_lv + seq0));
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    if (nseq > 0) stage_delays(0);
+    if (nseq > 1) stage_rows(1, __ldg(p.cta_pc + seq0 + 1), __ldg(p.cta_lv + seq0 + 1));
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    if (nseq > 1) stage_delays(1);
+    if (nseq > 2) stage_rows(2, __ldg(p.cta_pc + seq0 + 2), __ldg(p.cta_lv + seq0 + 2));
+    cp_commit();
+    // descriptor of piece t+3, loaded one iteration before it is staged
+    int4 nd = make_int4(0, 0, 0, 0);
+    int nlv = 0;
+    if (nseq > 3) {
+        nd = __ldg(p.cta_pc + seq0 + 3);
+        nlv = __ldg(p.cta_lv + seq0 + 3);
+    }
+
+    for (int t = 0; t < nseq; ++t) {
+        const int cur = t % NBUF, s2 = (t + 2) % NBUF, s3 = (t + 3) % NBUF;
+        const unsigned long long t_top = p.trace ? gtimer() : 0;
+        const int kc = s_meta[cur][0];
+        // (a) backward: prefetch at[] of this thread's first rows for the slack
+        // (rows(t) landed an iteration ago; independent of the dependency)
+        Vec<V> pre_at[2];
+        if (!FWD && tid < active) {
+            const int nst0 = min(s_meta[cur][2], p.ncap);
+            const int32_t *s_node0 =
+                reinterpret_cast<const int32_t *>(smem + cur * SL.bytes + SL.node);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int i = tid / lpn + r * slots;
+                if (i < nst0) pre_at[r] = ldv_cg<V>(p.other + int64_t(s_node0[i]) * p.S + col);
+            }
+        }
+        // (b) wait until the previous level (pass order) is fully published; a
+        // level whose only piece is this CTA's own needs no poll (same-CTA order)
+        const int dep = FWD ? kc - 1 : kc + 1;
+        if (tid == 0 && dep >= 0 && dep < p.L) {
+            const int need = pieces_in(p, dep);
+            if (!(need == 1 && b == 0)) {
+                if (ld_acquire(p.done + dep) < need)
+                    while (ld_acquire(p.done + dep) < need) __nanosleep(32);
+            }
+        }
+        if (tid == 0) s_nhub = 0;
+        // the group {delays(t), rows(t+1)} (committed two iterations ago) has landed
+        cp_wait_prev();
+        __syncthreads();
+
+        const unsigned long long t_ready = p.trace ? gtimer() : 0;
+        // (c) compute the piece in slot `cur`
+        unsigned char *sb = smem + cur * SL.bytes;
+        const int pos0 = s_meta[cur][1], nn = s_meta[cur][2], rb = s_meta[cur][3];
+        const int E = s_meta[cur][4];
+        const int est = min(E, p.ecap), nst = min(nn, p.ncap);
         const int32_t *s_node = reinterpret_cast<const int32_t *>(sb + SL.node);
         const int32_t *s_rp = reinterpret_cast<const int32_t *>(sb + SL.rp);
-        const int32_t *s_vb = reinterpret_cast<const int32_t *>(sb + SL.vb);
-        const int32_t *s_vnode = reinterpret_cast<const int32_t *>(sb + SL.vnode);
         const int32_t *s_nbr = reinterpret_cast<const int32_t *>(sb + SL.nbr);
-        const float *s_d = reinterpret_cast<const float *>(sb + SL.d);
-        const int64_t col = int64_t(g) * p.Sg + int64_t(lane) * V;   // scenario of lane
-        const int scol = lane * V;                                     // column in stage
-
-        // ---- wait until the previous level (pass order) of this group is published
-        const int dep = FWD ? lv - 1 : lv + 1;
-        if (tid == 0 && dep >= 0 && dep < p.L) {
-            const int need = __ldg(p.chunk_ptr + dep + 1) - __ldg(p.chunk_ptr + dep);
-            const int *cnt = p.done + g * p.L + dep;
-            if (ld_acquire(cnt) < need)
-                while (ld_acquire(cnt) < need) __nanosleep(20);
-        }
-        consumer_sync();
-
-        // ---- partial max/min of every vslot (<= PF edges) or hub strip ----------
-        auto edge_val = [&](int e, Vec<V> &acc, bool first) {
-            int u;
-            Vec<V> dd;
-            if (e < est) {
-                u = s_nbr[e];
-                dd = ldv_s<V>(s_d + int64_t(e) * p.Sg + scol);
-            } else {
-                u = __ldg(p.nbr + rb + e);
-                dd = ldv_g<V>(p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col);
-            }
-            Vec<V> a = ldv_cg<V>(p.out + int64_t(u) * p.S + col);
+        float *s_d = reinterpret_cast<float *>(sb + SL.d);
+        // (c1) edge-parallel: x = fl(a[u] +/- d), written in place over the delay;
+        // up to 4 items per thread issue their gathers together (one L2 round trip)
+        if ((lpn & (lpn - 1)) == 0) {   // power-of-two lanes: fixed lane per thread
+            const int estep = NT / lpn, e0 = tid / lpn;
+            for (int eb = e0; eb < est; eb += 4 * estep) {
+                Vec<V> a[4];
 #pragma unroll
-            for (int j = 0; j < V; ++j) {
-                float d1 = dd.x[j];
-                if (CHECK_D) {
-                    bad |= !isfinite(d1);
-                    d1 = canon0(d1);
-                }
-                const float x = relax<FWD>(a.x[j], d1);
-                acc.x[j] = first ? x : combine<FWD>(acc.x[j], x);
-            }
-        };
-        if (!hub) {
-            for (int vs = slot; has_slot && vs < nvs; vs += slots) {
-                const int j = s_vnode[vs];
-                const int eb = s_rp[j] + (vs - s_vb[j]) * PF;
-                const int ee = min(s_rp[j + 1], eb + PF);
-                Vec<V> acc;
-#pragma unroll
-                for (int k = 0; k < V; ++k) acc.x[k] = ident<FWD>();
-                // independent gathers of up to PF edges (one L2 round trip)
-                Vec<V> a[PF];
-                Vec<V> dd[PF];
-#pragma unroll
-                for (int k = 0; k < PF; ++k) {
-                    const int e = eb + k;
-                    if (e < ee) {
-                        int u;
-                        if (e < est) {
-                            u = s_nbr[e];
-                            dd[k] = ldv_s<V>(s_d + int64_t(e) * p.Sg + scol);
-                        } else {
-                            u = __ldg(p.nbr + rb + e);
-                            dd[k] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + rb + e)) * p.S + col);
-                        }
-                        a[k] = ldv_cg<V>(p.out + int64_t(u) * p.S + col);
-                    }
+                for (int r = 0; r < 4; ++r) {
+                    const int e = eb + r * estep;
+                    if (e < est) a[r] = ldv_cg<V>(p.out + int64_t(s_nbr[e]) * p.S + col);
                 }
 #pragma unroll
-                for (int k = 0; k < PF; ++k) {
-                    if (eb + k < ee) {
+                for (int r = 0; r < 4; ++r) {
+                    const int e = eb + r * estep;
+                    if (e < est) {
+                        float *dp = s_d + int64_t(e) * p.S + col;
+                        const Vec<V> dd = ldv_s<V>(dp);
+                        Vec<V> x;
 #pragma unroll
-                        for (int j2 = 0; j2 < V; ++j2) {
-                            float d1 = dd[k].x[j2];
+                        for (int j = 0; j < V; ++j) {
+                            float d1 = dd.x[j];
                             if (CHECK_D) {
                                 bad |= !isfinite(d1);
                                 d1 = canon0(d1);
                             }
-                            acc.x[j2] = combine<FWD>(acc.x[j2], relax<FWD>(a[k].x[j2], d1));
+                            x.x[j] = relax<FWD>(a[r].x[j], d1);
                         }
+                        stv_s<V>(dp, x);
                     }
                 }
-                stv_s<V>(s_part + int64_t(vs) * p.Sg + scol, acc);
             }
-        } else if (has_slot) {
+        } else {
+            const int items = est * lpn;
+            for (int q0 = tid; q0 < items; q0 += 4 * NT) {
+                Vec<V> a[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int q = q0 + r * NT;
+                    if (q < items) {
+                        const int e = q / lpn, l = q - e * lpn;
+                        a[r] = ldv_cg<V>(p.out + int64_t(s_nbr[e]) * p.S + l * V);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int q = q0 + r * NT;
+                    if (q < items) {
+                        const int e = q / lpn, l = q - e * lpn;
+                        float *dp = s_d + int64_t(e) * p.S + l * V;
+                        const Vec<V> dd = ldv_s<V>(dp);
+                        Vec<V> x;
+#pragma unroll
+                        for (int j = 0; j < V; ++j) {
+                            float d1 = dd.x[j];
+                            if (CHECK_D) {
+                                bad |= !isfinite(d1);
+                                d1 = canon0(d1);
+                            }
+                            x.x[j] = relax<FWD>(a[r].x[j], d1);
+                        }
+                        stv_s<V>(dp, x);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // (c1b) part piece: a slice of one split row; partial reduction of the staged
+        // edges by all slots, then an exact atomic max/min into the row's output
+        // (pre-set to the identity); backward folds the partial slack into run_min
+        const bool part = nn == 1 && (s_rp[1] - s_rp[0]) > p.split;
+        if (part) {
+            const int node = s_node[0];
+            const int slot = tid / lpn;
             Vec<V> acc;
 #pragma unroll
-            for (int k = 0; k < V; ++k) acc.x[k] = ident<FWD>();
-            for (int e = slot; e < E; e += slots) edge_val(e, acc, false);
-            stv_s<V>(s_part + int64_t(slot) * p.Sg + scol, acc);
-        }
-        consumer_sync();
-
-        // ---- combine each node's vslots, store, fused slack (backward) ----------
-        const int nodes_here = hub ? 1 : nn;
-        for (int j = slot; has_slot && j < nodes_here; j += slots) {
-            const int node = s_node[j];
-            Vec<V> best;
-            const bool leaf = s_rp[j + 1] == s_rp[j];
-            if (leaf) {
-                if (FWD) {
-                    const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+            for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+            if (tid < active)
+                for (int e = slot; e < est; e += slots) {
+                    const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
 #pragma unroll
-                    for (int k = 0; k < V; ++k) best.x[k] = a0;
-                } else {
-#pragma unroll
-                    for (int k = 0; k < V; ++k)
-                        best.x[k] = canon0(p.src_val ? __ldg(p.src_val + col + k) : p.t_scalar);
+                    for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
                 }
-            } else {
-                const int v0 = hub ? 0 : s_vb[j];
-                const int v1 = hub ? min(slots, E) : s_vb[j + 1];
-                best = ldv_s<V>(s_part + int64_t(v0) * p.Sg + scol);
-                for (int v = v0 + 1; v < v1; ++v) {
-                    Vec<V> q = ldv_s<V>(s_part + int64_t(v) * p.Sg + scol);
+            stv_s<V>(s_part + int64_t(tid) * V, acc);
+            __syncthreads();
+            if (tid < lpn) {
+                Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
+                for (int s2 = 1; s2 < slots; ++s2) {
+                    const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
 #pragma unroll
-                    for (int k = 0; k < V; ++k) best.x[k] = combine<FWD>(best.x[k], q.x[k]);
+                    for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
+                }
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    atomic_combine<FWD>(p.out + int64_t(node) * p.S + col + j, best.x[j]);
+                if (!FWD) {
+                    const Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        run_min.x[j] = fminf(run_min.x[j], __fsub_rn(best.x[j], a.x[j]));
                 }
             }
+        }
+        // (c2) rows reduced by their owner lanes; long rows deferred to (c3)
+        auto node_at = [&](int i) { return i < nst ? s_node[i] : __ldg(p.node_of + pos0 + i); };
+        auto rel = [&](int i) { return (i <= nst ? s_rp[i] : __ldg(p.row_ptr + pos0 + i)) - rb; };
+        auto finish = [&](int node, const Vec<V> &best, int i) {
             stv_g<V>(p.out + int64_t(node) * p.S + col, best);
             if (!FWD) {
-                Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
+                // rows i = tid/lpn and tid/lpn + slots were prefetched in (a2)
+                const int rr = i >= 0 ? (i - tid / lpn) / slots : 2;
+                const Vec<V> a = (rr < 2 && i < nst)
+                                     ? (rr == 0 ? pre_at[0] : pre_at[1])
+                                     : ldv_cg<V>(p.other + int64_t(node) * p.S + col);
                 Vec<V> sl;
 #pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    sl.x[k] = __fsub_rn(best.x[k], a.x[k]);
-                    run_min.x[k] = fminf(run_min.x[k], sl.x[k]);
+                for (int j = 0; j < V; ++j) {
+                    sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
+                    run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
                 }
                 if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
             }
+        };
+        if (tid < active && !part) {
+            for (int i = tid / lpn; i < nn; i += slots) {
+                const int eb = rel(i), ee = rel(i + 1);
+                const int deg = ee - eb;
+                if (deg > p.split) continue;   // split rows live in part pieces
+                if (deg > HUB_DEG) {
+                    if (lane == 0) {
+                        const int h = atomicAdd(&s_nhub, 1);
+                        if (h < MAX_HUBS) s_hub[h] = i;
+                        else atomicOr(p.err, 0x80000000u);   // internal invariant broken
+                    }
+                    continue;
+                }
+                const int node = node_at(i);
+                Vec<V> best;
+                if (deg == 0) {
+                    if (FWD) {
+                        const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+#pragma unroll
+                        for (int j = 0; j < V; ++j) best.x[j] = a0;
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < V; ++j)
+                            best.x[j] = canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < V; ++j) best.x[j] = ident<FWD>();
+                    for (int e = eb; e < ee; ++e) {
+                        Vec<V> x;
+                        if (e < est) {
+                            x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
+                        } else {   // row past the staged edges (piece behind a giant row)
+                            const int ge = rb + e;
+                            const Vec<V> a =
+                                ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + ge)) * p.S + col);
+                            const Vec<V> dd =
+                                ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
+#pragma unroll
+                            for (int j = 0; j < V; ++j) {
+                                float d1 = dd.x[j];
+                                if (CHECK_D) {
+                                    bad |= !isfinite(d1);
+                                    d1 = canon0(d1);
+                                }
+                                x.x[j] = relax<FWD>(a.x[j], d1);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
+                    }
+                }
+                finish(node, best, i);
+            }
         }
-        // ---- publish: stores visible at gpu scope, then bump the level counter --
-        __threadfence();
-        consumer_sync();
-        if (tid == 0) {
-            atomicAdd(p.done + g * p.L + lv, 1);
-            mbar_arrive(empty + st);
+        __syncthreads();
+        // (c3) long rows: all slots, strided partials, shared-memory combine
+        const int nhub = min(s_nhub, MAX_HUBS);
+        for (int h = 0; h < nhub; ++h) {
+            const int i = s_hub[h];
+            const int eb = rel(i), ee = rel(i + 1);
+            const int slot = tid / lpn;
+            Vec<V> acc;
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+            if (tid < active) {
+                int e = eb + slot;
+                for (; e < ee && e < est; e += slots) {
+                    const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
+                }
+                // unstaged tail: four independent gathers per step
+                for (; e < ee; e += 4 * slots) {
+                    Vec<V> a[4], dd[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int er = e + r * slots;
+                        if (er < ee) {
+                            const int ge = rb + er;
+                            a[r] = ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + ge)) * p.S + col);
+                            dd[r] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
+                        }
+                    }
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (e + r * slots < ee) {
+#pragma unroll
+                            for (int j = 0; j < V; ++j) {
+                                float d1 = dd[r].x[j];
+                                if (CHECK_D) {
+                                    bad |= !isfinite(d1);
+                                    d1 = canon0(d1);
+                                }
+                                acc.x[j] = combine<FWD>(acc.x[j], relax<FWD>(a[r].x[j], d1));
+                            }
+                        }
+                    }
+                }
+            }
+            stv_s<V>(s_part + int64_t(tid) * V, acc);
+            __syncthreads();
+            if (tid < lpn) {
+                Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
+                for (int s2 = 1; s2 < slots; ++s2) {
+                    const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
+                }
+                finish(node_at(i), best, -1);
+            }
+            __syncthreads();
         }
+
+        const unsigned long long t_comp = p.trace ? gtimer() : 0;
+        // (d) publish: stores visible at gpu scope (release), then count the piece
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) atomicAdd(p.done + kc, 1);
+        if (p.trace && tid == 0) {
+            const int r = atomicAdd(p.trace_n, 1);
+            if (r < p.trace_cap) {
+                unsigned long long *t = p.trace + int64_t(r) * 8;
+                t[0] = (unsigned long long)kc;
+                t[1] = (unsigned long long)b;
+                t[2] = t_top;
+                t[3] = t_ready;
+                t[4] = t_comp;
+                t[5] = gtimer();
+                t[6] = (unsigned long long)E;
+                t[7] = (unsigned long long)nn;
+            }
+        }
+        // (e) stage ahead, after the publish so the fence never waits on copies:
+        // delays(t+2) (its eids landed with the previous group) and rows(t+3)
+        cp_wait_all();
+        __syncthreads();
+        if (t + 2 < nseq) stage_delays(s2);
+        if (t + 3 < nseq) stage_rows(s3, nd, nlv);
+        cp_commit();
+        if (t + 4 < nseq) {   // next descriptor: consumed an iteration from now
+            nd = __ldg(p.cta_pc + seq0 + t + 4);
+            nlv = __ldg(p.cta_lv + seq0 + t + 4);
+        }
+
     }
+    cp_wait_all();
 
     if (CHECK_D && bad) atomicOr(p.err, ERR_NONFINITE);
     if (!FWD) {
-        // backward runs with one scenario group (G == 1), so lane owns scenarios
-        // lane*V .. lane*V+V-1 in every chunk
-        if (has_slot) {
+        if (tid < active) {
 #pragma unroll
-            for (int k = 0; k < V; ++k)
-                if (run_min.x[k] != ident<false>())
-                    atomicMin(s_min + lane * V + k, f2ord(run_min.x[k]));
+            for (int j = 0; j < V; ++j)
+                if (run_min.x[j] != ident<false>())
+                    atomicMin(s_min + col + j, f2ord(run_min.x[j]));
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory");
-        for (int s = tid; s < p.S; s += NCT)
+        __syncthreads();
+        for (int s = tid; s < p.S; s += NT)
             if (s_min[s] != 0x7f800000) atomicMin(p.wns_ord + s, s_min[s]);
     }
 }
@@ -520,87 +656,216 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
         if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
 }
 
-// ---- chunk schedule (per direction and T), cached in the graph ---------------
-__global__ void k_chunk_nv(const int32_t *__restrict__ row_ptr, int32_t n, int32_t *__restrict__ nv) {
+// ---- piece schedule (per direction; cached per (P, weights, split)) -----------
+// Rows of a level are in ascending degree, so the split rows (degree > split) form
+// the tail [le_normal, le) of every level.  Normal rows get weight degree + 1 and
+// are cut into weight-balanced pieces; a split row becomes ceil(deg/split) part
+// pieces of <= split edges each.
+__global__ void k_piece_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
+                             int32_t *__restrict__ w, int32_t *__restrict__ parts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int d = row_ptr[i + 1] - row_ptr[i];
-        nv[i] = max(1, (d + PF - 1) / PF);
+        w[i] = d > split ? 0 : d + 1;
+        parts[i] = d > split ? (d + split - 1) / split : 0;
     }
 }
-
-__global__ void k_chunk_flags(const int32_t *__restrict__ order, const int32_t *__restrict__ level,
-                              const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ nv,
-                              const int32_t *__restrict__ P, int32_t n, int32_t T,
-                              int32_t *__restrict__ flag) {
+__global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
+                              const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
+                              int32_t L, int32_t P, int32_t wt_cap, int32_t wt_min, int32_t split,
+                              int32_t *__restrict__ np, int32_t *__restrict__ npn,
+                              int32_t *__restrict__ lenorm) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+        const int ls = level_ptr[k], le = level_ptr[k + 1];
+        int lo = ls, hi = le;   // first row with degree > split
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
+            else lo = mid + 1;
+        }
+        const int64_t wk = int64_t(W[lo]) - W[ls];
+        const int64_t nk = lo - ls;
+        const int parts = Q[le] - Q[ls];
+        int64_t c = 0;
+        if (nk > 0) {   // keep normal + part pieces within one round of P CTAs if possible
+            c = std::max<int64_t>((wk + wt_cap - 1) / wt_cap,
+                                  std::min<int64_t>(std::max(1, P - parts),
+                                                    (wk + wt_min - 1) / wt_min));
+            c = std::max<int64_t>(1, std::min<int64_t>(nk, c));
+        }
+        npn[k] = int(c);
+        lenorm[k] = lo;
+        np[k] = int(c) + parts;
+    }
+}
+// normal piece j of level k starts at the first row whose weight prefix reaches j*W_k/np_k
+__global__ void k_piece_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
+                             const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ off,
+                             const int32_t *__restrict__ npn, const int32_t *__restrict__ lenorm,
+                             int32_t L, int4 *__restrict__ pieces) {
+    for (int k = blockIdx.x; k < L; k += gridDim.x) {
+        const int ls = level_ptr[k], le = lenorm[k];
+        const int np = npn[k];
+        const int64_t w0 = W[ls], wk = int64_t(W[le]) - w0;
+        auto start_of = [&](int jj) {
+            if (jj >= np) return le;
+            if (jj == 0) return ls;
+            const int64_t target = w0 + wk * jj / np;
+            int lo = ls, hi = le;   // first i in [ls, le] with W[i] >= target
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (W[mid] >= target) hi = mid;
+                else lo = mid + 1;
+            }
+            return lo;
+        };
+        for (int j = threadIdx.x; j < np; j += blockDim.x) {
+            const int a = start_of(j), z = start_of(j + 1);
+            pieces[off[k] + j] = make_int4(a, z, row_ptr[a], row_ptr[z]);
+        }
+    }
+}
+__global__ void k_piece_parts(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                              const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
+                              const int32_t *__restrict__ Q, const int32_t *__restrict__ off,
+                              const int32_t *__restrict__ npn, int32_t n, int32_t split,
+                              int4 *__restrict__ pieces) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int ls = level_ptr[level[order[i]]];
-        int f = 1;
-        if (i > ls) {
-            const int c = (P[i] - P[ls]) / T, cp = (P[i - 1] - P[ls]) / T;
-            f = (c != cp) || nv[i] > T || nv[i - 1] > T;
-        }
-        flag[i] = f;
+        const int rb = row_ptr[i], re = row_ptr[i + 1];
+        if (re - rb <= split) continue;
+        const int k = level[node_of[i]];
+        const int base = off[k] + npn[k] + (Q[i] - Q[level_ptr[k]]);
+        for (int t = 0; rb + t * split < re; ++t)
+            pieces[base + t] = make_int4(int(i), int(i) + 1, rb + t * split,
+                                         min(re, rb + (t + 1) * split));
     }
 }
-
-__global__ void k_chunk_scatter(const int32_t *__restrict__ flag, const int32_t *__restrict__ F,
-                                int32_t n, int32_t *__restrict__ chunk_pos) {
+// split rows: output pre-set to the identity before the pass (part pieces combine
+// into it), and their optional slack written after the pass
+__global__ void k_split_init(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                             int32_t n, int32_t split, int32_t S, float *__restrict__ out,
+                             float ident_v) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
-        if (flag[i]) chunk_pos[F[i]] = int(i);
-    if (blockIdx.x == 0 && threadIdx.x == 0) chunk_pos[F[n]] = n;
+        if (row_ptr[i + 1] - row_ptr[i] > split) {
+            float *o = out + int64_t(node_of[i]) * S;
+            for (int s = 0; s < S; ++s) o[s] = ident_v;
+        }
+}
+__global__ void k_split_slack(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                              int32_t n, int32_t split, int32_t S, const float *__restrict__ rat,
+                              const float *__restrict__ at, float *__restrict__ slack) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (row_ptr[i + 1] - row_ptr[i] > split) {
+            const int64_t o = int64_t(node_of[i]) * S;
+            for (int s = 0; s < S; ++s) slack[o + s] = __fsub_rn(rat[o + s], at[o + s]);
+        }
 }
 
-__global__ void k_chunk_levels(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ F,
-                               int32_t L, int32_t *__restrict__ chunk_ptr) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= L; k += gridDim.x * blockDim.x)
-        chunk_ptr[k] = F[level_ptr[k]];
-}
-
-void build_schedule(Graph &g, const int32_t *row_ptr, int T, DevBuf &pos_buf, DevBuf &ptr_buf,
-                    int32_t &C) {
+void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, int P, int wt_cap,
+                  int wt_min, int split, DevBuf &pieces, DevBuf &off) {
     cudaStream_t s = g.stream;
-    const int32_t n = g.n;
-    DevBuf nv, P, flag, F;
-    nv.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    P.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    F.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    HF_CUDA(cudaMemsetAsync(nv.as<int32_t>() + n, 0, sizeof(int32_t), s));
-    HF_CUDA(cudaMemsetAsync(flag.as<int32_t>() + n, 0, sizeof(int32_t), s));
-    k_chunk_nv<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, nv.as<int32_t>());
+    const int32_t n = g.n, L = g.L;
+    DevBuf w, W, q, Q, np, npn, lenorm;
+    w.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    W.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    Q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    np.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    npn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    lenorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    off.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    HF_CUDA(cudaMemsetAsync(w.as<int32_t>() + n, 0, sizeof(int32_t), s));
+    HF_CUDA(cudaMemsetAsync(q.as<int32_t>() + n, 0, sizeof(int32_t), s));
+    HF_CUDA(cudaMemsetAsync(np.as<int32_t>() + L, 0, sizeof(int32_t), s));
+    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, w.as<int32_t>(),
+                                                         q.as<int32_t>());
     HF_CHECK_LAUNCH();
-    scan_exclusive(nv.as<int32_t>(), P.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    k_chunk_flags<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-        g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), nv.as<int32_t>(),
-        P.as<int32_t>(), n, T, flag.as<int32_t>());
+    scan_exclusive(w.as<int32_t>(), W.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    scan_exclusive(q.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    k_piece_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
+        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, P, wt_cap, wt_min,
+        split, np.as<int32_t>(), npn.as<int32_t>(), lenorm.as<int32_t>());
     HF_CHECK_LAUNCH();
-    scan_exclusive(flag.as<int32_t>(), F.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    int32_t h_C = 0;
-    HF_CUDA(cudaMemcpyAsync(&h_C, F.as<int32_t>() + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    scan_exclusive(np.as<int32_t>(), off.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
+    int32_t total = 0;
+    HF_CUDA(cudaMemcpyAsync(&total, off.as<int32_t>() + L, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            s));
     HF_CUDA(cudaStreamSynchronize(s));
-    C = h_C;
-    pos_buf.alloc(sizeof(int32_t) * (int64_t(C) + 1), s);
-    ptr_buf.alloc(sizeof(int32_t) * (int64_t(g.L) + 1), s);
-    k_chunk_scatter<<<grid_for(n, 256, g.sms), 256, 0, s>>>(flag.as<int32_t>(), F.as<int32_t>(),
-                                                            n, pos_buf.as<int32_t>());
+    pieces.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
+    k_piece_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
+        g.level_ptr.as<int32_t>(), W.as<int32_t>(), row_ptr, off.as<int32_t>(),
+        npn.as<int32_t>(), lenorm.as<int32_t>(), L, pieces.as<int4>());
     HF_CHECK_LAUNCH();
-    k_chunk_levels<<<grid_for(int64_t(g.L) + 1, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), F.as<int32_t>(), g.L, ptr_buf.as<int32_t>());
+    k_piece_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+        row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q.as<int32_t>(),
+        off.as<int32_t>(), npn.as<int32_t>(), n, split, pieces.as<int4>());
     HF_CHECK_LAUNCH();
     g.launches += 5;
 }
 
-int pick_vec(int32_t Sg, std::initializer_list<const void *> ptrs) {
+__global__ void k_gather_pieces(const int4 *__restrict__ pieces, const int32_t *__restrict__ idx,
+                                int32_t total, int4 *__restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = pieces[idx[i]];
+}
+
+// Deal piece j of every level to CTA j mod P and lay each CTA's pieces out
+// contiguously in pass order, so a CTA walks its schedule with sequential loads.
+template <bool FWD> void deal_pieces(Graph &g, PieceSched &ps) {
+    cudaStream_t s = g.stream;
+    const int L = g.L, P = g.sms;
+    std::vector<int32_t> off(size_t(L) + 1);
+    HF_CUDA(cudaMemcpyAsync(off.data(), ps.off.p, sizeof(int32_t) * off.size(),
+                            cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaStreamSynchronize(s));
+    const int32_t total = off[L];
+    std::vector<int32_t> cnt(size_t(P) + 1, 0), idx(size_t(std::max(total, 1))),
+        lv(size_t(std::max(total, 1)));
+    for (int k = 0; k < L; ++k)
+        for (int j = 0; j < off[k + 1] - off[k]; ++j) cnt[size_t(j % P) + 1]++;
+    for (int c = 0; c < P; ++c) cnt[c + 1] += cnt[c];
+    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+    for (int kk = 0; kk < L; ++kk) {
+        const int k = FWD ? kk : L - 1 - kk;
+        for (int j = 0; j < off[k + 1] - off[k]; ++j) {
+            const int c = j % P;
+            idx[cur[c]] = off[k] + j;
+            lv[cur[c]] = k;
+            ++cur[c];
+        }
+    }
+    DevBuf d_idx;
+    d_idx.alloc(sizeof(int32_t) * idx.size(), s);
+    ps.cta_lv.alloc(sizeof(int32_t) * lv.size(), s);
+    ps.cta_off.alloc(sizeof(int32_t) * cnt.size(), s);
+    ps.cta_pc.alloc(sizeof(int4) * idx.size(), s);
+    HF_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), sizeof(int32_t) * idx.size(),
+                            cudaMemcpyHostToDevice, s));
+    HF_CUDA(cudaMemcpyAsync(ps.cta_lv.p, lv.data(), sizeof(int32_t) * lv.size(),
+                            cudaMemcpyHostToDevice, s));
+    HF_CUDA(cudaMemcpyAsync(ps.cta_off.p, cnt.data(), sizeof(int32_t) * cnt.size(),
+                            cudaMemcpyHostToDevice, s));
+    if (total > 0) {
+        k_gather_pieces<<<grid_for(total, 256, g.sms), 256, 0, s>>>(
+            ps.pieces.as<int4>(), d_idx.as<int32_t>(), total, ps.cta_pc.as<int4>());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+    HF_CUDA(cudaStreamSynchronize(s));   // host vectors go out of scope
+}
+
+int pick_vec(int32_t S, std::initializer_list<const void *> ptrs) {
     auto aligned = [&](int bytes) {
         for (const void *q : ptrs)
             if (q && (reinterpret_cast<uintptr_t>(q) % bytes)) return false;
         return true;
     };
-    if (Sg % 4 == 0 && aligned(16)) return 4;
-    if (Sg % 2 == 0 && aligned(8)) return 2;
+    if (S % 4 == 0 && aligned(16)) return 4;
+    if (S % 2 == 0 && aligned(8)) return 2;
     return 1;
 }
 
@@ -608,72 +873,106 @@ void prof_record(Graph &g, int idx) {
     if (g.prof) HF_CUDA(cudaEventRecord(g.ev[idx], g.stream));
 }
 
-template <int V, bool FWD, bool CHECK_D, bool BULK>
+template <int V, bool FWD, bool CHECK_D, bool VEC16>
 void launch(Graph &g, PassParams &p, size_t smem) {
-    auto kern = k_propagate<V, FWD, CHECK_D, BULK>;
+    auto kern = k_propagate<V, FWD, CHECK_D, VEC16>;
     HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
-    const int grid = std::max(1, std::min(per_sm * g.sms, p.C * p.G));
-    kern<<<grid, BLOCK, smem, g.stream>>>(p);
-    HF_CHECK_LAUNCH();
+    void *args[] = {&p};
+    // one CTA per SM; the piece schedule was built for exactly g.sms CTAs
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, NT, args, smem, g.stream));
     g.launches += 1;
 }
 
-template <bool FWD>
-void run_pass(Graph &g, PassParams &p, bool check_d, int V, bool bulk) {
-    const int lpn = p.Sg / V;
-    const int T = NCT / lpn;
-    p.T = T;
-    // chunk schedule (cached per direction and T)
-    DevBuf &pos = FWD ? g.sched_f_pos : g.sched_b_pos;
-    DevBuf &ptr = FWD ? g.sched_f_ptr : g.sched_b_ptr;
-    int32_t &C = FWD ? g.sched_f_C : g.sched_b_C;
-    int32_t &Tc = FWD ? g.sched_f_T : g.sched_b_T;
-    if (Tc != T || !pos.p) {
-        build_schedule(g, p.row_ptr, T, pos, ptr, C);
-        Tc = T;
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+inline float __int_as_float_host(uint32_t b) {
+    float f;
+    memcpy(&f, &b, 4);
+    return f;
+}
+
+template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) {
+    if (p.S / V > NT) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass (S/V > 512)");
+    // staging capacity per ring slot: ecap edges of S floats (+ two ids), ncap rows
+    const int fixed = NT * 4 * 4 + p.S * 4;
+    const int per_slot = (SMEM_BUDGET - fixed) / NBUF;
+    if (per_slot < 2048) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass");
+    int ecap = std::min(4096, std::max(8, (per_slot * 3 / 4) / (8 + 4 * p.S)));
+    int ncap = std::min(2048, std::max(16, (per_slot - ecap * (8 + 4 * p.S)) / 8 - 2));
+    p.ecap = ecap;
+    p.ncap = ncap;
+    const int wt_cap = std::max(8, std::min(ecap, ncap));
+    const int wt_min = 32;
+    const int split = std::max(HUB_DEG, ecap / 2);
+    p.split = split;
+    PieceSched &ps = FWD ? g.ps_f : g.ps_b;
+    const int32_t want = wt_cap * 4096 + g.sms;
+    if (ps.key != want || !ps.pieces.p) {
+        build_pieces(g, p.row_ptr, p.node_of, g.sms, wt_cap, wt_min, split, ps.pieces, ps.off);
+        deal_pieces<FWD>(g, ps);
+        ps.key = want;
     }
-    p.chunk_pos = pos.as<int32_t>();
-    p.chunk_ptr = ptr.as<int32_t>();
-    p.C = C;
+    p.cta_pc = ps.cta_pc.as<int4>();
+    p.cta_lv = ps.cta_lv.as<int32_t>();
+    p.cta_off = ps.cta_off.as<int32_t>();
+    p.piece_off = ps.off.as<int32_t>();
+    k_split_init<<<grid_for(g.n, 256, g.sms), 256, 0, g.stream>>>(
+        p.row_ptr, p.node_of, g.n, split, p.S, p.out,
+        __int_as_float_host(FWD ? 0xff800000u : 0x7f800000u));
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
     p.L = g.L;
-    p.ecap = std::min(2 * T * PF, std::max(64, 16384 / (4 * p.Sg)));
-    const StageLayout SL = stage_layout(T, p.ecap, p.Sg);
-    size_t smem = size_t(NB) * SL.bytes + 2 * NB * 8 + sizeof(float) * 2 * T * p.Sg +
-                  (FWD ? 0 : sizeof(int32_t) * p.S);
-    // per-pass counters: done[G*L] + ticket
-    g.ws_sync.alloc(sizeof(int32_t) * (size_t(p.G) * g.L + 1), g.stream);
-    HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(p.G) * g.L + 1), g.stream));
+    const SlotLayout SL = slot_layout(ncap, ecap, p.S);
+    const size_t smem = size_t(NBUF) * SL.bytes + size_t(fixed);
+    g.ws_sync.alloc(sizeof(int32_t) * (size_t(g.L) + 1), g.stream);
+    HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(g.L) + 1), g.stream));
     p.done = g.ws_sync.as<int32_t>();
-    p.ticket = p.done + size_t(p.G) * g.L;
     p.err = g.d_err();
-#define HF_LAUNCH(VV)                                                                       \
-    do {                                                                                    \
-        if (check_d && bulk) launch<VV, FWD, true, true>(g, p, smem);                       \
-        else if (check_d) launch<VV, FWD, true, false>(g, p, smem);                         \
-        else if (bulk) launch<VV, FWD, false, true>(g, p, smem);                            \
-        else launch<VV, FWD, false, false>(g, p, smem);                                     \
+    const bool vec16 = (p.S % 4 == 0) && (reinterpret_cast<uintptr_t>(p.d) % 16 == 0);
+    // debugging timeline: HF_TRACE=<file prefix> dumps one record per piece
+    const char *trace_env = getenv("HF_TRACE");
+    DevBuf tbuf;
+    const int tcap = 1 << 20;
+    if (trace_env) {
+        tbuf.alloc(sizeof(unsigned long long) * 8 * tcap + 16, g.stream);
+        HF_CUDA(cudaMemsetAsync(tbuf.p, 0, 16, g.stream));
+        p.trace_n = reinterpret_cast<int32_t *>(tbuf.as<unsigned char>());
+        p.trace = reinterpret_cast<unsigned long long *>(tbuf.as<unsigned char>() + 16);
+        p.trace_cap = tcap;
+    }
+#define HF_LAUNCH(VV)                                                            \
+    do {                                                                         \
+        if (check_d && vec16) launch<VV, FWD, true, true>(g, p, smem);           \
+        else if (check_d) launch<VV, FWD, true, false>(g, p, smem);              \
+        else if (vec16) launch<VV, FWD, false, true>(g, p, smem);                \
+        else launch<VV, FWD, false, false>(g, p, smem);                          \
     } while (0)
     if (V == 4) HF_LAUNCH(4);
     else if (V == 2) HF_LAUNCH(2);
     else HF_LAUNCH(1);
 #undef HF_LAUNCH
-}
-
-// scenario groups: Sg = S / G with Sg / V <= NCT
-void choose_groups(int32_t S, const std::initializer_list<const void *> &ptrs, int &G, int &Sg,
-                   int &V) {
-    G = 1;
-    while (true) {
-        if (S % G == 0) {
-            Sg = S / G;
-            V = pick_vec(Sg, ptrs);
-            if (Sg / V <= NCT) break;
+    if (trace_env) {
+        int32_t cnt = 0;
+        HF_CUDA(cudaMemcpyAsync(&cnt, p.trace_n, 4, cudaMemcpyDeviceToHost, g.stream));
+        HF_CUDA(cudaStreamSynchronize(g.stream));
+        cnt = std::min(cnt, tcap);
+        std::vector<unsigned long long> h(size_t(cnt) * 8);
+        HF_CUDA(cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+        std::string fn = std::string(trace_env) + (FWD ? "_fwd_S" : "_bwd_S") + std::to_string(p.S) +
+                         ".bin";
+        if (FILE *f = fopen(fn.c_str(), "wb")) {
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
         }
-        ++G;
-        if (G > S) fail(HF_ERR_INVALID_ARG, "cannot split scenarios into groups");
+    }
+    if (!FWD && p.slack) {
+        k_split_slack<<<grid_for(g.n, 256, g.sms), 256, 0, g.stream>>>(
+            p.row_ptr, p.node_of, g.n, split, p.S, p.out, p.other, p.slack);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
     }
 }
 
@@ -684,20 +983,16 @@ void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const flo
                     float *at) {
     if (g.n == 0) return;
     PassParams p{};
-    int G, Sg, V;
-    choose_groups(S, {d, at}, G, Sg, V);
+    const int V = pick_vec(S, {d, at});
     p.row_ptr = g.lo_in_ptr.as<int32_t>();
     p.nbr = g.lo_in_src.as<int32_t>();
     p.eid = g.lo_in_eid.as<int32_t>();
-    p.node_of = g.order.as<int32_t>();
+    p.node_of = g.lo_in_node.as<int32_t>();
     p.S = S;
-    p.Sg = Sg;
-    p.G = G;
     p.d = d;
     p.src_val = at_src;
     p.out = at;
-    const bool bulk = (Sg % 4 == 0) && (reinterpret_cast<uintptr_t>(d) % 16 == 0) && S % 4 == 0;
-    run_pass<true>(g, p, check_d, V, bulk);
+    run_pass<true>(g, p, check_d, V);
 }
 
 // Backward over all levels + slack + wns (ordered ints, decoded into wns_f[S]).
@@ -716,16 +1011,12 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
     }
     if (g.n > 0) {
         PassParams p{};
-        int G, Sg, V;
-        choose_groups(S, {d, at, rat, slack}, G, Sg, V);
-        if (G > 1) fail(HF_ERR_INVALID_ARG, "backward: more than 1024 scenarios per call");
+        const int V = pick_vec(S, {d, at, rat, slack});
         p.row_ptr = g.lo_out_ptr.as<int32_t>();
         p.nbr = g.lo_out_dst.as<int32_t>();
         p.eid = g.lo_out_eid.as<int32_t>();
-        p.node_of = g.order.as<int32_t>();
+        p.node_of = g.lo_out_node.as<int32_t>();
         p.S = S;
-        p.Sg = Sg;
-        p.G = G;
         p.d = d;
         p.src_val = t_arr;
         p.t_scalar = t_scalar;
@@ -733,8 +1024,7 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         p.out = rat;
         p.slack = slack;
         p.wns_ord = ord;
-        const bool bulk = (Sg % 4 == 0) && (reinterpret_cast<uintptr_t>(d) % 16 == 0) && S % 4 == 0;
-        run_pass<false>(g, p, false, V, bulk);
+        run_pass<false>(g, p, false, V);
     }
     if (wns_f) {
         k_ord_to_float<<<1, 256, 0, s>>>(ord, wns_f, S);
