@@ -73,6 +73,10 @@ struct PieceSched {
     DevBuf pieces;   // int4 {pos_begin, pos_end, edge_begin, edge_end}, level-major
     DevBuf off;      // [L+1] first piece of every level
     DevBuf cta_pc, cta_lv, cta_off;   // the same pieces dealt to CTAs, pass order
+    DevBuf q;                         // [n+1] first part id of every (split) row
+    DevBuf part_np;                   // [parts] parts of the row starting at that id
+    DevBuf nbr_enc;                   // [m] neighbour ids, split rows as -(part id + 1)
+    int32_t nparts = 0;
     int32_t key = -1;                 // (piece weight, CTAs) the schedule was built for
 };
 

@@ -46,8 +46,11 @@ namespace hf {
 
 namespace {
 
-constexpr int NT = 512;        // threads per CTA (one CTA per SM)
-constexpr int NBUF = 4;        // staging ring slots
+constexpr int NCW = 16;                 // consumer warps
+constexpr int NC = NCW * 32;            // consumer threads
+constexpr int NPW = 2;                  // producer warps
+constexpr int BLOCK = NC + 32 * NPW;
+constexpr int NBUF = 4;                 // staging ring slots
 constexpr int HUB_DEG = 64;    // rows longer than this are reduced by the whole CTA
 constexpr int MAX_HUBS = 256;  // long rows per piece (piece weight bounds this)
 
@@ -148,6 +151,11 @@ struct PassParams {
     int32_t L;
     int32_t ncap, ecap;        // staged rows / edges per ring slot
     int32_t split;             // rows longer than this are cut into part pieces
+    int32_t psize;             // edges per part piece
+    const int32_t *q;          // [n+1] first part id of every row (split rows)
+    const int32_t *part_np;    // [parts] number of parts of the row whose first part id it is
+    float *part_buf;           // [parts][S] partial results of part pieces
+    int32_t *part_cnt;         // [parts] parts finished, indexed by a row's first part id
     int32_t S;                 // scenarios (row stride of at / rat / delays)
     const float *d;            // [m][S]
     const float *src_val;      // forward: at_src [n] (or null); backward: t_req [S] (or null)
@@ -171,22 +179,27 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// ring-slot layout in shared memory (bytes)
+// ring-slot layout in shared memory (bytes); identical on host and device
 struct SlotLayout {
-    int node, rp, nbr, eid, d, bytes;
+    int meta, node, rp, nbr, medrow, medpre, d, bytes;
 };
+constexpr int MAXMED = 256;   // medium rows per piece (bounded by ecap / CH)
+constexpr int CH = 8;         // chunk of a medium row pre-reduced by one item
 __host__ __device__ inline SlotLayout slot_layout(int ncap, int ecap, int S) {
     SlotLayout L;
     int o = 0;
-    L.node = o; o += ncap * 4;
-    L.rp = o;   o += (ncap + 1) * 4;
-    L.nbr = o;  o += ecap * 4;
-    L.eid = o;  o += ecap * 4;
-    o = (o + 15) & ~15;
-    L.d = o;    o += ecap * S * 4;
+    L.meta = o;   o += 16 * 4;
+    L.node = o;   o += ncap * 4;
+    L.rp = o;     o += (ncap + 1) * 4;
+    L.nbr = o;    o += ecap * 4;
+    L.medrow = o; o += MAXMED * 4;
+    L.medpre = o; o += (MAXMED + 1) * 4;
+    o = (o + 127) & ~127;
+    L.d = o;      o += ecap * S * 4;
     L.bytes = (o + 127) & ~127;
     return L;
 }
+enum { MT_LV = 0, MT_POS, MT_NN, MT_RB, MT_E, MT_EST, MT_NMED, MT_PART, MT_QB };
 
 template <bool FWD> __device__ __forceinline__ float combine(float best, float x) {
     return FWD ? fmaxf(best, x) : fminf(best, x);
@@ -211,160 +224,280 @@ template <bool FWD> __device__ __forceinline__ void atomic_combine(float *addr, 
     }
 }
 
+// at[u] / rat[u] of a neighbour; a neighbour that is a split row is encoded as
+// -(first part id + 1) and read as the combine of its part partials (the row's
+// own value is finalised off the critical path)
+template <int V, bool FWD>
+__device__ __forceinline__ Vec<V> gather_val(const PassParams &p, int u, int64_t col) {
+    if (u >= 0) return ldv_cg<V>(p.out + int64_t(u) * p.S + col);
+    const int qb = -u - 1;
+    const int np = __ldg(p.part_np + qb);
+    Vec<V> a = ldv_cg<V>(p.part_buf + int64_t(qb) * p.S + col);
+    for (int k = 1; k < np; ++k) {
+        const Vec<V> b = ldv_cg<V>(p.part_buf + int64_t(qb + k) * p.S + col);
+#pragma unroll
+        for (int j = 0; j < V; ++j) a.x[j] = combine<FWD>(a.x[j], b.x[j]);
+    }
+    return a;
+}
+
 __device__ __forceinline__ int pieces_in(const PassParams &p, int k) {
     return __ldg(p.piece_off + k + 1) - __ldg(p.piece_off + k);
 }
 
-template <int V, bool FWD, bool CHECK_D, bool VEC16>
-__global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
+// ---- mbarrier / bulk-copy / named-barrier PTX ----------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred q;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, q;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {   // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
+}
+
+// One CTA per SM: warps NCW.. are producers (stage pieces into a NBUF-slot ring
+// with TMA bulk copies, off the critical path); warps 0..NCW-1 compute.
+template <int V, bool FWD, bool CHECK_D, bool BULK>
+__global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SlotLayout SL = slot_layout(p.ncap, p.ecap, p.S);
-    float *s_part = reinterpret_cast<float *>(smem + NBUF * SL.bytes);       // [NT*V]
-    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + NT * V);           // [S]
-    __shared__ int s_meta[NBUF][5];   // level, pos_begin, rows, edge_begin, edges
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NBUF * SL.bytes);
+    uint64_t *empty = full + NBUF;
+    float *s_part = reinterpret_cast<float *>(empty + NBUF);                  // [NC*V]
+    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + NC * V);           // [S]
+    float *s_row = reinterpret_cast<float *>(s_min + p.S);                    // [S]
     __shared__ int s_nhub;
     __shared__ int s_hub[MAX_HUBS];
 
     const int tid = threadIdx.x;
-    const int P = gridDim.x, b = blockIdx.x;
+    const int b = blockIdx.x;
+    const int seq0 = __ldg(p.cta_off + b), nseq = __ldg(p.cta_off + b + 1) - seq0;
+    if (tid == 0) {
+        for (int s = 0; s < NBUF; ++s) {
+            mbar_init(full + s, 32);
+            mbar_init(empty + s, NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (!FWD)
+        for (int s = tid; s < p.S; s += BLOCK) s_min[s] = 0x7f800000;
+    __syncthreads();
+
+    if (tid >= NC) {
+        // ============================ producers (NPW warps) ============================
+        // warp w stages pieces t = w, w + NPW, ...; every load of a piece depends only
+        // on its (prefetched) descriptor, so rows, neighbour ids and edge ids are
+        // fetched in one round of independent loads, then the delay rows follow as
+        // TMA bulk copies completing on the slot's mbarrier.
+        const int pw = (tid - NC) >> 5, lane = (tid - NC) & 31;
+        int4 pcn = make_int4(0, 0, 0, 0);
+        int lvn = 0;
+        if (pw < nseq) {
+            pcn = __ldg(p.cta_pc + seq0 + pw);
+            lvn = __ldg(p.cta_lv + seq0 + pw);
+        }
+        for (int t = pw; t < nseq; t += NPW) {
+            const int st = t % NBUF;
+            const int4 pc = pcn;
+            const int lvl = lvn;
+            if (t + NPW < nseq) {   // prefetch the next descriptor
+                pcn = __ldg(p.cta_pc + seq0 + t + NPW);
+                lvn = __ldg(p.cta_lv + seq0 + t + NPW);
+            }
+            mbar_wait(empty + st, ((t / NBUF) & 1) ^ 1);
+            unsigned char *sb = smem + st * SL.bytes;
+            int32_t *meta = reinterpret_cast<int32_t *>(sb + SL.meta);
+            int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
+            int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
+            int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
+            int32_t *s_mr = reinterpret_cast<int32_t *>(sb + SL.medrow);
+            int32_t *s_mp = reinterpret_cast<int32_t *>(sb + SL.medpre);
+            float *s_d = reinterpret_cast<float *>(sb + SL.d);
+            const int pos0 = pc.x, nn = pc.y - pc.x, rb = pc.z, E = pc.w - pc.z;
+            const int nst = min(nn, p.ncap), est = min(E, p.ecap);
+            const int rounds = max((nst + 1 + 127) / 128, (est + 127) / 128);
+            for (int r0 = 0; r0 < rounds; ++r0) {
+                int nd[4], rpv[4], nb[4], ev[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {   // independent loads first
+                    const int i = r0 * 128 + u * 32 + lane;
+                    if (i < nst) nd[u] = __ldg(p.node_of + pos0 + i);
+                    if (i <= nst) rpv[u] = __ldg(p.row_ptr + pos0 + i);
+                    if (i < est) {
+                        nb[u] = __ldg(p.nbr + rb + i);
+                        ev[u] = __ldg(p.eid + rb + i);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = r0 * 128 + u * 32 + lane;
+                    if (i < nst) s_node[i] = nd[u];
+                    if (i <= nst) s_rp[i] = rpv[u] - rb;
+                    if (i < est) {
+                        s_nbr[i] = nb[u];
+                        const float *src = p.d + int64_t(ev[u]) * p.S;
+                        if (BULK) {
+                            bulk_g2s(s_d + int64_t(i) * p.S, src, uint32_t(p.S) * 4u, full + st);
+                        } else {
+                            for (int c = 0; c < p.S; ++c) s_d[int64_t(i) * p.S + c] = __ldg(src + c);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            // part piece: one slice of a split row; else list the medium rows
+            const bool part = nn == 1 && (s_rp[1] - s_rp[0]) > p.split;
+            int nrow = 0, nchk = 0;
+            if (!part) {
+                for (int i0 = 0; i0 < nst; i0 += 32) {
+                    const int i = i0 + lane;
+                    int nch = 0;
+                    if (i < nst) {
+                        const int eb = s_rp[i], ee = s_rp[i + 1];
+                        if (ee - eb > CH && ee - eb <= p.split && ee <= est)
+                            nch = (ee - eb + CH - 1) / CH;
+                    }
+                    const unsigned mk = __ballot_sync(0xffffffffu, nch > 0);
+                    if (mk == 0) continue;
+                    int incl = nch;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (nch > 0) {
+                        const int slot = nrow + __popc(mk & ((1u << lane) - 1u));
+                        if (slot < MAXMED) {
+                            s_mr[slot] = i;
+                            s_mp[slot] = nchk + incl - nch;
+                        }
+                    }
+                    nrow += __popc(mk);
+                    nchk += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                if (nrow > MAXMED) {   // cannot happen with ecap/CH <= MAXMED; stay correct
+                    nrow = 0;
+                    nchk = 0;
+                }
+            }
+            if (lane == 0) {
+                s_mp[nrow] = nchk;
+                meta[MT_LV] = lvl;
+                meta[MT_POS] = pos0;
+                meta[MT_NN] = nn;
+                meta[MT_RB] = rb;
+                meta[MT_E] = E;
+                meta[MT_EST] = est;
+                meta[MT_NMED] = nrow;
+                meta[MT_PART] = part;
+                meta[MT_QB] = part ? __ldg(p.q + pos0) : 0;
+            }
+            __syncwarp();
+            if (BULK && lane == 0)
+                mbar_arrive_tx(full + st, uint32_t(est) * uint32_t(p.S) * 4u);
+            else
+                mbar_arrive(full + st);
+        }
+        return;
+    }
+
+    // ================================= consumers ==================================
+    const int warp = tid >> 5, wl = tid & 31;
     const int lpn = p.S / V;                       // lanes per node row
-    const int active = (NT / lpn) * lpn;           // threads with a fixed lane
+    const int active = (NC / lpn) * lpn;           // threads with a fixed lane
     const int slots = active / lpn;                // rows handled side by side
     const int lane = tid % lpn;
     const int64_t col = int64_t(lane) * V;
+    const bool pow2 = (lpn & (lpn - 1)) == 0;
     bool bad = false;
     Vec<V> run_min;
 #pragma unroll
     for (int k = 0; k < V; ++k) run_min.x[k] = ident<false>();
-    if (!FWD)
-        for (int s = tid; s < p.S; s += NT) s_min[s] = 0x7f800000;
-
-    // ---- staging ------------------------------------------------------------------
-    const int seq0 = __ldg(p.cta_off + b), nseq = __ldg(p.cta_off + b + 1) - seq0;
-    auto stage_rows = [&](int slot, int4 pc, int lvl) {  // phase 1: rows and ids (async)
-        unsigned char *sb = smem + slot * SL.bytes;
-        const int nn = pc.y - pc.x, E = pc.w - pc.z;
-        const int nst = min(nn, p.ncap), est = min(E, p.ecap);
-        if (tid == 0) {
-            s_meta[slot][0] = lvl;
-            s_meta[slot][1] = pc.x;
-            s_meta[slot][2] = nn;
-            s_meta[slot][3] = pc.z;
-            s_meta[slot][4] = E;
-        }
-        int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
-        int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
-        int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
-        int32_t *s_eid = reinterpret_cast<int32_t *>(sb + SL.eid);
-        for (int i = tid; i < nst; i += NT) cp_async4(s_node + i, p.node_of + pc.x + i);
-        for (int i = tid; i <= nst; i += NT) cp_async4(s_rp + i, p.row_ptr + pc.x + i);
-        for (int e = tid; e < est; e += NT) {
-            cp_async4(s_nbr + e, p.nbr + pc.z + e);
-            cp_async4(s_eid + e, p.eid + pc.z + e);
-        }
-    };
-    auto stage_delays = [&](int slot) {                  // phase 2: needs the staged eids
-        unsigned char *sb = smem + slot * SL.bytes;
-        const int est = min(s_meta[slot][4], p.ecap);
-        const int32_t *s_eid = reinterpret_cast<const int32_t *>(sb + SL.eid);
-        float *s_d = reinterpret_cast<float *>(sb + SL.d);
-        if (VEC16) {
-            const int gpr = p.S / 4;                       // 16-byte granules per row
-            if ((gpr & (gpr - 1)) == 0 && gpr <= NT) {     // fixed column per thread
-                const int c = tid & (gpr - 1), estep = NT / gpr;
-                for (int e = tid / gpr; e < est; e += estep)
-                    cp_async16(s_d + int64_t(e) * p.S + 4 * c,
-                               p.d + int64_t(s_eid[e]) * p.S + 4 * c);
-            } else {
-                for (int q = tid; q < est * gpr; q += NT) {
-                    const int e = q / gpr, c = q - e * gpr;
-                    cp_async16(s_d + int64_t(e) * p.S + 4 * c,
-                               p.d + int64_t(s_eid[e]) * p.S + 4 * c);
-                }
-            }
-        } else {
-            for (int q = tid; q < est * p.S; q += NT) {
-                const int e = q / p.S, c = q - e * p.S;
-                cp_async4(s_d + int64_t(e) * p.S + c, p.d + int64_t(s_eid[e]) * p.S + c);
-            }
-        }
-    };
-
-    // ---- prologue: groups {rows(0)}, {delays(0), rows(1)}, {delays(1), rows(2)} -----
-    // In steady state iteration t commits {delays(t+2), rows(t+3)}: delays are in
-    // flight for a whole iteration before the piece is computed.
-    if (nseq > 0) stage_rows(0, __ldg(p.cta_pc + seq0), __ldg(p.cta_lv + seq0));
-    cp_commit();
-    cp_wait_all();
-    __syncthreads();
-    if (nseq > 0) stage_delays(0);
-    if (nseq > 1) stage_rows(1, __ldg(p.cta_pc + seq0 + 1), __ldg(p.cta_lv + seq0 + 1));
-    cp_commit();
-    cp_wait_all();
-    __syncthreads();
-    if (nseq > 1) stage_delays(1);
-    if (nseq > 2) stage_rows(2, __ldg(p.cta_pc + seq0 + 2), __ldg(p.cta_lv + seq0 + 2));
-    cp_commit();
-    // descriptor of piece t+3, loaded one iteration before it is staged
-    int4 nd = make_int4(0, 0, 0, 0);
-    int nlv = 0;
-    if (nseq > 3) {
-        nd = __ldg(p.cta_pc + seq0 + 3);
-        nlv = __ldg(p.cta_lv + seq0 + 3);
-    }
 
     for (int t = 0; t < nseq; ++t) {
-        const int cur = t % NBUF, s2 = (t + 2) % NBUF, s3 = (t + 3) % NBUF;
+        const int st = t % NBUF;
         const unsigned long long t_top = p.trace ? gtimer() : 0;
-        const int kc = s_meta[cur][0];
-        // (a) backward: prefetch at[] of this thread's first rows for the slack
-        // (rows(t) landed an iteration ago; independent of the dependency)
-        Vec<V> pre_at[2];
-        if (!FWD && tid < active) {
-            const int nst0 = min(s_meta[cur][2], p.ncap);
-            const int32_t *s_node0 =
-                reinterpret_cast<const int32_t *>(smem + cur * SL.bytes + SL.node);
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int i = tid / lpn + r * slots;
-                if (i < nst0) pre_at[r] = ldv_cg<V>(p.other + int64_t(s_node0[i]) * p.S + col);
-            }
-        }
-        // (b) wait until the previous level (pass order) is fully published; a
-        // level whose only piece is this CTA's own needs no poll (same-CTA order)
-        const int dep = FWD ? kc - 1 : kc + 1;
-        if (tid == 0 && dep >= 0 && dep < p.L) {
-            const int need = pieces_in(p, dep);
-            if (!(need == 1 && b == 0)) {
-                if (ld_acquire(p.done + dep) < need)
-                    while (ld_acquire(p.done + dep) < need) __nanosleep(32);
-            }
-        }
-        if (tid == 0) s_nhub = 0;
-        // the group {delays(t), rows(t+1)} (committed two iterations ago) has landed
-        cp_wait_prev();
-        __syncthreads();
-
-        const unsigned long long t_ready = p.trace ? gtimer() : 0;
-        // (c) compute the piece in slot `cur`
-        unsigned char *sb = smem + cur * SL.bytes;
-        const int pos0 = s_meta[cur][1], nn = s_meta[cur][2], rb = s_meta[cur][3];
-        const int E = s_meta[cur][4];
-        const int est = min(E, p.ecap), nst = min(nn, p.ncap);
+        mbar_wait(full + st, (t / NBUF) & 1);
+        unsigned char *sb = smem + st * SL.bytes;
+        const int32_t *meta = reinterpret_cast<const int32_t *>(sb + SL.meta);
         const int32_t *s_node = reinterpret_cast<const int32_t *>(sb + SL.node);
         const int32_t *s_rp = reinterpret_cast<const int32_t *>(sb + SL.rp);
         const int32_t *s_nbr = reinterpret_cast<const int32_t *>(sb + SL.nbr);
+        const int32_t *s_mr = reinterpret_cast<const int32_t *>(sb + SL.medrow);
+        const int32_t *s_mp = reinterpret_cast<const int32_t *>(sb + SL.medpre);
         float *s_d = reinterpret_cast<float *>(sb + SL.d);
-        // (c1) edge-parallel: x = fl(a[u] +/- d), written in place over the delay;
-        // up to 4 items per thread issue their gathers together (one L2 round trip)
-        if ((lpn & (lpn - 1)) == 0) {   // power-of-two lanes: fixed lane per thread
-            const int estep = NT / lpn, e0 = tid / lpn;
+        const int kc = meta[MT_LV], pos0 = meta[MT_POS], nn = meta[MT_NN], rb = meta[MT_RB];
+        const int E = meta[MT_E], est = meta[MT_EST], nmed = meta[MT_NMED];
+        const bool part = meta[MT_PART] != 0;
+        const int nst = min(nn, p.ncap);
+        // split-row bookkeeping, read now: the slot is recycled once the piece publishes
+        const int part_node = part ? s_node[0] : 0;
+        const int part_qb = part ? meta[MT_QB] : 0;
+        const int part_n = part ? (s_rp[1] - s_rp[0] + p.psize - 1) / p.psize : 0;
+
+        // (a) backward: prefetch at[] of this thread's first two rows (for the slack)
+        Vec<V> pre_at[2];
+        if (!FWD && tid < active) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int i = tid / lpn + r * slots;
+                if (i < nst) pre_at[r] = ldv_cg<V>(p.other + int64_t(s_node[i]) * p.S + col);
+            }
+        }
+        // (b) wait until the previous level (pass order) is fully published; a level
+        // whose only piece was this CTA's needs no poll (named barriers order it)
+        const int dep = FWD ? kc - 1 : kc + 1;
+        if (tid == 0 && dep >= 0 && dep < p.L) {
+            const int np = pieces_in(p, dep);
+            if (!(np == 1 && b == 0)) {
+                const int need = np;
+                if (ld_acquire(p.done + dep) < need)
+                    while (ld_acquire(p.done + dep) < need) __nanosleep(20);
+            }
+        }
+        consumer_sync();
+        const unsigned long long t_ready = p.trace ? gtimer() : 0;
+        if (tid == 0) s_nhub = 0;
+
+        // (c1) edge-parallel: x = fl(a[u] +/- d) in place over the staged delay; up to
+        // four items per thread issue their gathers together (one L2 round trip)
+        if (pow2) {
+            const int estep = NC / lpn, e0 = tid / lpn;
             for (int eb = e0; eb < est; eb += 4 * estep) {
                 Vec<V> a[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const int e = eb + r * estep;
-                    if (e < est) a[r] = ldv_cg<V>(p.out + int64_t(s_nbr[e]) * p.S + col);
+                    if (e < est) a[r] = gather_val<V, FWD>(p, s_nbr[e], col);
                 }
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -387,83 +520,31 @@ __global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
                 }
             }
         } else {
-            const int items = est * lpn;
-            for (int q0 = tid; q0 < items; q0 += 4 * NT) {
-                Vec<V> a[4];
+            for (int q = tid; q < est * lpn; q += NC) {
+                const int e = q / lpn, l = q - e * lpn;
+                float *dp = s_d + int64_t(e) * p.S + l * V;
+                const Vec<V> dd = ldv_s<V>(dp);
+                const Vec<V> a = gather_val<V, FWD>(p, s_nbr[e], int64_t(l) * V);
+                Vec<V> x;
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int q = q0 + r * NT;
-                    if (q < items) {
-                        const int e = q / lpn, l = q - e * lpn;
-                        a[r] = ldv_cg<V>(p.out + int64_t(s_nbr[e]) * p.S + l * V);
+                for (int j = 0; j < V; ++j) {
+                    float d1 = dd.x[j];
+                    if (CHECK_D) {
+                        bad |= !isfinite(d1);
+                        d1 = canon0(d1);
                     }
+                    x.x[j] = relax<FWD>(a.x[j], d1);
                 }
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int q = q0 + r * NT;
-                    if (q < items) {
-                        const int e = q / lpn, l = q - e * lpn;
-                        float *dp = s_d + int64_t(e) * p.S + l * V;
-                        const Vec<V> dd = ldv_s<V>(dp);
-                        Vec<V> x;
-#pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            float d1 = dd.x[j];
-                            if (CHECK_D) {
-                                bad |= !isfinite(d1);
-                                d1 = canon0(d1);
-                            }
-                            x.x[j] = relax<FWD>(a[r].x[j], d1);
-                        }
-                        stv_s<V>(dp, x);
-                    }
-                }
+                stv_s<V>(dp, x);
             }
         }
-        __syncthreads();
-        // (c1b) part piece: a slice of one split row; partial reduction of the staged
-        // edges by all slots, then an exact atomic max/min into the row's output
-        // (pre-set to the identity); backward folds the partial slack into run_min
-        const bool part = nn == 1 && (s_rp[1] - s_rp[0]) > p.split;
-        if (part) {
-            const int node = s_node[0];
-            const int slot = tid / lpn;
-            Vec<V> acc;
-#pragma unroll
-            for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
-            if (tid < active)
-                for (int e = slot; e < est; e += slots) {
-                    const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
-                }
-            stv_s<V>(s_part + int64_t(tid) * V, acc);
-            __syncthreads();
-            if (tid < lpn) {
-                Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
-                for (int s2 = 1; s2 < slots; ++s2) {
-                    const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
-                }
-#pragma unroll
-                for (int j = 0; j < V; ++j)
-                    atomic_combine<FWD>(p.out + int64_t(node) * p.S + col + j, best.x[j]);
-                if (!FWD) {
-                    const Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
-#pragma unroll
-                    for (int j = 0; j < V; ++j)
-                        run_min.x[j] = fminf(run_min.x[j], __fsub_rn(best.x[j], a.x[j]));
-                }
-            }
-        }
-        // (c2) rows reduced by their owner lanes; long rows deferred to (c3)
+        consumer_sync();
+
         auto node_at = [&](int i) { return i < nst ? s_node[i] : __ldg(p.node_of + pos0 + i); };
-        auto rel = [&](int i) { return (i <= nst ? s_rp[i] : __ldg(p.row_ptr + pos0 + i)) - rb; };
+        auto rel = [&](int i) { return i <= nst ? s_rp[i] : __ldg(p.row_ptr + pos0 + i) - rb; };
         auto finish = [&](int node, const Vec<V> &best, int i) {
             stv_g<V>(p.out + int64_t(node) * p.S + col, best);
             if (!FWD) {
-                // rows i = tid/lpn and tid/lpn + slots were prefetched in (a2)
                 const int rr = i >= 0 ? (i - tid / lpn) / slots : 2;
                 const Vec<V> a = (rr < 2 && i < nst)
                                      ? (rr == 0 ? pre_at[0] : pre_at[1])
@@ -477,108 +558,56 @@ __global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
                 if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
             }
         };
-        if (tid < active && !part) {
-            for (int i = tid / lpn; i < nn; i += slots) {
-                const int eb = rel(i), ee = rel(i + 1);
-                const int deg = ee - eb;
-                if (deg > p.split) continue;   // split rows live in part pieces
-                if (deg > HUB_DEG) {
-                    if (lane == 0) {
-                        const int h = atomicAdd(&s_nhub, 1);
-                        if (h < MAX_HUBS) s_hub[h] = i;
-                        else atomicOr(p.err, 0x80000000u);   // internal invariant broken
+        // gather-reduce of unstaged edges [e, ee) with stride `step` (rare paths)
+        auto tail = [&](int e, int ee, int step, Vec<V> &acc) {   // rare paths
+            for (; e < ee; e += 2 * step) {
+                Vec<V> a[2], dd[2];
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int er = e + r * step;
+                    if (er < ee) {
+                        const int ge = rb + er;
+                        a[r] = gather_val<V, FWD>(p, __ldg(p.nbr + ge), col);
+                        dd[r] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
                     }
-                    continue;
                 }
-                const int node = node_at(i);
-                Vec<V> best;
-                if (deg == 0) {
-                    if (FWD) {
-                        const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
 #pragma unroll
-                        for (int j = 0; j < V; ++j) best.x[j] = a0;
-                    } else {
+                for (int r = 0; r < 2; ++r) {
+                    if (e + r * step < ee) {
 #pragma unroll
-                        for (int j = 0; j < V; ++j)
-                            best.x[j] = canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < V; ++j) best.x[j] = ident<FWD>();
-                    for (int e = eb; e < ee; ++e) {
-                        Vec<V> x;
-                        if (e < est) {
-                            x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
-                        } else {   // row past the staged edges (piece behind a giant row)
-                            const int ge = rb + e;
-                            const Vec<V> a =
-                                ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + ge)) * p.S + col);
-                            const Vec<V> dd =
-                                ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
-#pragma unroll
-                            for (int j = 0; j < V; ++j) {
-                                float d1 = dd.x[j];
-                                if (CHECK_D) {
-                                    bad |= !isfinite(d1);
-                                    d1 = canon0(d1);
-                                }
-                                x.x[j] = relax<FWD>(a.x[j], d1);
+                        for (int j = 0; j < V; ++j) {
+                            float d1 = dd[r].x[j];
+                            if (CHECK_D) {
+                                bad |= !isfinite(d1);
+                                d1 = canon0(d1);
                             }
+                            acc.x[j] = combine<FWD>(acc.x[j], relax<FWD>(a[r].x[j], d1));
                         }
-#pragma unroll
-                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
                     }
                 }
-                finish(node, best, i);
             }
-        }
-        __syncthreads();
-        // (c3) long rows: all slots, strided partials, shared-memory combine
-        const int nhub = min(s_nhub, MAX_HUBS);
-        for (int h = 0; h < nhub; ++h) {
-            const int i = s_hub[h];
-            const int eb = rel(i), ee = rel(i + 1);
+        };
+
+        if (part) {
+            // (c1b) one slice of a split row: partial over the staged edges by all slots,
+            // stored to the row's part buffer; the last slice to finish (atomic count)
+            // combines all partials and writes the row -- exact, no float atomics
+            const int node = s_node[0];
             const int slot = tid / lpn;
+            const int deg = s_rp[1] - s_rp[0];
+            const int nparts = (deg + p.psize - 1) / p.psize;
+            const int pid = meta[MT_QB] + (-s_rp[0]) / p.psize;
             Vec<V> acc;
 #pragma unroll
             for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
-            if (tid < active) {
-                int e = eb + slot;
-                for (; e < ee && e < est; e += slots) {
+            if (tid < active)
+                for (int e = slot; e < est; e += slots) {
                     const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
 #pragma unroll
                     for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
                 }
-                // unstaged tail: four independent gathers per step
-                for (; e < ee; e += 4 * slots) {
-                    Vec<V> a[4], dd[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const int er = e + r * slots;
-                        if (er < ee) {
-                            const int ge = rb + er;
-                            a[r] = ldv_cg<V>(p.out + int64_t(__ldg(p.nbr + ge)) * p.S + col);
-                            dd[r] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
-                        }
-                    }
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        if (e + r * slots < ee) {
-#pragma unroll
-                            for (int j = 0; j < V; ++j) {
-                                float d1 = dd[r].x[j];
-                                if (CHECK_D) {
-                                    bad |= !isfinite(d1);
-                                    d1 = canon0(d1);
-                                }
-                                acc.x[j] = combine<FWD>(acc.x[j], relax<FWD>(a[r].x[j], d1));
-                            }
-                        }
-                    }
-                }
-            }
             stv_s<V>(s_part + int64_t(tid) * V, acc);
-            __syncthreads();
+            consumer_sync();
             if (tid < lpn) {
                 Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
                 for (int s2 = 1; s2 < slots; ++s2) {
@@ -586,44 +615,181 @@ __global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
 #pragma unroll
                     for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
                 }
-                finish(node_at(i), best, -1);
+                if (nparts == 1) {   // the whole row: final value directly
+                    stv_g<V>(p.out + int64_t(node) * p.S + col, best);
+                    if (!FWD) {
+                        const Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
+                        Vec<V> sl;
+#pragma unroll
+                        for (int j = 0; j < V; ++j) {
+                            sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
+                            run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
+                        }
+                        if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
+                    }
+                } else {   // readers combine the partials; finalised after the publish
+                    stv_g<V>(p.part_buf + int64_t(pid) * p.S + col, best);
+                }
             }
-            __syncthreads();
+        } else {
+            // (c1c) medium rows: every CH-edge chunk pre-reduced in place (partial over
+            // the chunk's first edge) by all threads in parallel
+            if (nmed > 0) {
+                const int items = s_mp[nmed] * lpn;
+                for (int q = tid; q < items; q += NC) {
+                    const int c = q / lpn, l = q - c * lpn;
+                    int lo = 0, hi = nmed - 1;   // last r with s_mp[r] <= c
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_mp[mid] <= c) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    const int i = s_mr[lo];
+                    const int eb = s_rp[i] + (c - s_mp[lo]) * CH;
+                    const int ee = min(s_rp[i + 1], eb + CH);
+                    float *dp = s_d + int64_t(eb) * p.S + l * V;
+                    Vec<V> acc = ldv_s<V>(dp);
+                    for (int e = eb + 1; e < ee; ++e) {
+                        const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + l * V);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
+                    }
+                    stv_s<V>(dp, acc);
+                }
+                consumer_sync();
+            }
+            // (c2) rows reduced by their owner lanes; unstaged long rows deferred
+            if (tid < active) {
+                for (int i = tid / lpn; i < nn; i += slots) {
+                    const int eb = rel(i), ee = rel(i + 1);
+                    const int deg = ee - eb;
+                    if (deg > p.split) continue;   // split rows live in part pieces
+                    const bool chunked = deg > CH && ee <= est && nmed > 0 && i < nst;
+                    if (deg > HUB_DEG && ee > est) {
+                        if (lane == 0) {
+                            const int h = atomicAdd(&s_nhub, 1);
+                            if (h < MAX_HUBS) s_hub[h] = i;
+                            else atomicOr(p.err, 0x80000000u);
+                        }
+                        continue;
+                    }
+                    const int node = node_at(i);
+                    Vec<V> best;
+                    if (deg == 0) {
+                        if (FWD) {
+                            const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+#pragma unroll
+                            for (int j = 0; j < V; ++j) best.x[j] = a0;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < V; ++j)
+                                best.x[j] =
+                                    canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < V; ++j) best.x[j] = ident<FWD>();
+                        const int es = min(ee, est);
+                        for (int e = eb; e < es; e += chunked ? CH : 1) {
+                            const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
+#pragma unroll
+                            for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
+                        }
+                        if (ee > es) tail(max(eb, es), ee, 1, best);
+                    }
+                    finish(node, best, i);
+                }
+            }
+            consumer_sync();
+            // (c3) unstaged long rows: all slots, strided, shared-memory combine
+            const int nhub = min(s_nhub, MAX_HUBS);
+            for (int h = 0; h < nhub; ++h) {
+                const int i = s_hub[h];
+                const int eb = rel(i), ee = rel(i + 1);
+                const int slot = tid / lpn;
+                Vec<V> acc;
+#pragma unroll
+                for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+                if (tid < active) {
+                    int e = eb + slot;
+                    for (; e < ee && e < est; e += slots) {
+                        const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
+                    }
+                    tail(e, ee, slots, acc);
+                }
+                stv_s<V>(s_part + int64_t(tid) * V, acc);
+                consumer_sync();
+                if (tid < lpn) {
+                    Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
+                    for (int s2 = 1; s2 < slots; ++s2) {
+                        const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
+                    }
+                    finish(node_at(i), best, -1);
+                }
+                consumer_sync();
+            }
         }
-
+        // (d) publish: every warp releases its stores at gpu scope, the slot goes back
+        // to the producer, and one thread counts the piece after all warps fenced
         const unsigned long long t_comp = p.trace ? gtimer() : 0;
-        // (d) publish: stores visible at gpu scope (release), then count the piece
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        __syncthreads();
+        __syncwarp();
+        if (wl == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            mbar_arrive(empty + st);
+        }
+        consumer_sync();
         if (tid == 0) atomicAdd(p.done + kc, 1);
+        // a split row is finalised by its last part, off the critical path (readers
+        // use the partials): its value, slack and worst-slack contribution
+        if (part) {
+            const int nparts = part_n;
+            if (nparts > 1) {
+                if (tid == 0) {
+                    const int qb = part_qb;
+                    int done_parts;
+                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
+                                 : "=r"(done_parts)
+                                 : "l"(p.part_cnt + qb)
+                                 : "memory");
+                    s_nhub = done_parts == nparts - 1 ? -1 : 0;   // flag
+                }
+                consumer_sync();
+                if (s_nhub < 0) {
+                    const int qb = part_qb, node = part_node;
+                    for (int s2 = tid; s2 < p.S; s2 += NC) {
+                        float v = ident<FWD>();
+                        for (int k = 0; k < nparts; ++k)
+                            v = combine<FWD>(v, __ldcg(p.part_buf + int64_t(qb + k) * p.S + s2));
+                        __stcg(p.out + int64_t(node) * p.S + s2, v);
+                        if (!FWD) {
+                            const float sl =
+                                __fsub_rn(v, __ldcg(p.other + int64_t(node) * p.S + s2));
+                            atomicMin(s_min + s2, f2ord(sl));
+                            if (p.slack) __stcg(p.slack + int64_t(node) * p.S + s2, sl);
+                        }
+                    }
+                }
+            }
+        }
         if (p.trace && tid == 0) {
             const int r = atomicAdd(p.trace_n, 1);
             if (r < p.trace_cap) {
-                unsigned long long *t = p.trace + int64_t(r) * 8;
-                t[0] = (unsigned long long)kc;
-                t[1] = (unsigned long long)b;
-                t[2] = t_top;
-                t[3] = t_ready;
-                t[4] = t_comp;
-                t[5] = gtimer();
-                t[6] = (unsigned long long)E;
-                t[7] = (unsigned long long)nn;
+                unsigned long long *tr = p.trace + int64_t(r) * 8;
+                tr[0] = (unsigned long long)kc;
+                tr[1] = (unsigned long long)b;
+                tr[2] = t_top;
+                tr[3] = t_ready;
+                tr[4] = t_comp;
+                tr[5] = gtimer();
+                tr[6] = (unsigned long long)E;
+                tr[7] = (unsigned long long)nn;
             }
         }
-        // (e) stage ahead, after the publish so the fence never waits on copies:
-        // delays(t+2) (its eids landed with the previous group) and rows(t+3)
-        cp_wait_all();
-        __syncthreads();
-        if (t + 2 < nseq) stage_delays(s2);
-        if (t + 3 < nseq) stage_rows(s3, nd, nlv);
-        cp_commit();
-        if (t + 4 < nseq) {   // next descriptor: consumed an iteration from now
-            nd = __ldg(p.cta_pc + seq0 + t + 4);
-            nlv = __ldg(p.cta_lv + seq0 + t + 4);
-        }
-
     }
-    cp_wait_all();
 
     if (CHECK_D && bad) atomicOr(p.err, ERR_NONFINITE);
     if (!FWD) {
@@ -633,8 +799,8 @@ __global__ void __launch_bounds__(NT, 1) k_propagate(PassParams p) {
                 if (run_min.x[j] != ident<false>())
                     atomicMin(s_min + col + j, f2ord(run_min.x[j]));
         }
-        __syncthreads();
-        for (int s = tid; s < p.S; s += NT)
+        consumer_sync();
+        for (int s = tid; s < p.S; s += NC)
             if (s_min[s] != 0x7f800000) atomicMin(p.wns_ord + s, s_min[s]);
     }
 }
@@ -662,18 +828,18 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
 // are cut into weight-balanced pieces; a split row becomes ceil(deg/split) part
 // pieces of <= split edges each.
 __global__ void k_piece_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                             int32_t *__restrict__ w, int32_t *__restrict__ parts) {
+                             int32_t psize, int32_t *__restrict__ w, int32_t *__restrict__ parts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int d = row_ptr[i + 1] - row_ptr[i];
-        w[i] = d > split ? 0 : d + 1;
-        parts[i] = d > split ? (d + split - 1) / split : 0;
+        w[i] = d > split ? 0 : 2 * d + 1;   // an edge moves ~2x the bytes of a row
+        parts[i] = d > split ? (d + psize - 1) / psize : 0;
     }
 }
 __global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
                               const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
-                              int32_t L, int32_t P, int32_t wt_cap, int32_t wt_min, int32_t split,
-                              int32_t *__restrict__ np, int32_t *__restrict__ npn,
+                              int32_t L, int32_t P, int32_t ecap, int32_t ncap, int32_t wt_min,
+                              int32_t split, int32_t *__restrict__ np, int32_t *__restrict__ npn,
                               int32_t *__restrict__ lenorm) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
         const int ls = level_ptr[k], le = level_ptr[k + 1];
@@ -683,14 +849,18 @@ __global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32
             if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
             else lo = mid + 1;
         }
-        const int64_t wk = int64_t(W[lo]) - W[ls];
+        const int64_t wk = int64_t(W[lo]) - W[ls];   // 2*edges + rows of the normal rows
         const int64_t nk = lo - ls;
+        const int64_t ek = (wk - nk) / 2;
         const int parts = Q[le] - Q[ls];
         int64_t c = 0;
-        if (nk > 0) {   // keep normal + part pieces within one round of P CTAs if possible
-            c = std::max<int64_t>((wk + wt_cap - 1) / wt_cap,
-                                  std::min<int64_t>(std::max(1, P - parts),
-                                                    (wk + wt_min - 1) / wt_min));
+        if (nk > 0) {
+            // enough pieces to fit a ring slot (3/4 of its edge and row capacity), else
+            // one per CTA left after the part pieces, so a level is a single round
+            const int64_t need = std::max<int64_t>((ek * 4 + 3 * ecap - 1) / (3 * ecap),
+                                                   (nk * 4 + 3 * ncap - 1) / (3 * ncap));
+            c = std::max<int64_t>(need, std::min<int64_t>(std::max(1, P - parts),
+                                                          (wk + wt_min - 1) / wt_min));
             c = std::max<int64_t>(1, std::min<int64_t>(nk, c));
         }
         npn[k] = int(c);
@@ -729,46 +899,51 @@ __global__ void k_piece_parts(const int32_t *__restrict__ row_ptr, const int32_t
                               const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
                               const int32_t *__restrict__ Q, const int32_t *__restrict__ off,
                               const int32_t *__restrict__ npn, int32_t n, int32_t split,
-                              int4 *__restrict__ pieces) {
+                              int32_t psize, int4 *__restrict__ pieces) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int rb = row_ptr[i], re = row_ptr[i + 1];
         if (re - rb <= split) continue;
         const int k = level[node_of[i]];
         const int base = off[k] + npn[k] + (Q[i] - Q[level_ptr[k]]);
-        for (int t = 0; rb + t * split < re; ++t)
-            pieces[base + t] = make_int4(int(i), int(i) + 1, rb + t * split,
-                                         min(re, rb + (t + 1) * split));
+        for (int t = 0; rb + t * psize < re; ++t)
+            pieces[base + t] = make_int4(int(i), int(i) + 1, rb + t * psize,
+                                         min(re, rb + (t + 1) * psize));
     }
 }
-// split rows: output pre-set to the identity before the pass (part pieces combine
-// into it), and their optional slack written after the pass
-__global__ void k_split_init(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
-                             int32_t n, int32_t split, int32_t S, float *__restrict__ out,
-                             float ident_v) {
+// neighbour ids with split rows encoded as -(first part id + 1), and parts per row
+__global__ void k_pos_of(const int32_t *__restrict__ node_of, int32_t n, int32_t *__restrict__ pos) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
-        if (row_ptr[i + 1] - row_ptr[i] > split) {
-            float *o = out + int64_t(node_of[i]) * S;
-            for (int s = 0; s < S; ++s) o[s] = ident_v;
-        }
+        pos[node_of[i]] = int(i);
 }
-__global__ void k_split_slack(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
-                              int32_t n, int32_t split, int32_t S, const float *__restrict__ rat,
-                              const float *__restrict__ at, float *__restrict__ slack) {
+__global__ void k_part_np(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ Q,
+                          int32_t n, int32_t split, int32_t psize, int32_t *__restrict__ part_np) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        if (row_ptr[i + 1] - row_ptr[i] > split) {
-            const int64_t o = int64_t(node_of[i]) * S;
-            for (int s = 0; s < S; ++s) slack[o + s] = __fsub_rn(rat[o + s], at[o + s]);
-        }
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int d = row_ptr[i + 1] - row_ptr[i];
+        if (d > split) part_np[Q[i]] = (d + psize - 1) / psize;
+    }
+}
+__global__ void k_nbr_enc(const int32_t *__restrict__ nbr, int32_t m, const int32_t *__restrict__ pos,
+                          const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ Q,
+                          int32_t split, int32_t psize, int32_t *__restrict__ enc) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int v = nbr[e];
+        const int i = pos[v];
+        const int d = row_ptr[i + 1] - row_ptr[i];
+        // only rows cut into >= 2 parts are read through their partials
+        enc[e] = (d > split && d > psize) ? -(Q[i] + 1) : v;
+    }
 }
 
-void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, int P, int wt_cap,
-                  int wt_min, int split, DevBuf &pieces, DevBuf &off) {
+void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *nbr,
+                  int P, int ecap, int ncap, int wt_min, int split, int psize, PieceSched &ps) {
     cudaStream_t s = g.stream;
     const int32_t n = g.n, L = g.L;
-    DevBuf w, W, q, Q, np, npn, lenorm;
+    DevBuf w, W, q, np, npn, lenorm;
+    DevBuf &Q = ps.q, &off = ps.off, &pieces = ps.pieces;
     w.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     W.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
@@ -780,19 +955,21 @@ void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, int 
     HF_CUDA(cudaMemsetAsync(w.as<int32_t>() + n, 0, sizeof(int32_t), s));
     HF_CUDA(cudaMemsetAsync(q.as<int32_t>() + n, 0, sizeof(int32_t), s));
     HF_CUDA(cudaMemsetAsync(np.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, w.as<int32_t>(),
-                                                         q.as<int32_t>());
+    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, psize,
+                                                         w.as<int32_t>(), q.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(w.as<int32_t>(), W.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
     scan_exclusive(q.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
     k_piece_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, P, wt_cap, wt_min,
-        split, np.as<int32_t>(), npn.as<int32_t>(), lenorm.as<int32_t>());
+        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, P, ecap, ncap,
+        wt_min, split, np.as<int32_t>(), npn.as<int32_t>(), lenorm.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(np.as<int32_t>(), off.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
     int32_t total = 0;
     HF_CUDA(cudaMemcpyAsync(&total, off.as<int32_t>() + L, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             s));
+    HF_CUDA(cudaMemcpyAsync(&ps.nparts, Q.as<int32_t>() + n, sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s));
     HF_CUDA(cudaStreamSynchronize(s));
     pieces.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
     k_piece_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
@@ -801,8 +978,32 @@ void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, int 
     HF_CHECK_LAUNCH();
     k_piece_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
         row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q.as<int32_t>(),
-        off.as<int32_t>(), npn.as<int32_t>(), n, split, pieces.as<int4>());
+        off.as<int32_t>(), npn.as<int32_t>(), n, split, psize, pieces.as<int4>());
     HF_CHECK_LAUNCH();
+    // neighbours that are split rows, and the part count of every split row
+    const int32_t m = g.m;
+    ps.nbr_enc.alloc(sizeof(int32_t) * size_t(m > 0 ? m : 1), s);
+    ps.part_np.alloc(sizeof(int32_t) * size_t(std::max(ps.nparts, 1)), s);
+    if (ps.nparts == 0) {
+        if (m)
+            HF_CUDA(cudaMemcpyAsync(ps.nbr_enc.p, nbr, sizeof(int32_t) * size_t(m),
+                                    cudaMemcpyDeviceToDevice, s));
+    } else {
+        DevBuf pos;
+        pos.alloc(sizeof(int32_t) * size_t(n), s);
+        k_pos_of<<<grid_for(n, 256, g.sms), 256, 0, s>>>(node_of, n, pos.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        k_part_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, Q.as<int32_t>(), n, split,
+                                                          psize, ps.part_np.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        if (m) {
+            k_nbr_enc<<<grid_for(m, 256, g.sms), 256, 0, s>>>(nbr, m, pos.as<int32_t>(), row_ptr,
+                                                              Q.as<int32_t>(), split, psize,
+                                                              ps.nbr_enc.as<int32_t>());
+            HF_CHECK_LAUNCH();
+        }
+        g.launches += 3;
+    }
     g.launches += 5;
 }
 
@@ -878,11 +1079,11 @@ void launch(Graph &g, PassParams &p, size_t smem) {
     auto kern = k_propagate<V, FWD, CHECK_D, VEC16>;
     HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
     void *args[] = {&p};
     // one CTA per SM; the piece schedule was built for exactly g.sms CTAs
-    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, NT, args, smem, g.stream));
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, BLOCK, args, smem, g.stream));
     g.launches += 1;
 }
 
@@ -895,23 +1096,24 @@ inline float __int_as_float_host(uint32_t b) {
 }
 
 template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) {
-    if (p.S / V > NT) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass (S/V > 512)");
-    // staging capacity per ring slot: ecap edges of S floats (+ two ids), ncap rows
-    const int fixed = NT * 4 * 4 + p.S * 4;
-    const int per_slot = (SMEM_BUDGET - fixed) / NBUF;
+    if (p.S / V > NC) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass (S/V > 512)");
+    // staging capacity per ring slot: ecap edges of S floats (+ id), ncap rows
+    const int fixed = 2 * NBUF * 8 + NC * 4 * 4 + 2 * p.S * 4;
+    const int per_slot = (SMEM_BUDGET - fixed) / NBUF - 2 * MAXMED * 4 - 256;
     if (per_slot < 2048) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass");
-    int ecap = std::min(4096, std::max(8, (per_slot * 3 / 4) / (8 + 4 * p.S)));
-    int ncap = std::min(2048, std::max(16, (per_slot - ecap * (8 + 4 * p.S)) / 8 - 2));
+    int ecap = std::min(std::min(4096, CH * MAXMED),
+                        std::max(8, (per_slot - 256 * 8) / (4 + 4 * p.S)));
+    int ncap = std::min(2048, std::max(16, (per_slot - ecap * (4 + 4 * p.S)) / 8 - 2));
     p.ecap = ecap;
     p.ncap = ncap;
-    const int wt_cap = std::max(8, std::min(ecap, ncap));
     const int wt_min = 32;
-    const int split = std::max(HUB_DEG, ecap / 2);
+    const int split = std::max(32, ecap / 4);
     p.split = split;
+    p.psize = ecap;
     PieceSched &ps = FWD ? g.ps_f : g.ps_b;
-    const int32_t want = wt_cap * 4096 + g.sms;
+    const int32_t want = (ecap * 4096 + ncap) * 8 + (g.sms & 7);
     if (ps.key != want || !ps.pieces.p) {
-        build_pieces(g, p.row_ptr, p.node_of, g.sms, wt_cap, wt_min, split, ps.pieces, ps.off);
+        build_pieces(g, p.row_ptr, p.node_of, p.nbr, g.sms, ecap, ncap, wt_min, split, ecap, ps);
         deal_pieces<FWD>(g, ps);
         ps.key = want;
     }
@@ -919,18 +1121,25 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
     p.cta_lv = ps.cta_lv.as<int32_t>();
     p.cta_off = ps.cta_off.as<int32_t>();
     p.piece_off = ps.off.as<int32_t>();
-    k_split_init<<<grid_for(g.n, 256, g.sms), 256, 0, g.stream>>>(
-        p.row_ptr, p.node_of, g.n, split, p.S, p.out,
-        __int_as_float_host(FWD ? 0xff800000u : 0x7f800000u));
-    HF_CHECK_LAUNCH();
-    g.launches += 1;
+    p.q = ps.q.as<int32_t>();
+    p.nbr = ps.nbr_enc.as<int32_t>();   // split-row neighbours encoded
+    p.part_np = ps.part_np.as<int32_t>();
+    DevBuf part_buf, part_cnt;
+    if (ps.nparts > 0) {
+        part_buf.alloc(sizeof(float) * size_t(ps.nparts) * p.S, g.stream);
+        part_cnt.alloc(sizeof(int32_t) * size_t(ps.nparts), g.stream);
+        HF_CUDA(cudaMemsetAsync(part_cnt.p, 0, sizeof(int32_t) * size_t(ps.nparts), g.stream));
+        p.part_buf = part_buf.as<float>();
+        p.part_cnt = part_cnt.as<int32_t>();
+    }
     p.L = g.L;
     const SlotLayout SL = slot_layout(ncap, ecap, p.S);
     const size_t smem = size_t(NBUF) * SL.bytes + size_t(fixed);
-    g.ws_sync.alloc(sizeof(int32_t) * (size_t(g.L) + 1), g.stream);
+    g.ws_sync.alloc(sizeof(int32_t) * (size_t(g.L) + 1), g.stream);   // warps published per level
     HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(g.L) + 1), g.stream));
     p.done = g.ws_sync.as<int32_t>();
     p.err = g.d_err();
+    // TMA bulk copies need 16-byte rows and 16-byte aligned sources
     const bool vec16 = (p.S % 4 == 0) && (reinterpret_cast<uintptr_t>(p.d) % 16 == 0);
     // debugging timeline: HF_TRACE=<file prefix> dumps one record per piece
     const char *trace_env = getenv("HF_TRACE");
@@ -967,12 +1176,6 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
             fwrite(h.data(), 8, h.size(), f);
             fclose(f);
         }
-    }
-    if (!FWD && p.slack) {
-        k_split_slack<<<grid_for(g.n, 256, g.sms), 256, 0, g.stream>>>(
-            p.row_ptr, p.node_of, g.n, split, p.S, p.out, p.other, p.slack);
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
     }
 }
 
