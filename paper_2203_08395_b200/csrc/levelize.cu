@@ -19,6 +19,10 @@
 // Nodes never resolved (on or below a cycle) are counted -> HF_ERR_CYCLE.
 // Both persistent loops run as cooperative kernels with a grid barrier.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -27,8 +31,8 @@ namespace hf {
 namespace {
 
 struct GridBar {
-    unsigned count;
-    unsigned gen;
+    unsigned count;   // monotonic: arrivals over the kernel's lifetime
+    unsigned pad;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
@@ -37,20 +41,14 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     return v;
 }
 
-__device__ __forceinline__ void grid_sync(GridBar *b) {
+// Grid barrier for a cooperative launch: one release-add per CTA, then spin until
+// all CTAs of this generation arrived (target grows by gridDim.x per call).
+__device__ __forceinline__ void grid_sync(GridBar *b, unsigned &target) {
+    target += gridDim.x;
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned g0 = ld_acquire_u32(&b->gen);
-        __threadfence();
-        unsigned arrived = atomicAdd(&b->count, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(&b->count, 0u);
-            __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            while (ld_acquire_u32(&b->gen) == g0) __nanosleep(32);
-        }
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&b->count) : "memory");
+        while (ld_acquire_u32(&b->count) < target) __nanosleep(20);
     }
     __syncthreads();
 }
@@ -100,7 +98,7 @@ __global__ void k_lev_init(const int32_t *__restrict__ in_ptr, const int32_t *__
             lev[v] = 0;
         }
         warp_append(in && deg == 1, int(v), active, sc + SC_ACT + 0);
-        warp_append(in && deg == 0, int(v), frontier, sc + SC_FR + 0);
+        warp_append(in && deg == 0, int(v), frontier, sc + SC_FR + 1);
     }
 }
 
@@ -111,8 +109,10 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
                            int32_t *__restrict__ act_b, int32_t *sc, int max_rounds,
                            GridBar *bar) {
     const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
-    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    // warp-granular interleave across SMs (a warp stays contiguous for coalescing)
+    const int64_t tid = (int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
     int32_t *lists[2] = {act_a, act_b};
+    unsigned bar_target = 0;
     for (int r = 0; r < max_rounds; ++r) {
         volatile int32_t *vsc = sc;
         int size = vsc[SC_ACT + r % 3];
@@ -135,72 +135,100 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
             }
             warp_append(keep, v, out, sc + SC_ACT + (r + 1) % 3);
         }
-        grid_sync(bar);
+        grid_sync(bar, bar_target);
     }
 }
 
 // Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w) over the
 // contracted edges r -> j (cdst, cw), released by the atomic join counter cnt[j].
+__device__ __forceinline__ unsigned long long lev_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr int KCH = 1;    // contracted edges per frontier entry (one lane per edge)
+
+// warp-aggregated append of `cnt` entries {start + t*KCH, node} (t < cnt) per lane
+__device__ __forceinline__ void warp_append_chunks(int cnt, int start, int node, int2 *list,
+                                                   int *count) {
+    const int lane = threadIdx.x & 31;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    int base = 0;
+    if (lane == 31) base = atomicAdd(count, total);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+    for (int t = 0; t < cnt; ++t) list[base + t] = make_int2(start + t * KCH, node);
+}
+
+// Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w) over the
+// contracted edges r -> j (cdst, cw), released by the atomic join counter cnt[j].
+// A frontier entry is one contracted edge {edge, source node}: every lane does
+// exactly one relaxation per round, so hub fan-outs are spread over the whole GPU.
 __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__restrict__ cdst,
                            const int32_t *__restrict__ cw, int32_t *__restrict__ cnt,
-                           int32_t *__restrict__ lev, int32_t *__restrict__ fr_a,
-                           int32_t *__restrict__ fr_b, int32_t *sc, GridBar *bar) {
+                           int32_t *__restrict__ lev, int2 *__restrict__ fr_a,
+                           int2 *__restrict__ fr_b, int32_t *sc, GridBar *bar,
+                           unsigned long long *trace) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-    int32_t *lists[2] = {fr_a, fr_b};
+    // consecutive warp slots land on different SMs, so a small frontier is spread
+    // over the whole GPU instead of the first few CTAs
+    const int64_t wid = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    int2 *lists[2] = {fr_a, fr_b};
+    unsigned bar_target = 0;
     for (int r = 0;; ++r) {
         volatile int32_t *vsc = sc;
-        int size = vsc[SC_FR + r % 3];
+        const int size = vsc[SC_FR + r % 3];
         if (size == 0) break;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            vsc[SC_FR + (r + 2) % 3] = 0;
-            vsc[SC_VIS] += size;
+        if (blockIdx.x == 0 && threadIdx.x == 0) vsc[SC_FR + (r + 2) % 3] = 0;
+        const int2 *in = lists[r & 1];
+        int2 *out = lists[(r + 1) & 1];
+        if (trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 4096) {
+            trace[3 * r] = lev_gtimer();
+            trace[3 * r + 2] = (unsigned long long)size;
         }
-        const int32_t *in = lists[r & 1];
-        int32_t *out = lists[(r + 1) & 1];
         for (int64_t base = wid * 32; base < size; base += nwarps * 32) {
-            int64_t i = base + lane;
-            int deg = 0, start = 0, lj = 0;
+            const int64_t i = base + lane;
+            int nch = 0, kstart = 0, k = 0;
             if (i < size) {
-                int j = __ldcg(in + i);
-                start = __ldg(cptr + j);
-                deg = __ldg(cptr + j + 1) - start;
-                lj = __ldcg(lev + j);
-            }
-            int incl = deg;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            int excl = incl - deg;
-            int total = __shfl_sync(0xffffffffu, incl, 31);
-            // edge-balanced expansion: lane idx handles the idx-th edge of the warp's rows
-            for (int eb = 0; eb < total; eb += 32) {
-                int idx = eb + lane;
-                int lo = 0;
-#pragma unroll
-                for (int step = 16; step >= 1; step >>= 1) {
-                    int cand = lo + step;
-                    int ev = __shfl_sync(0xffffffffu, excl, cand & 31);
-                    if (cand < 32 && ev <= idx) lo = cand;
+                const int2 en = __ldcg(in + i);   // one contracted edge per entry
+                k = __ldg(cdst + en.x);
+                const int w = __ldg(cw + en.x);
+                const int lj = __ldcg(lev + en.y);
+                atomicMax(lev + k, lj + w);
+                if (atomicSub(cnt + k, 1) == 1) {   // k ready: queue its out-edges
+                    kstart = __ldg(cptr + k);
+                    nch = __ldg(cptr + k + 1) - kstart;
                 }
-                int o_excl = __shfl_sync(0xffffffffu, excl, lo);
-                int o_start = __shfl_sync(0xffffffffu, start, lo);
-                int o_lev = __shfl_sync(0xffffffffu, lj, lo);
-                bool ready = false;
-                int k = 0;
-                if (idx < total) {
-                    int c = o_start + (idx - o_excl);
-                    k = __ldg(cdst + c);
-                    atomicMax(lev + k, o_lev + __ldg(cw + c));
-                    ready = atomicSub(cnt + k, 1) == 1;
-                }
-                warp_append(ready, k, out, sc + SC_FR + (r + 1) % 3);
             }
+            warp_append_chunks(nch, kstart, k, out, sc + SC_FR + (r + 1) % 3);
         }
-        grid_sync(bar);
+        if (trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 4096) trace[3 * r + 1] = lev_gtimer();
+        grid_sync(bar, bar_target);
+    }
+}
+
+// initial frontier: the sources' contracted out-edges as chunk entries
+__global__ void k_lev_seed(const int32_t *__restrict__ src_list, const int32_t *__restrict__ cptr,
+                           int2 *__restrict__ out, int32_t *sc) {
+    const int size = sc[SC_FR + 1];   // sources were counted in slot 1 by k_lev_init
+    const int64_t lim = (int64_t(size) + 31) / 32 * 32;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < lim;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int nch = 0, st = 0, v = 0;
+        if (i < size) {
+            v = src_list[i];
+            st = cptr[v];
+            nch = cptr[v + 1] - st;
+        }
+        warp_append_chunks(nch, st, v, out, sc + SC_FR + 0);
     }
 }
 
@@ -427,16 +455,44 @@ int64_t levelize_device(Graph &g) {
         g.launches += 1;
     }
     {
+        // frontier entries {first contracted edge, node}: at most n + m/KCH per round
+        DevBuf ea, eb2;
+        const size_t ecap = size_t(n) + size_t(m) / KCH + 1;
+        ea.alloc(sizeof(int2) * ecap, s);
+        eb2.alloc(sizeof(int2) * ecap, s);
+        k_lev_seed<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lb.as<int32_t>(), cptr.as<int32_t>(),
+                                                          ea.as<int2>(), sc);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+        HF_CUDA(cudaMemsetAsync(sc + SC_FR + 1, 0, sizeof(int32_t), s));   // round 0 appends here
         const int block = 1024;
         int grid = coop_grid((const void *)k_lev_kahn, block, g.sms, 1);
         HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), s));
         const int32_t *cp = cptr.as<int32_t>(), *cd = cdst.as<int32_t>(), *cwp = cw.as<int32_t>();
         int32_t *cn = cnt.as<int32_t>(), *lv = lev.as<int32_t>();
-        int32_t *fa = lb.as<int32_t>(), *fb = la.as<int32_t>();
+        int2 *fa = ea.as<int2>(), *fb = eb2.as<int2>();
         GridBar *barp = bar.as<GridBar>();
-        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &barp};
+        const char *trace_env = getenv("HF_TRACE");
+        DevBuf tb;
+        unsigned long long *tr = nullptr;
+        if (trace_env) {
+            tb.alloc(sizeof(unsigned long long) * 3 * 4096, s);
+            HF_CUDA(cudaMemsetAsync(tb.p, 0, sizeof(unsigned long long) * 3 * 4096, s));
+            tr = tb.as<unsigned long long>();
+        }
+        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &barp, &tr};
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn, grid, block, args, 0, s));
         g.launches += 1;
+        if (trace_env) {
+            std::vector<unsigned long long> h(3 * 4096);
+            HF_CUDA(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            HF_CUDA(cudaStreamSynchronize(s));
+            std::string fn = std::string(trace_env) + "_kahn.bin";
+            if (FILE *f = fopen(fn.c_str(), "wb")) {
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
     }
     k_lev_final<<<grid_for(n, 256, g.sms), 256, 0, s>>>(pd.as<long long>(), cnt.as<int32_t>(),
                                                         lev.as<int32_t>(), n,
