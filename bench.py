@@ -61,10 +61,8 @@ def dist_env():
 
 
 def scenario_block(args, rank, world):
-    if args.scaling == "weak":
-        return rank * args.scenarios, (rank + 1) * args.scenarios
-    S = args.scenarios
-    return rank * S // world, (rank + 1) * S // world
+    from paper_2203_08395_b200.shard import scenario_block as blk
+    return blk(rank, world, args.scenarios, args.scaling)
 
 
 def algorithmic_bytes(n, m, S):

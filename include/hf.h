@@ -171,11 +171,12 @@ hf_status hf_nccl_unique_id(void *id128);
 hf_status hf_nccl_comm_init(const void *id128, int rank, int nranks, int device, void **comm);
 hf_status hf_nccl_comm_destroy(void *comm);
 
-/* Per-phase device timing (CUDA events on the graph's stream) and launch count.
+/* Device timing (CUDA events on the graph's stream) and launch count.
  * hf_profile_enable(g, 1) starts recording; hf_profile_read synchronises and
- * returns the milliseconds of the most recent levelize / forward / backward
- * phase (forward and backward cover all scenarios of the last batch) and the
- * total number of kernels libhf launched on this graph so far. */
+ * returns the milliseconds of the most recent hf_levelize call (whole call) and
+ * of the most recent forward / backward propagation KERNEL (one persistent
+ * launch each, all scenarios of the batch), and the total number of kernels
+ * libhf launched on this graph so far. */
 hf_status hf_profile_enable(hf_graph g, int on);
 hf_status hf_profile_read(hf_graph g, float *ms_levelize, float *ms_forward,
                           float *ms_backward, int64_t *kernel_launches);

@@ -331,9 +331,7 @@ hf_status hf_propagate_forward_d(hf_graph h, const float *at_src_d, float *at_d)
         Graph *g = G(h);
         DeviceGuard dg(g->device);
         need_levels(g);
-        if (g->prof) profile_mark(*g, 2);
         forward_device(*g, g->delay.as<float>(), 1, false, at_src_d, at_d);
-        if (g->prof) profile_mark(*g, 3);
         return HF_OK;
     });
 }
@@ -370,9 +368,7 @@ hf_status hf_propagate_backward_d(hf_graph h, float t_req, const float *at_d, fl
         Graph *g = G(h);
         DeviceGuard dg(g->device);
         need_levels(g);
-        if (g->prof) profile_mark(*g, 5);
         backward_device(*g, g->delay.as<float>(), 1, nullptr, t_req, at_d, rat_d, slack_d, wns_d);
-        if (g->prof) profile_mark(*g, 4);
         return HF_OK;
     });
 }
@@ -418,12 +414,8 @@ static void batch_core(Graph *g, int32_t S, const float *d_ms, const float *t_d,
         if (g->ws_rat.bytes < nb || g->ws_rat.s != g->stream) g->ws_rat.alloc(nb, g->stream);
         rat_d = g->ws_rat.as<float>();
     }
-    if (g->prof) profile_mark(*g, 2);
     forward_device(*g, d_ms, S, true, at_src_d, at_d);
-    if (g->prof) profile_mark(*g, 3);
-    if (g->prof) profile_mark(*g, 5);
     backward_device(*g, d_ms, S, t_d, 0.0f, at_d, rat_d, nullptr, wns_d);
-    if (g->prof) profile_mark(*g, 4);
     if (comm) {
         nccl::load();
         nccl::check(nccl::api.all_gather(wns_d, wns_all_d, size_t(S), nccl::kFloat32, comm,

@@ -1082,8 +1082,11 @@ void launch(Graph &g, PassParams &p, size_t smem) {
     HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
     void *args[] = {&p};
-    // one CTA per SM; the piece schedule was built for exactly g.sms CTAs
+    // one CTA per SM; the piece schedule was built for exactly g.sms CTAs.  With
+    // profiling on, events bracket exactly this launch (forward: ev 2/3, backward 5/4).
+    prof_record(g, FWD ? 2 : 5);
     HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, BLOCK, args, smem, g.stream));
+    prof_record(g, FWD ? 3 : 4);
     g.launches += 1;
 }
 

@@ -329,3 +329,36 @@ def test_batch_full_c4_and_shard_invariance(hf):
             parts.append(gpu_batch_device(hf, g, np.ascontiguousarray(D[:, lo:hi]), T[lo:hi],
                                           hi - lo, want_at_rat=False)[0])
         assert_bits_equal(np.concatenate(parts), w, f"shards G={G_}")
+
+
+def test_batch_nccl_gather_single_rank(hf):
+    """hf_run_batch with a 1-rank NCCL communicator: wns_all == wns_local."""
+    import torch
+    g = hfgen.config("C1")
+    S = 8
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    uid = hf.hf_nccl_unique_id()
+    comm = hf.hf_nccl_comm_init(uid, 0, 1, 0)
+    try:
+        dev = torch.device("cuda:0")
+        G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=g.delay,
+                               stream=torch.cuda.current_stream())
+        hf.levelize_np(G)
+        w = torch.empty(S, dtype=torch.float32, device=dev)
+        wall = torch.empty(S, dtype=torch.float32, device=dev)
+        hf.hf_run_batch(G, S, torch.from_numpy(D).to(dev), hf.HF_LAYOUT_MS,
+                        torch.from_numpy(T).to(dev), torch.from_numpy(g.at_src).to(dev), w,
+                        comm, wall)
+        hf.hf_sync(G)
+        wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4)
+        assert_bits_equal(w.cpu().numpy(), wo, "wns_local")
+        assert_bits_equal(wall.cpu().numpy(), wo, "wns_all")
+        # host-pointer variant with the communicator
+        wh = np.zeros(S, F32)
+        wah = np.zeros(S, F32)
+        hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, g.at_src, wh, comm, wah)
+        assert_bits_equal(wah, wo, "wns_all host")
+        G.close()
+    finally:
+        hf.hf_nccl_comm_destroy(comm)
