@@ -464,11 +464,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
         const int part_qb = part ? meta[MT_QB] : 0;
         const int part_n = part ? (s_rp[1] - s_rp[0] + p.psize - 1) / p.psize : 0;
 
-        // (a) backward: prefetch at[] of this thread's first two rows (for the slack)
-        Vec<V> pre_at[2];
+        // (a) backward: prefetch at[] of this thread's first four rows (for the slack)
+        Vec<V> pre_at[4];
         if (!FWD && tid < active) {
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < 4; ++r) {
                 const int i = tid / lpn + r * slots;
                 if (i < nst) pre_at[r] = ldv_cg<V>(p.other + int64_t(s_node[i]) * p.S + col);
             }
@@ -545,9 +545,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
         auto finish = [&](int node, const Vec<V> &best, int i) {
             stv_g<V>(p.out + int64_t(node) * p.S + col, best);
             if (!FWD) {
-                const int rr = i >= 0 ? (i - tid / lpn) / slots : 2;
-                const Vec<V> a = (rr < 2 && i < nst)
-                                     ? (rr == 0 ? pre_at[0] : pre_at[1])
+                const int rr = i >= 0 ? (i - tid / lpn) / slots : 4;
+                const Vec<V> a = (rr < 4 && i < nst)
+                                     ? (rr == 0   ? pre_at[0]
+                                        : rr == 1 ? pre_at[1]
+                                        : rr == 2 ? pre_at[2]
+                                                  : pre_at[3])
                                      : ldv_cg<V>(p.other + int64_t(node) * p.S + col);
                 Vec<V> sl;
 #pragma unroll
@@ -743,38 +746,8 @@ __global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
         }
         consumer_sync();
         if (tid == 0) atomicAdd(p.done + kc, 1);
-        // a split row is finalised by its last part, off the critical path (readers
-        // use the partials): its value, slack and worst-slack contribution
-        if (part) {
-            const int nparts = part_n;
-            if (nparts > 1) {
-                if (tid == 0) {
-                    const int qb = part_qb;
-                    int done_parts;
-                    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;"
-                                 : "=r"(done_parts)
-                                 : "l"(p.part_cnt + qb)
-                                 : "memory");
-                    s_nhub = done_parts == nparts - 1 ? -1 : 0;   // flag
-                }
-                consumer_sync();
-                if (s_nhub < 0) {
-                    const int qb = part_qb, node = part_node;
-                    for (int s2 = tid; s2 < p.S; s2 += NC) {
-                        float v = ident<FWD>();
-                        for (int k = 0; k < nparts; ++k)
-                            v = combine<FWD>(v, __ldcg(p.part_buf + int64_t(qb + k) * p.S + s2));
-                        __stcg(p.out + int64_t(node) * p.S + s2, v);
-                        if (!FWD) {
-                            const float sl =
-                                __fsub_rn(v, __ldcg(p.other + int64_t(node) * p.S + s2));
-                            atomicMin(s_min + s2, f2ord(sl));
-                            if (p.slack) __stcg(p.slack + int64_t(node) * p.S + s2, sl);
-                        }
-                    }
-                }
-            }
-        }
+        // split rows (>= 2 parts) are finalised by k_finalize_split after the pass;
+        // readers inside the pass combine their partials
         if (p.trace && tid == 0) {
             const int r = atomicAdd(p.trace_n, 1);
             if (r < p.trace_cap) {
@@ -805,6 +778,81 @@ __global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
     }
 }
 
+// After a pass: every row cut into >= 2 part pieces gets its value (combine of the
+// partials), its optional slack and its worst-slack contribution.  One warp per
+// split row; the rows are the positions with degree > split and > psize.
+template <bool FWD>
+__global__ void k_finalize_split(const int32_t *__restrict__ row_ptr,
+                                 const int32_t *__restrict__ node_of, const int32_t *__restrict__ q,
+                                 int32_t n, int32_t split, int32_t psize, int32_t S,
+                                 const float *__restrict__ part_buf, float *__restrict__ out,
+                                 const float *__restrict__ other, float *__restrict__ slack,
+                                 int32_t *__restrict__ wns_ord) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n; i += nw) {
+        const int d = row_ptr[i + 1] - row_ptr[i];
+        if (d <= split || d <= psize) continue;
+        const int np = (d + psize - 1) / psize, qb = q[i];
+        const int64_t node = node_of[i];
+        for (int s = lane; s < S; s += 32) {
+            float v = part_buf[int64_t(qb) * S + s];
+            for (int k = 1; k < np; ++k) v = combine<FWD>(v, part_buf[int64_t(qb + k) * S + s]);
+            out[node * S + s] = v;
+            if (!FWD) {
+                const float sl = __fsub_rn(v, other[node * S + s]);
+                if (slack) slack[node * S + s] = sl;
+                atomicMin(wns_ord + s, f2ord(sl));
+            }
+        }
+    }
+}
+
+// Backward sinks (out-degree 0) do not depend on any level: rat = T_s, their
+// slack and worst-slack contribution, in one bandwidth-bound sweep before the pass.
+template <int V>
+__global__ void k_bwd_sinks(const int32_t *__restrict__ out_ptr, int32_t n, int32_t S,
+                            const float *__restrict__ t_arr, float t_scalar,
+                            const float *__restrict__ at, float *__restrict__ rat,
+                            float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
+    extern __shared__ int32_t s_wmin[];
+    for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
+    __syncthreads();
+    const int lpn = S / V;
+    const int apb = blockDim.x / lpn * lpn;                 // active threads per block
+    const int64_t step = int64_t(gridDim.x) * apb;          // a multiple of lpn: lane fixed
+    const int64_t t0 = blockIdx.x * int64_t(apb) + threadIdx.x;
+    const int lane = int(threadIdx.x % lpn);
+    float mn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+    if (int(threadIdx.x) < apb) {
+        for (int64_t t = t0; t < int64_t(n) * lpn; t += step) {
+            const int64_t v = t / lpn;
+            if (out_ptr[v + 1] != out_ptr[v]) continue;
+            const int64_t o = v * S + int64_t(lane) * V;
+            Vec<V> r, a, sl;
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                r.x[j] = canon0(t_arr ? __ldg(t_arr + lane * V + j) : t_scalar);
+            stv_g<V>(rat + o, r);
+            a = ldv_cg<V>(at + o);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                sl.x[j] = __fsub_rn(r.x[j], a.x[j]);
+                mn[j] = fminf(mn[j], sl.x[j]);
+            }
+            if (slack) stv_g<V>(slack + o, sl);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + lane * V + j, f2ord(mn[j]));
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x)
+        if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
+}
+
 __global__ void k_fill_i32(int32_t *p, int32_t v, int64_t count) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -827,31 +875,45 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
 // the tail [le_normal, le) of every level.  Normal rows get weight degree + 1 and
 // are cut into weight-balanced pieces; a split row becomes ceil(deg/split) part
 // pieces of <= split edges each.
+// weight of a row: 2 per edge (delay + gather) + rw for the row itself (forward:
+// the at store; backward: rat store + at read for the slack)
 __global__ void k_piece_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                             int32_t psize, int32_t *__restrict__ w, int32_t *__restrict__ parts) {
+                             int32_t psize, int32_t rw, int32_t *__restrict__ w,
+                             int32_t *__restrict__ parts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int d = row_ptr[i + 1] - row_ptr[i];
-        w[i] = d > split ? 0 : 2 * d + 1;   // an edge moves ~2x the bytes of a row
+        w[i] = d > split ? 0 : 2 * d + rw;
         parts[i] = d > split ? (d + psize - 1) / psize : 0;
     }
 }
 __global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
                               const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
                               int32_t L, int32_t P, int32_t ecap, int32_t ncap, int32_t wt_min,
-                              int32_t split, int32_t *__restrict__ np, int32_t *__restrict__ npn,
+                              int32_t split, int32_t rw, int32_t skip0, int32_t *__restrict__ np,
+                              int32_t *__restrict__ npn, int32_t *__restrict__ lsnorm,
                               int32_t *__restrict__ lenorm) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
-        const int ls = level_ptr[k], le = level_ptr[k + 1];
+        int ls = level_ptr[k];
+        const int le = level_ptr[k + 1];
+        if (skip0) {   // degree-0 rows (backward sinks) are done by k_bwd_sinks
+            int a = ls, z = le;
+            while (a < z) {
+                const int mid = (a + z) >> 1;
+                if (row_ptr[mid + 1] - row_ptr[mid] > 0) z = mid;
+                else a = mid + 1;
+            }
+            ls = a;
+        }
         int lo = ls, hi = le;   // first row with degree > split
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
             else lo = mid + 1;
         }
-        const int64_t wk = int64_t(W[lo]) - W[ls];   // 2*edges + rows of the normal rows
+        const int64_t wk = int64_t(W[lo]) - W[ls];   // 2*edges + rw*rows, normal rows
         const int64_t nk = lo - ls;
-        const int64_t ek = (wk - nk) / 2;
+        const int64_t ek = (wk - rw * nk) / 2;
         const int parts = Q[le] - Q[ls];
         int64_t c = 0;
         if (nk > 0) {
@@ -863,18 +925,20 @@ __global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32
                                                           (wk + wt_min - 1) / wt_min));
             c = std::max<int64_t>(1, std::min<int64_t>(nk, c));
         }
+        if (c + parts == 0) c = 1;   // keep one (empty) piece: levels publish in order
         npn[k] = int(c);
+        lsnorm[k] = ls;
         lenorm[k] = lo;
         np[k] = int(c) + parts;
     }
 }
 // normal piece j of level k starts at the first row whose weight prefix reaches j*W_k/np_k
-__global__ void k_piece_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
+__global__ void k_piece_fill(const int32_t *__restrict__ lsnorm, const int32_t *__restrict__ W,
                              const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ off,
                              const int32_t *__restrict__ npn, const int32_t *__restrict__ lenorm,
                              int32_t L, int4 *__restrict__ pieces) {
     for (int k = blockIdx.x; k < L; k += gridDim.x) {
-        const int ls = level_ptr[k], le = lenorm[k];
+        const int ls = lsnorm[k], le = lenorm[k];
         const int np = npn[k];
         const int64_t w0 = W[ls], wk = int64_t(W[le]) - w0;
         auto start_of = [&](int jj) {
@@ -939,10 +1003,11 @@ __global__ void k_nbr_enc(const int32_t *__restrict__ nbr, int32_t m, const int3
 }
 
 void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *nbr,
-                  int P, int ecap, int ncap, int wt_min, int split, int psize, PieceSched &ps) {
+                  int P, int ecap, int ncap, int wt_min, int split, int psize, int rw,
+                  int skip0, PieceSched &ps) {
     cudaStream_t s = g.stream;
     const int32_t n = g.n, L = g.L;
-    DevBuf w, W, q, np, npn, lenorm;
+    DevBuf w, W, q, np, npn, lsnorm, lenorm;
     DevBuf &Q = ps.q, &off = ps.off, &pieces = ps.pieces;
     w.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     W.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
@@ -951,18 +1016,20 @@ void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, cons
     np.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     npn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     lenorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    lsnorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     off.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     HF_CUDA(cudaMemsetAsync(w.as<int32_t>() + n, 0, sizeof(int32_t), s));
     HF_CUDA(cudaMemsetAsync(q.as<int32_t>() + n, 0, sizeof(int32_t), s));
     HF_CUDA(cudaMemsetAsync(np.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, psize,
+    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, psize, rw,
                                                          w.as<int32_t>(), q.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(w.as<int32_t>(), W.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
     scan_exclusive(q.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
     k_piece_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
         g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, P, ecap, ncap,
-        wt_min, split, np.as<int32_t>(), npn.as<int32_t>(), lenorm.as<int32_t>());
+        wt_min, split, rw, skip0, np.as<int32_t>(), npn.as<int32_t>(), lsnorm.as<int32_t>(),
+        lenorm.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(np.as<int32_t>(), off.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
     int32_t total = 0;
@@ -973,7 +1040,7 @@ void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, cons
     HF_CUDA(cudaStreamSynchronize(s));
     pieces.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
     k_piece_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
-        g.level_ptr.as<int32_t>(), W.as<int32_t>(), row_ptr, off.as<int32_t>(),
+        lsnorm.as<int32_t>(), W.as<int32_t>(), row_ptr, off.as<int32_t>(),
         npn.as<int32_t>(), lenorm.as<int32_t>(), L, pieces.as<int4>());
     HF_CHECK_LAUNCH();
     k_piece_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
@@ -1116,7 +1183,8 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
     PieceSched &ps = FWD ? g.ps_f : g.ps_b;
     const int32_t want = (ecap * 4096 + ncap) * 8 + (g.sms & 7);
     if (ps.key != want || !ps.pieces.p) {
-        build_pieces(g, p.row_ptr, p.node_of, p.nbr, g.sms, ecap, ncap, wt_min, split, ecap, ps);
+        build_pieces(g, p.row_ptr, p.node_of, p.nbr, g.sms, ecap, ncap, wt_min, split, ecap,
+                     FWD ? 1 : 2, FWD ? 0 : 1, ps);
         deal_pieces<FWD>(g, ps);
         ps.key = want;
     }
@@ -1127,13 +1195,10 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
     p.q = ps.q.as<int32_t>();
     p.nbr = ps.nbr_enc.as<int32_t>();   // split-row neighbours encoded
     p.part_np = ps.part_np.as<int32_t>();
-    DevBuf part_buf, part_cnt;
+    DevBuf part_buf;
     if (ps.nparts > 0) {
         part_buf.alloc(sizeof(float) * size_t(ps.nparts) * p.S, g.stream);
-        part_cnt.alloc(sizeof(int32_t) * size_t(ps.nparts), g.stream);
-        HF_CUDA(cudaMemsetAsync(part_cnt.p, 0, sizeof(int32_t) * size_t(ps.nparts), g.stream));
         p.part_buf = part_buf.as<float>();
-        p.part_cnt = part_cnt.as<int32_t>();
     }
     p.L = g.L;
     const SlotLayout SL = slot_layout(ncap, ecap, p.S);
@@ -1166,6 +1231,13 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
     else if (V == 2) HF_LAUNCH(2);
     else HF_LAUNCH(1);
 #undef HF_LAUNCH
+    if (ps.nparts > 0) {
+        k_finalize_split<FWD><<<grid_for(int64_t(g.n) * 32, 256, g.sms), 256, 0, g.stream>>>(
+            p.row_ptr, p.node_of, p.q, g.n, split, p.psize, p.S, p.part_buf, p.out, p.other,
+            p.slack, p.wns_ord);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
     if (trace_env) {
         int32_t cnt = 0;
         HF_CUDA(cudaMemcpyAsync(&cnt, p.trace_n, 4, cudaMemcpyDeviceToHost, g.stream));
@@ -1230,6 +1302,22 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         p.out = rat;
         p.slack = slack;
         p.wns_ord = ord;
+        // sinks first (independent of every level); the pass skips them
+        const int lpn = S / V;
+        const int grid = grid_for(int64_t(g.n) * lpn, 512, g.sms);
+        const size_t sm = sizeof(int32_t) * size_t(S);
+        if (sm > 48 * 1024) fail(HF_ERR_INVALID_ARG, "too many scenarios");
+        if (V == 4)
+            k_bwd_sinks<4><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
+                                                 at, rat, slack, ord);
+        else if (V == 2)
+            k_bwd_sinks<2><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
+                                                 at, rat, slack, ord);
+        else
+            k_bwd_sinks<1><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
+                                                 at, rat, slack, ord);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
         run_pass<false>(g, p, false, V);
     }
     if (wns_f) {
