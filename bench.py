@@ -269,9 +269,9 @@ def main():
     prop_ms = (fwd_ms + bwd_ms) / K
     achieved = (b_fwd + b_bwd) / (prop_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    traffic = None
+    traffic = None   # measured dram bytes of the same two kernels (profiles/traffic.json)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and S == 64:
         try:
             traffic = json.load(open(tpath)).get(args.config)
         except Exception:

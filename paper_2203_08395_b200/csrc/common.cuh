@@ -76,6 +76,7 @@ struct PieceSched {
     DevBuf q;                         // [n+1] first part id of every (split) row
     DevBuf part_np;                   // [parts] parts of the row starting at that id
     DevBuf nbr_enc;                   // [m] neighbour ids, split rows as -(part id + 1)
+    DevBuf split_rows;                // [1 + rows]: count, then positions of rows with >= 2 parts
     int32_t nparts = 0;
     int32_t key = -1;                 // (piece weight, CTAs) the schedule was built for
 };

@@ -782,17 +782,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
 // partials), its optional slack and its worst-slack contribution.  One warp per
 // split row; the rows are the positions with degree > split and > psize.
 template <bool FWD>
-__global__ void k_finalize_split(const int32_t *__restrict__ row_ptr,
+__global__ void k_finalize_split(const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows,
+                                 const int32_t *__restrict__ row_ptr,
                                  const int32_t *__restrict__ node_of, const int32_t *__restrict__ q,
-                                 int32_t n, int32_t split, int32_t psize, int32_t S,
-                                 const float *__restrict__ part_buf, float *__restrict__ out,
-                                 const float *__restrict__ other, float *__restrict__ slack,
-                                 int32_t *__restrict__ wns_ord) {
+                                 int32_t psize, int32_t S, const float *__restrict__ part_buf,
+                                 float *__restrict__ out, const float *__restrict__ other,
+                                 float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; i < n; i += nw) {
+    const int cnt = *nrows;
+    for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < cnt; r += nw) {
+        const int i = rows[r];
         const int d = row_ptr[i + 1] - row_ptr[i];
-        if (d <= split || d <= psize) continue;
         const int np = (d + psize - 1) / psize, qb = q[i];
         const int64_t node = node_of[i];
         for (int s = lane; s < S; s += 32) {
@@ -805,6 +806,16 @@ __global__ void k_finalize_split(const int32_t *__restrict__ row_ptr,
                 atomicMin(wns_ord + s, f2ord(sl));
             }
         }
+    }
+}
+
+// positions of the rows cut into >= 2 parts (read through their partials)
+__global__ void k_split_list(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
+                             int32_t psize, int32_t *__restrict__ rows, int32_t *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int d = row_ptr[i + 1] - row_ptr[i];
+        if (d > split && d > psize) rows[atomicAdd(cnt, 1)] = int(i);
     }
 }
 
@@ -1063,6 +1074,12 @@ void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, cons
         k_part_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, Q.as<int32_t>(), n, split,
                                                           psize, ps.part_np.as<int32_t>());
         HF_CHECK_LAUNCH();
+        ps.split_rows.alloc(sizeof(int32_t) * (size_t(ps.nparts) + 1), s);
+        HF_CUDA(cudaMemsetAsync(ps.split_rows.p, 0, sizeof(int32_t), s));
+        k_split_list<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            row_ptr, n, split, psize, ps.split_rows.as<int32_t>() + 1, ps.split_rows.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
         if (m) {
             k_nbr_enc<<<grid_for(m, 256, g.sms), 256, 0, s>>>(nbr, m, pos.as<int32_t>(), row_ptr,
                                                               Q.as<int32_t>(), split, psize,
@@ -1232,9 +1249,9 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
     else HF_LAUNCH(1);
 #undef HF_LAUNCH
     if (ps.nparts > 0) {
-        k_finalize_split<FWD><<<grid_for(int64_t(g.n) * 32, 256, g.sms), 256, 0, g.stream>>>(
-            p.row_ptr, p.node_of, p.q, g.n, split, p.psize, p.S, p.part_buf, p.out, p.other,
-            p.slack, p.wns_ord);
+        k_finalize_split<FWD><<<g.sms, 256, 0, g.stream>>>(
+            ps.split_rows.as<int32_t>() + 1, ps.split_rows.as<int32_t>(), p.row_ptr, p.node_of,
+            p.q, p.psize, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
