@@ -68,17 +68,23 @@ struct DevBuf {
     template <class T> T *as() const { return static_cast<T *>(p); }
 };
 
-// ---- piece schedule of one propagation direction (propagate.cu) ------------
-struct PieceSched {
-    DevBuf pieces;   // int4 {pos_begin, pos_end, edge_begin, edge_end}, level-major
-    DevBuf off;      // [L+1] first piece of every level
-    DevBuf cta_pc, cta_lv, cta_off;   // the same pieces dealt to CTAs, pass order
-    DevBuf q;                         // [n+1] first part id of every (split) row
-    DevBuf part_np;                   // [parts] parts of the row starting at that id
-    DevBuf nbr_enc;                   // [m] neighbour ids, split rows as -(part id + 1)
-    DevBuf split_rows;                // [1 + rows]: count, then positions of rows with >= 2 parts
+// ---- task schedule of one propagation direction (propagate.cu) -------------
+// A pass is a list of warp tasks in pass order (levels ascending forward,
+// descending backward; scenario chunks inside a level).  Descriptors are stored
+// once per level; chunk c of level q reuses them.
+struct TaskSched {
+    DevBuf desc;        // int4: normal {row_begin, row_end, edge_begin, edge_end};
+                        //       part   {row, -(part id + 1), edge_begin, edge_end}
+    DevBuf nt;          // [L] tasks per chunk of pass-level q
+    DevBuf doff;        // [L+1] first descriptor of pass-level q
+    DevBuf tb;          // [L+1] first global task of pass-level q (for tb_nch chunks)
+    int32_t tb_nch = -1;
+    DevBuf q;           // [n+1] first part id of every row (exclusive scan of parts)
+    DevBuf part_np;     // [parts] number of parts of the row whose first part id it is
+    DevBuf nbr_enc;     // [m] neighbour ids; split rows as -(first part id + 1)
+    DevBuf split_rows;  // [1 + rows]: count, then positions of split rows
     int32_t nparts = 0;
-    int32_t key = -1;                 // (piece weight, CTAs) the schedule was built for
+    int64_t key = -1;   // (tw, split, pe) the schedule was built for
 };
 
 // ---- the graph -------------------------------------------------------------
@@ -102,8 +108,8 @@ struct Graph {
     // lo_in_node / lo_out_node.
     DevBuf lo_in_node, lo_in_ptr, lo_in_src, lo_in_eid;
     DevBuf lo_out_node, lo_out_ptr, lo_out_dst, lo_out_eid;
-    // piece schedules of the persistent propagation kernels (per direction)
-    PieceSched ps_f, ps_b;
+    // task schedules of the dataflow propagation kernels (per direction)
+    TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // small device scalars: [0] error bits, [1..] scratch

@@ -566,7 +566,7 @@ int64_t levelize_device(Graph &g) {
         HF_CHECK_LAUNCH();
         g.launches += 5;
     }
-    g.ps_f.key = g.ps_b.key = -1;   // piece schedules depend on the levels
+    g.ts_f.key = g.ts_b.key = -1;   // task schedules depend on the levels
     g.L = L;
     g.levelized = true;
     return 0;

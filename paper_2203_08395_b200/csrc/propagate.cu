@@ -1,38 +1,38 @@
 // propagate.cu -- forward max-plus and backward min-plus (+ fused slack / worst
 // slack) over the levelized DAG, for one delay set or S scenario sets.
-// SURVEY.md §8(a) a5-a7; BASELINE.json:5.
+// SURVEY.md §8(a) a5-a7; BASELINE.json:5 ("at[v] = max over fan-in of at[u] +
+// d(u,v)", "min-plus required time").
 //
 // Data layout in HBM (scenario-minor): at[v*S + s], rat[v*S + s],
-// delays[e*S + s].  A node's S values are contiguous, so each edge touches S*4
-// contiguous bytes; a node row is owned by LPN = S/V lanes holding V-wide
-// vectors (V = 4 -> LDG.128 / STG.128).  Pull-based, no float atomics: every
-// output is one fp32 max/min over fl(x +/- d) terms, which is order-independent
-// (0 ULP against the oracle, reading R10).
+// delays[e*S + s].  Pull-based, no float atomics: every output is one fp32
+// max/min over fl(x +/- d) terms, which is order-independent (0 ULP against
+// the oracle, reading R10).
 //
-// One persistent launch per pass (cooperative launch, one CTA per SM; no
-// per-level launches, no grid barrier):
-//   * every level is cut into weight-balanced PIECES (weight = edges + nodes);
-//     piece j of a level belongs to CTA j mod P, and a CTA walks its pieces in
-//     pass order (levels ascending forward, descending backward);
-//   * STAGING: a piece's level-ordered rows, neighbour ids, edge ids and delay
-//     slices are copied into shared memory with cp.async by all threads -- rows
-//     two pieces ahead, delays one piece ahead of the piece being computed
-//     (3-slot ring).  None of this depends on earlier levels, so the HBM stream
-//     of delays runs ahead of the dependency front;
-//   * DEPENDENCY: before computing a piece of level k the CTA waits until level
-//     k-1 (k+1 backward) has published all its pieces: one acquire-poll of a
-//     per-level counter by one thread.  Level k complete => every earlier level
-//     complete, by induction; a CTA only waits on earlier levels whose pieces
-//     belong to co-resident CTAs, so the schedule cannot deadlock;
-//   * COMPUTE: edge-parallel gathers of at[u] / rat[v] from L2 (all edge-lane
-//     items issue their loads at once), x = fl(a +/- d) written in place over the
-//     staged delay, then each node's owner lanes reduce their row from shared
-//     memory; rows longer than HUB_DEG are reduced by the whole CTA (strided
-//     partials, shared-memory combine).  Stores, gpu-scope fence, one atomicAdd
-//     publishes the piece;
-//   * backward fuses slack = rat - at and keeps a per-lane running min; one
-//     shared-memory reduction and one global atomicMin per scenario per CTA give
-//     the worst slack.
+// Dataflow design.  One persistent cooperative launch per pass.
+//   * The pass is a list of WARP TASKS in pass order (levels ascending forward,
+//     descending backward; inside a level, scenario chunks of SC columns).  A
+//     normal task is a run of consecutive level-ordered rows (weight = edges +
+//     rows <= tw + split); a row with more than `split` edges is cut into PART
+//     tasks whose partial max/min go to part_buf.  Task t belongs to warp
+//     t mod W; warps are all co-resident, walk their tasks in order, and a task
+//     only depends on tasks of earlier levels, so the earliest unfinished task
+//     can always proceed (no deadlock).
+//   * READINESS IS THE DATA.  Before a pass the output rows (and part_buf) are
+//     filled with a NaN sentinel.  Finite inputs never produce NaN at/rat values
+//     (only +-inf on overflow), so a gathered value that is not NaN is the final
+//     value: each 32-bit element is written exactly once and read with strong
+//     (relaxed, gpu-scope) loads, so there is no flag, fence or barrier on the
+//     dependency path -- a consumer re-polls only the elements still NaN.
+//   * A warp stages the task's delay rows (and, backward, the at rows for the
+//     slack) into its shared-memory scratch with cp.async while its gathers are
+//     in flight; the task's index data (rows, neighbours, edge ids) were loaded
+//     into registers during the previous task.
+//   * Rows are reduced from shared memory by lane groups (LPN lanes x V floats
+//     per SC-column chunk); backward fuses slack = rat - at and keeps per-lane
+//     minima, folded per CTA into the worst slack (ordered-int atomicMin).
+//   * Rows cut into parts are read by their consumers as the combine of their
+//     partials (each sentinel-checked); their own rows are written after the
+//     pass by k_finalize_split.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -46,59 +46,44 @@ namespace hf {
 
 namespace {
 
-constexpr int NCW = 16;                 // consumer warps
-constexpr int NC = NCW * 32;            // consumer threads
-constexpr int NPW = 2;                  // producer warps
-constexpr int BLOCK = NC + 32 * NPW;
-constexpr int NBUF = 4;                 // staging ring slots
-constexpr int HUB_DEG = 64;    // rows longer than this are reduced by the whole CTA
-constexpr int MAX_HUBS = 256;  // long rows per piece (piece weight bounds this)
+constexpr int NWARP = 4;              // warps per CTA
+constexpr int FLOW_THREADS = NWARP * 32;
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int V> struct Vec {
     float x[V];
 };
 
-template <int V> __device__ __forceinline__ Vec<V> ldv_g(const float *p) {   // read-only input
+template <int V> __device__ __forceinline__ Vec<V> ld_relaxed(const float *p) {
     Vec<V> r;
     if constexpr (V == 4) {
-        float4 t = __ldg(reinterpret_cast<const float4 *>(p));
-        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+        asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+                     : "l"(p)
+                     : "memory");
     } else if constexpr (V == 2) {
-        float2 t = __ldg(reinterpret_cast<const float2 *>(p));
-        r.x[0] = t.x; r.x[1] = t.y;
+        asm volatile("ld.relaxed.gpu.global.v2.f32 {%0,%1}, [%2];"
+                     : "=f"(r.x[0]), "=f"(r.x[1])
+                     : "l"(p)
+                     : "memory");
     } else {
-        r.x[0] = __ldg(p);
+        asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(r.x[0]) : "l"(p) : "memory");
     }
     return r;
 }
-// values produced inside this launch by other CTAs: L2-coherent loads (never L1)
-template <int V> __device__ __forceinline__ Vec<V> ldv_cg(const float *p) {
-    Vec<V> r;
+template <int V> __device__ __forceinline__ void st_relaxed(float *p, const Vec<V> &v) {
     if constexpr (V == 4) {
-        float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
-        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+        asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x[0]),
+                     "f"(v.x[1]), "f"(v.x[2]), "f"(v.x[3])
+                     : "memory");
     } else if constexpr (V == 2) {
-        float2 t = __ldcg(reinterpret_cast<const float2 *>(p));
-        r.x[0] = t.x; r.x[1] = t.y;
+        asm volatile("st.relaxed.gpu.global.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(v.x[0]), "f"(v.x[1])
+                     : "memory");
     } else {
-        r.x[0] = __ldcg(p);
+        asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v.x[0]) : "memory");
     }
-    return r;
 }
-template <int V> __device__ __forceinline__ Vec<V> ldv_s(const float *p) {
-    Vec<V> r;
-    if constexpr (V == 4) {
-        float4 t = *reinterpret_cast<const float4 *>(p);
-        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
-    } else if constexpr (V == 2) {
-        float2 t = *reinterpret_cast<const float2 *>(p);
-        r.x[0] = t.x; r.x[1] = t.y;
-    } else {
-        r.x[0] = *p;
-    }
-    return r;
-}
-template <int V> __device__ __forceinline__ void stv_s(float *p, const Vec<V> &v) {
+template <int V> __device__ __forceinline__ void st_plain(float *p, const Vec<V> &v) {
     if constexpr (V == 4) {
         *reinterpret_cast<float4 *>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
     } else if constexpr (V == 2) {
@@ -107,99 +92,49 @@ template <int V> __device__ __forceinline__ void stv_s(float *p, const Vec<V> &v
         *p = v.x[0];
     }
 }
-template <int V> __device__ __forceinline__ void stv_g(float *p, const Vec<V> &v) {
+template <int V> __device__ __forceinline__ Vec<V> ld_s(const float *p) {
+    Vec<V> r;
     if constexpr (V == 4) {
-        __stcg(reinterpret_cast<float4 *>(p), make_float4(v.x[0], v.x[1], v.x[2], v.x[3]));
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
     } else if constexpr (V == 2) {
-        __stcg(reinterpret_cast<float2 *>(p), make_float2(v.x[0], v.x[1]));
+        const float2 t = *reinterpret_cast<const float2 *>(p);
+        r.x[0] = t.x; r.x[1] = t.y;
     } else {
-        __stcg(p, v.x[0]);
+        r.x[0] = *p;
     }
+    return r;
+}
+template <int V> __device__ __forceinline__ void st_s(float *p, const Vec<V> &v) { st_plain<V>(p, v); }
+
+template <int V> __device__ __forceinline__ bool has_nan(const Vec<V> &v) {
+    bool b = false;
+#pragma unroll
+    for (int j = 0; j < V; ++j) b |= (v.x[j] != v.x[j]);
+    return b;
 }
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
+// V floats global -> shared, asynchronous (LDGSTS); 16-byte copies bypass L1
+template <int V> __device__ __forceinline__ void cp_async_v(float *dst, const float *src) {
+    if constexpr (V == 4) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                     : "memory");
+    } else if constexpr (V == 2) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src)
+                     : "memory");
+    } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+                     : "memory");
+    }
 }
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
+__device__ __forceinline__ void cp_async_commit_wait() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-struct PassParams {
-    // level-ordered CSR of this direction: row i <-> node node_of[i]
-    const int32_t *row_ptr;    // [n+1]
-    const int32_t *nbr;        // [m] neighbour node id (fan-in src / fan-out dst)
-    const int32_t *eid;        // [m] edge id (delay row)
-    const int32_t *node_of;    // [n]
-    const int4 *cta_pc;        // per-CTA piece sequence (pass order): {pos_begin, pos_end,
-                               // edge_begin, edge_end}
-    const int32_t *cta_lv;     // level of each entry of cta_pc
-    const int32_t *cta_off;    // [P+1] first entry of every CTA
-    const int32_t *piece_off;  // [L+1] first piece of every level (pieces per level)
-    int32_t L;
-    int32_t ncap, ecap;        // staged rows / edges per ring slot
-    int32_t split;             // rows longer than this are cut into part pieces
-    int32_t psize;             // edges per part piece
-    const int32_t *q;          // [n+1] first part id of every row (split rows)
-    const int32_t *part_np;    // [parts] number of parts of the row whose first part id it is
-    float *part_buf;           // [parts][S] partial results of part pieces
-    int32_t *part_cnt;         // [parts] parts finished, indexed by a row's first part id
-    int32_t S;                 // scenarios (row stride of at / rat / delays)
-    const float *d;            // [m][S]
-    const float *src_val;      // forward: at_src [n] (or null); backward: t_req [S] (or null)
-    float t_scalar;            // backward: T when t_req is null
-    const float *other;        // backward: at (for slack)
-    float *out;                // forward: at; backward: rat
-    float *slack;              // backward, optional [n][S]
-    int32_t *wns_ord;          // backward: [S] ordered-int mins
-    int32_t *done;             // [L] pieces published per level
-    uint32_t *err;
-    // optional timeline (HF_TRACE=1): per piece {level<<8|slot, cta, t_top, t_ready,
-    // t_computed, t_published, edges, rows} in globaltimer ns
-    unsigned long long *trace;
-    int32_t *trace_n;
-    int32_t trace_cap;
-};
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// ring-slot layout in shared memory (bytes); identical on host and device
-struct SlotLayout {
-    int meta, node, rp, nbr, medrow, medpre, d, bytes;
-};
-constexpr int MAXMED = 256;   // medium rows per piece (bounded by ecap / CH)
-constexpr int CH = 8;         // chunk of a medium row pre-reduced by one item
-__host__ __device__ inline SlotLayout slot_layout(int ncap, int ecap, int S) {
-    SlotLayout L;
-    int o = 0;
-    L.meta = o;   o += 16 * 4;
-    L.node = o;   o += ncap * 4;
-    L.rp = o;     o += (ncap + 1) * 4;
-    L.nbr = o;    o += ecap * 4;
-    L.medrow = o; o += MAXMED * 4;
-    L.medpre = o; o += (MAXMED + 1) * 4;
-    o = (o + 127) & ~127;
-    L.d = o;      o += ecap * S * 4;
-    L.bytes = (o + 127) & ~127;
-    return L;
-}
-enum { MT_LV = 0, MT_POS, MT_NN, MT_RB, MT_E, MT_EST, MT_NMED, MT_PART, MT_QB };
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <bool FWD> __device__ __forceinline__ float combine(float best, float x) {
     return FWD ? fmaxf(best, x) : fminf(best, x);
@@ -211,581 +146,387 @@ template <bool FWD> __device__ __forceinline__ float ident() {
     return __int_as_float(FWD ? 0xff800000 : 0x7f800000);   // -inf for max, +inf for min
 }
 
-// combine v into *addr with max (forward) / min (backward); exact, order-free
-template <bool FWD> __device__ __forceinline__ void atomic_combine(float *addr, float v) {
-    int *ai = reinterpret_cast<int *>(addr);
-    int old = __ldcg(ai);
-    for (;;) {
-        const float nv = combine<FWD>(__int_as_float(old), v);
-        if (__float_as_int(nv) == old) return;
-        const int prev = atomicCAS(ai, old, __float_as_int(nv));
-        if (prev == old) return;
-        old = prev;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct FlowParams {
+    // level-ordered CSR of this direction: row i <-> node node_of[i]
+    const int32_t *row_ptr;   // [n+1]
+    const int32_t *nbr;       // [m] neighbour node id, split rows as -(first part id + 1)
+    const int32_t *eid;       // [m] edge id (delay row)
+    const int32_t *node_of;   // [n]
+    const int4 *desc;         // task descriptors (TaskSched)
+    const int32_t *nt;        // [L] tasks per chunk of pass-level q
+    const int32_t *doff;      // [L+1]
+    const int32_t *tb;        // [L+1] first global task of pass-level q
+    int32_t L, S, nch;
+    int32_t ecap, ncap;       // per-warp scratch capacity (edges, rows)
+    const int32_t *part_np;   // [parts] by first part id
+    float *part_buf;          // [parts][S]
+    const float *d;           // [m][S] by edge id
+    const float *src_val;     // forward: at_src [n] (or null); backward: t_req [S] (or null)
+    float t_scalar;           // backward: T when t_req is null
+    const float *other;       // backward: at (for slack)
+    float *out;               // forward: at; backward: rat
+    float *slack;             // backward, optional [n][S]
+    int32_t *wns_ord;         // backward: [S] ordered-int minima
+    uint32_t *err;
+    int32_t sleep_max;        // ns, cap of the poll back-off
+    int32_t poll_all;         // 1: every lane re-polls its missing vectors; 0: one lane polls
+    unsigned long long *trace;   // optional: per task {t, level, t_start, t_ready, t_done}
+    int32_t trace_cap;
+};
+
+// per-warp shared-memory scratch (bytes), identical on host and device
+struct WarpLayout {
+    int d, at, nbr, eid, rp, node, bytes;
+};
+__host__ __device__ inline WarpLayout warp_layout(int ecap, int ncap, int SC, bool fwd) {
+    WarpLayout L;
+    int o = 0;
+    L.d = o;    o += ecap * SC * 4;
+    L.at = o;   o += fwd ? 0 : ncap * SC * 4;
+    L.nbr = o;  o += ecap * 4;
+    L.eid = o;  o += ecap * 4;
+    L.rp = o;   o += (ncap + 1) * 4;
+    L.node = o; o += ncap * 4;
+    L.bytes = (o + 15) & ~15;
+    return L;
+}
+__host__ __device__ inline int wmin_bytes(int S) { return (S * 4 + 15) & ~15; }
+
+// one task's index data, loaded into registers one task ahead (NSL slots per lane:
+// a task has <= 32*NSL edges and <= 32*NSL - 1 rows)
+template <int NSL> struct Idx {
+    int4 dsc;
+    int c;
+    int nbr0, eid0, rp0, node0;   // slot 0: edge / row `lane`
+    int nbr1, eid1, rp1, node1;   // slot 1: edge / row `lane + 32` (NSL == 2)
+};
+template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
+
+template <int V, int LPN, bool FWD, bool CHECK_D, int RB>
+__global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
+    constexpr int SC = V * LPN;   // columns per chunk
+    constexpr int G = 32 / LPN;   // lane groups per warp
+    constexpr int NSL = idx_slots<LPN>();
+    // RB: gathers in flight per lane per batch
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane / LPN, gl = lane % LPN;
+    const int S = p.S;
+    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD);
+    int32_t *s_wmin = reinterpret_cast<int32_t *>(smem);
+    unsigned char *wb = smem + wmin_bytes(S) + wib * WL.bytes;
+    float *s_d = reinterpret_cast<float *>(wb + WL.d);
+    float *s_at = reinterpret_cast<float *>(wb + WL.at);
+    int32_t *s_nbr = reinterpret_cast<int32_t *>(wb + WL.nbr);
+    int32_t *s_eid = reinterpret_cast<int32_t *>(wb + WL.eid);
+    int32_t *s_rp = reinterpret_cast<int32_t *>(wb + WL.rp);
+    int32_t *s_node = reinterpret_cast<int32_t *>(wb + WL.node);
+
+    if (!FWD) {
+        for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
+        __syncthreads();
     }
-}
+    const int W = gridDim.x * NWARP;
+    const int w = wib * gridDim.x + blockIdx.x;   // consecutive tasks on different SMs
+    const int T = __ldg(p.tb + p.L);
+    const int L = p.L;
 
-// at[u] / rat[u] of a neighbour; a neighbour that is a split row is encoded as
-// -(first part id + 1) and read as the combine of its part partials (the row's
-// own value is finalised off the critical path)
-template <int V, bool FWD>
-__device__ __forceinline__ Vec<V> gather_val(const PassParams &p, int u, int64_t col) {
-    if (u >= 0) return ldv_cg<V>(p.out + int64_t(u) * p.S + col);
-    const int qb = -u - 1;
-    const int np = __ldg(p.part_np + qb);
-    Vec<V> a = ldv_cg<V>(p.part_buf + int64_t(qb) * p.S + col);
-    for (int k = 1; k < np; ++k) {
-        const Vec<V> b = ldv_cg<V>(p.part_buf + int64_t(qb + k) * p.S + col);
-#pragma unroll
-        for (int j = 0; j < V; ++j) a.x[j] = combine<FWD>(a.x[j], b.x[j]);
-    }
-    return a;
-}
-
-__device__ __forceinline__ int pieces_in(const PassParams &p, int k) {
-    return __ldg(p.piece_off + k + 1) - __ldg(p.piece_off + k);
-}
-
-// ---- mbarrier / bulk-copy / named-barrier PTX ----------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-                     smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred q;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 q, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, q;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void consumer_sync() {   // named barrier 1: consumer warps only
-    asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");
-}
-
-// One CTA per SM: warps NCW.. are producers (stage pieces into a NBUF-slot ring
-// with TMA bulk copies, off the critical path); warps 0..NCW-1 compute.
-template <int V, bool FWD, bool CHECK_D, bool BULK>
-__global__ void __launch_bounds__(BLOCK, 1) k_propagate(PassParams p) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    const SlotLayout SL = slot_layout(p.ncap, p.ecap, p.S);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NBUF * SL.bytes);
-    uint64_t *empty = full + NBUF;
-    float *s_part = reinterpret_cast<float *>(empty + NBUF);                  // [NC*V]
-    int32_t *s_min = reinterpret_cast<int32_t *>(s_part + NC * V);           // [S]
-    float *s_row = reinterpret_cast<float *>(s_min + p.S);                    // [S]
-    __shared__ int s_nhub;
-    __shared__ int s_hub[MAX_HUBS];
-
-    const int tid = threadIdx.x;
-    const int b = blockIdx.x;
-    const int seq0 = __ldg(p.cta_off + b), nseq = __ldg(p.cta_off + b + 1) - seq0;
-    if (tid == 0) {
-        for (int s = 0; s < NBUF; ++s) {
-            mbar_init(full + s, 32);
-            mbar_init(empty + s, NCW);
+    // ---- task locator: pass-level q with tb[q] <= t < tb[q+1] (t increases) ----
+    auto locate = [&](int t, int &q, int &c, int4 &dsc) {
+        if (__ldg(p.tb + q + 1) <= t) {
+            int lo = q + 1, step = 1;
+            while (lo + step < L && __ldg(p.tb + lo + step) <= t) {
+                lo += step;
+                step <<= 1;
+            }
+            int hi = min(lo + step, L);
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(p.tb + mid) <= t) lo = mid;
+                else hi = mid;
+            }
+            q = lo;
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (!FWD)
-        for (int s = tid; s < p.S; s += BLOCK) s_min[s] = 0x7f800000;
-    __syncthreads();
-
-    if (tid >= NC) {
-        // ============================ producers (NPW warps) ============================
-        // warp w stages pieces t = w, w + NPW, ...; every load of a piece depends only
-        // on its (prefetched) descriptor, so rows, neighbour ids and edge ids are
-        // fetched in one round of independent loads, then the delay rows follow as
-        // TMA bulk copies completing on the slot's mbarrier.
-        const int pw = (tid - NC) >> 5, lane = (tid - NC) & 31;
-        int4 pcn = make_int4(0, 0, 0, 0);
-        int lvn = 0;
-        if (pw < nseq) {
-            pcn = __ldg(p.cta_pc + seq0 + pw);
-            lvn = __ldg(p.cta_lv + seq0 + pw);
+        const int rel = t - __ldg(p.tb + q);
+        const int ntq = __ldg(p.nt + q);
+        c = rel / ntq;
+        const int j = rel - c * ntq;
+        dsc = __ldg(p.desc + __ldg(p.doff + q) + j);
+    };
+    // index loads of one task (no use of the results here: they land during the
+    // current task)
+    auto load_idx = [&](const int4 &dsc, Idx<NSL> &x) {
+        const bool part = dsc.y < 0;
+        const int E = dsc.w - dsc.z;
+        const int NR = part ? 1 : dsc.y - dsc.x;
+        const int k0 = lane, k1 = lane + 32;
+        x.nbr0 = k0 < E ? __ldg(p.nbr + dsc.z + k0) : 0;
+        x.eid0 = k0 < E ? __ldg(p.eid + dsc.z + k0) : 0;
+        x.rp0 = (!part && k0 <= NR) ? __ldg(p.row_ptr + dsc.x + k0) : 0;
+        x.node0 = k0 < NR ? __ldg(p.node_of + dsc.x + k0) : 0;
+        if (NSL == 2) {
+            x.nbr1 = k1 < E ? __ldg(p.nbr + dsc.z + k1) : 0;
+            x.eid1 = k1 < E ? __ldg(p.eid + dsc.z + k1) : 0;
+            x.rp1 = (!part && k1 <= NR) ? __ldg(p.row_ptr + dsc.x + k1) : 0;
+            x.node1 = k1 < NR ? __ldg(p.node_of + dsc.x + k1) : 0;
         }
-        for (int t = pw; t < nseq; t += NPW) {
-            const int st = t % NBUF;
-            const int4 pc = pcn;
-            const int lvl = lvn;
-            if (t + NPW < nseq) {   // prefetch the next descriptor
-                pcn = __ldg(p.cta_pc + seq0 + t + NPW);
-                lvn = __ldg(p.cta_lv + seq0 + t + NPW);
-            }
-            mbar_wait(empty + st, ((t / NBUF) & 1) ^ 1);
-            unsigned char *sb = smem + st * SL.bytes;
-            int32_t *meta = reinterpret_cast<int32_t *>(sb + SL.meta);
-            int32_t *s_node = reinterpret_cast<int32_t *>(sb + SL.node);
-            int32_t *s_rp = reinterpret_cast<int32_t *>(sb + SL.rp);
-            int32_t *s_nbr = reinterpret_cast<int32_t *>(sb + SL.nbr);
-            int32_t *s_mr = reinterpret_cast<int32_t *>(sb + SL.medrow);
-            int32_t *s_mp = reinterpret_cast<int32_t *>(sb + SL.medpre);
-            float *s_d = reinterpret_cast<float *>(sb + SL.d);
-            const int pos0 = pc.x, nn = pc.y - pc.x, rb = pc.z, E = pc.w - pc.z;
-            const int nst = min(nn, p.ncap), est = min(E, p.ecap);
-            const int rounds = max((nst + 1 + 127) / 128, (est + 127) / 128);
-            for (int r0 = 0; r0 < rounds; ++r0) {
-                int nd[4], rpv[4], nb[4], ev[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {   // independent loads first
-                    const int i = r0 * 128 + u * 32 + lane;
-                    if (i < nst) nd[u] = __ldg(p.node_of + pos0 + i);
-                    if (i <= nst) rpv[u] = __ldg(p.row_ptr + pos0 + i);
-                    if (i < est) {
-                        nb[u] = __ldg(p.nbr + rb + i);
-                        ev[u] = __ldg(p.eid + rb + i);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = r0 * 128 + u * 32 + lane;
-                    if (i < nst) s_node[i] = nd[u];
-                    if (i <= nst) s_rp[i] = rpv[u] - rb;
-                    if (i < est) {
-                        s_nbr[i] = nb[u];
-                        const float *src = p.d + int64_t(ev[u]) * p.S;
-                        if (BULK) {
-                            bulk_g2s(s_d + int64_t(i) * p.S, src, uint32_t(p.S) * 4u, full + st);
-                        } else {
-                            for (int c = 0; c < p.S; ++c) s_d[int64_t(i) * p.S + c] = __ldg(src + c);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            // part piece: one slice of a split row; else list the medium rows
-            const bool part = nn == 1 && (s_rp[1] - s_rp[0]) > p.split;
-            int nrow = 0, nchk = 0;
-            if (!part) {
-                for (int i0 = 0; i0 < nst; i0 += 32) {
-                    const int i = i0 + lane;
-                    int nch = 0;
-                    if (i < nst) {
-                        const int eb = s_rp[i], ee = s_rp[i + 1];
-                        if (ee - eb > CH && ee - eb <= p.split && ee <= est)
-                            nch = (ee - eb + CH - 1) / CH;
-                    }
-                    const unsigned mk = __ballot_sync(0xffffffffu, nch > 0);
-                    if (mk == 0) continue;
-                    int incl = nch;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    if (nch > 0) {
-                        const int slot = nrow + __popc(mk & ((1u << lane) - 1u));
-                        if (slot < MAXMED) {
-                            s_mr[slot] = i;
-                            s_mp[slot] = nchk + incl - nch;
-                        }
-                    }
-                    nrow += __popc(mk);
-                    nchk += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (nrow > MAXMED) {   // cannot happen with ecap/CH <= MAXMED; stay correct
-                    nrow = 0;
-                    nchk = 0;
-                }
-            }
-            if (lane == 0) {
-                s_mp[nrow] = nchk;
-                meta[MT_LV] = lvl;
-                meta[MT_POS] = pos0;
-                meta[MT_NN] = nn;
-                meta[MT_RB] = rb;
-                meta[MT_E] = E;
-                meta[MT_EST] = est;
-                meta[MT_NMED] = nrow;
-                meta[MT_PART] = part;
-                meta[MT_QB] = part ? __ldg(p.q + pos0) : 0;
-            }
-            __syncwarp();
-            if (BULK && lane == 0)
-                mbar_arrive_tx(full + st, uint32_t(est) * uint32_t(p.S) * 4u);
-            else
-                mbar_arrive(full + st);
-        }
-        return;
-    }
+    };
 
-    // ================================= consumers ==================================
-    const int warp = tid >> 5, wl = tid & 31;
-    const int lpn = p.S / V;                       // lanes per node row
-    const int active = (NC / lpn) * lpn;           // threads with a fixed lane
-    const int slots = active / lpn;                // rows handled side by side
-    const int lane = tid % lpn;
-    const int64_t col = int64_t(lane) * V;
-    const bool pow2 = (lpn & (lpn - 1)) == 0;
     bool bad = false;
-    Vec<V> run_min;
+    Vec<V> run;   // backward: running min of slack for column chunk run_c
+    int run_c = -1;
 #pragma unroll
-    for (int k = 0; k < V; ++k) run_min.x[k] = ident<false>();
-
-    for (int t = 0; t < nseq; ++t) {
-        const int st = t % NBUF;
-        const unsigned long long t_top = p.trace ? gtimer() : 0;
-        mbar_wait(full + st, (t / NBUF) & 1);
-        unsigned char *sb = smem + st * SL.bytes;
-        const int32_t *meta = reinterpret_cast<const int32_t *>(sb + SL.meta);
-        const int32_t *s_node = reinterpret_cast<const int32_t *>(sb + SL.node);
-        const int32_t *s_rp = reinterpret_cast<const int32_t *>(sb + SL.rp);
-        const int32_t *s_nbr = reinterpret_cast<const int32_t *>(sb + SL.nbr);
-        const int32_t *s_mr = reinterpret_cast<const int32_t *>(sb + SL.medrow);
-        const int32_t *s_mp = reinterpret_cast<const int32_t *>(sb + SL.medpre);
-        float *s_d = reinterpret_cast<float *>(sb + SL.d);
-        const int kc = meta[MT_LV], pos0 = meta[MT_POS], nn = meta[MT_NN], rb = meta[MT_RB];
-        const int E = meta[MT_E], est = meta[MT_EST], nmed = meta[MT_NMED];
-        const bool part = meta[MT_PART] != 0;
-        const int nst = min(nn, p.ncap);
-        // split-row bookkeeping, read now: the slot is recycled once the piece publishes
-        const int part_node = part ? s_node[0] : 0;
-        const int part_qb = part ? meta[MT_QB] : 0;
-        const int part_n = part ? (s_rp[1] - s_rp[0] + p.psize - 1) / p.psize : 0;
-
-        // (a) backward: prefetch at[] of this thread's first four rows (for the slack)
-        Vec<V> pre_at[4];
-        if (!FWD && tid < active) {
+    for (int j = 0; j < V; ++j) run.x[j] = ident<false>();
+    auto flush_run = [&]() {
+        if (!FWD && run_c >= 0) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int i = tid / lpn + r * slots;
-                if (i < nst) pre_at[r] = ldv_cg<V>(p.other + int64_t(s_node[i]) * p.S + col);
-            }
+            for (int j = 0; j < V; ++j)
+                if (run.x[j] != ident<false>())
+                    atomicMin(s_wmin + run_c * SC + gl * V + j, f2ord(run.x[j]));
+#pragma unroll
+            for (int j = 0; j < V; ++j) run.x[j] = ident<false>();
         }
-        // (b) wait until the previous level (pass order) is fully published; a level
-        // whose only piece was this CTA's needs no poll (named barriers order it)
-        const int dep = FWD ? kc - 1 : kc + 1;
-        if (tid == 0 && dep >= 0 && dep < p.L) {
-            const int np = pieces_in(p, dep);
-            if (!(np == 1 && b == 0)) {
-                const int need = np;
-                if (ld_acquire(p.done + dep) < need)
-                    while (ld_acquire(p.done + dep) < need) __nanosleep(20);
-            }
-        }
-        consumer_sync();
-        const unsigned long long t_ready = p.trace ? gtimer() : 0;
-        if (tid == 0) s_nhub = 0;
+    };
 
-        // (c1) edge-parallel: x = fl(a[u] +/- d) in place over the staged delay; up to
-        // four items per thread issue their gathers together (one L2 round trip)
-        if (pow2) {
-            const int estep = NC / lpn, e0 = tid / lpn;
-            for (int eb = e0; eb < est; eb += 4 * estep) {
-                Vec<V> a[4];
+    // software pipeline: D1 = descriptor of the next task, X0 = index registers of
+    // the current task, X1 of the next
+    int qa = 0, qb = 0;          // locator cursors of the two look-ahead streams
+    int t0 = w;
+    Idx<NSL> X0, X1;
+    int4 D1 = make_int4(0, 0, 0, 0);
+    int c1 = 0;
+    if (t0 < T) {
+        locate(t0, qa, X0.c, X0.dsc);
+        load_idx(X0.dsc, X0);
+        qb = qa;
+        if (t0 + W < T) locate(t0 + W, qb, c1, D1);
+    }
+    for (int t = t0; t < T; t += W) {
+        const unsigned long long tr0 = p.trace ? gtimer() : 0;
+        // ---- (1) this task's index data -> shared scratch; stage delays (+ at) ----
+        const int4 dsc = X0.dsc;
+        const int c = X0.c;
+        const bool part = dsc.y < 0;
+        const int E = dsc.w - dsc.z;
+        const int NR = part ? 1 : dsc.y - dsc.x;
+        const int col = c * SC + gl * V;
+        if (lane < E) {
+            s_nbr[lane] = X0.nbr0;
+            s_eid[lane] = X0.eid0;
+        }
+        if (!part && lane <= NR) s_rp[lane] = X0.rp0 - dsc.z;
+        if (lane < NR) s_node[lane] = X0.node0;
+        if (NSL == 2) {
+            const int k = lane + 32;
+            if (k < E) {
+                s_nbr[k] = X0.nbr1;
+                s_eid[k] = X0.eid1;
+            }
+            if (!part && k <= NR) s_rp[k] = X0.rp1 - dsc.z;
+            if (k < NR) s_node[k] = X0.node1;
+        }
+        __syncwarp();
+        for (int k = g; k < E; k += G)
+            cp_async_v<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col);
+        if (!FWD && !part)
+            for (int i = g; i < NR; i += G)
+                cp_async_v<V>(s_at + i * SC + gl * V, p.other + int64_t(s_node[i]) * S + col);
+        cp_async_commit();
+        // ---- (2) look-ahead: index loads of the next task, descriptor of the one after
+        if (t + W < T) {
+            X1.dsc = D1;
+            X1.c = c1;
+            load_idx(D1, X1);
+            if (t + 2 * W < T) locate(t + 2 * W, qb, c1, D1);
+        }
+        // ---- (3) edge-parallel gathers: x = fl(a[u] +/- d), sentinel-polled ----
+        unsigned long long tr1 = 0;
+        for (int k0 = 0; k0 < E; k0 += G * RB) {
+            Vec<V> a[RB];
+            int uu[RB];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int e = eb + r * estep;
-                    if (e < est) a[r] = gather_val<V, FWD>(p, s_nbr[e], col);
-                }
+            for (int r = 0; r < RB; ++r) {
+                const int k = k0 + r * G + g;
+                uu[r] = k < E ? s_nbr[k] : INT32_MAX;
+                if (uu[r] >= 0 && uu[r] != INT32_MAX)
+                    a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);
+            }
+            // neighbours cut into parts: combine of their partials (rare)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const int e = eb + r * estep;
-                    if (e < est) {
-                        float *dp = s_d + int64_t(e) * p.S + col;
-                        const Vec<V> dd = ldv_s<V>(dp);
-                        Vec<V> x;
+            for (int r = 0; r < RB; ++r) {
+                if (uu[r] < 0) {
+                    const int q0 = -uu[r] - 1;
+                    const int np = __ldg(p.part_np + q0);
 #pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            float d1 = dd.x[j];
-                            if (CHECK_D) {
-                                bad |= !isfinite(d1);
-                                d1 = canon0(d1);
-                            }
-                            x.x[j] = relax<FWD>(a[r].x[j], d1);
+                    for (int j = 0; j < V; ++j) a[r].x[j] = ident<FWD>();
+                    for (int k = 0; k < np; ++k) {
+                        const float *src = p.part_buf + int64_t(q0 + k) * S + col;
+                        Vec<V> v = ld_relaxed<V>(src);
+                        int ns = 32;
+                        while (has_nan<V>(v)) {
+                            __nanosleep(ns);
+                            ns = min(ns * 2, p.sleep_max);
+                            v = ld_relaxed<V>(src);
                         }
-                        stv_s<V>(dp, x);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) a[r].x[j] = combine<FWD>(a[r].x[j], v.x[j]);
                     }
                 }
             }
-        } else {
-            for (int q = tid; q < est * lpn; q += NC) {
-                const int e = q / lpn, l = q - e * lpn;
-                float *dp = s_d + int64_t(e) * p.S + l * V;
-                const Vec<V> dd = ldv_s<V>(dp);
-                const Vec<V> a = gather_val<V, FWD>(p, s_nbr[e], int64_t(l) * V);
-                Vec<V> x;
+            // wait until every gathered element is final (not the NaN sentinel): one
+            // lane polls one missing vector with back-off, then all lanes re-load
+            bool miss = false;
 #pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    float d1 = dd.x[j];
-                    if (CHECK_D) {
-                        bad |= !isfinite(d1);
-                        d1 = canon0(d1);
+            for (int r = 0; r < RB; ++r)
+                if (uu[r] >= 0 && uu[r] != INT32_MAX) miss |= has_nan<V>(a[r]);
+            unsigned bal = __ballot_sync(FULL, miss);
+            int ns = 32;
+            while (bal) {
+                if (p.poll_all) {
+                    // every lane re-loads its own missing vectors (one round trip per round)
+                    __nanosleep(ns);
+                    ns = min(ns * 2, p.sleep_max);
+                } else if (lane == __ffs(bal) - 1) {
+                    // one lane polls one missing vector with back-off, then all re-load
+                    const float *src = nullptr;
+#pragma unroll
+                    for (int r = RB - 1; r >= 0; --r)
+                        if (uu[r] >= 0 && uu[r] != INT32_MAX && has_nan<V>(a[r]))
+                            src = p.out + int64_t(uu[r]) * S + col;
+                    Vec<V> v = ld_relaxed<V>(src);
+                    while (has_nan<V>(v)) {
+                        __nanosleep(ns);
+                        ns = min(ns * 2, p.sleep_max);
+                        v = ld_relaxed<V>(src);
                     }
-                    x.x[j] = relax<FWD>(a.x[j], d1);
                 }
-                stv_s<V>(dp, x);
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+                    if (uu[r] >= 0 && uu[r] != INT32_MAX && has_nan<V>(a[r]))
+                        a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);
+                miss = false;
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+                    if (uu[r] >= 0 && uu[r] != INT32_MAX) miss |= has_nan<V>(a[r]);
+                bal = __ballot_sync(FULL, miss);
+            }
+            if (p.trace && k0 == 0) tr1 = gtimer();
+            cp_async_wait();   // this lane's own delay copies (it reads only those)
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                const int k = k0 + r * G + g;
+                if (k < E) {
+                    float *dp = s_d + k * SC + gl * V;
+                    const Vec<V> dv = ld_s<V>(dp);
+                    Vec<V> x;
+#pragma unroll
+                    for (int j = 0; j < V; ++j) {
+                        float d1 = dv.x[j];
+                        if (CHECK_D) {
+                            bad |= !isfinite(d1);
+                            d1 = canon0(d1);
+                        }
+                        x.x[j] = relax<FWD>(a[r].x[j], d1);
+                    }
+                    st_s<V>(dp, x);
+                }
             }
         }
-        consumer_sync();
-
-        auto node_at = [&](int i) { return i < nst ? s_node[i] : __ldg(p.node_of + pos0 + i); };
-        auto rel = [&](int i) { return i <= nst ? s_rp[i] : __ldg(p.row_ptr + pos0 + i) - rb; };
-        auto finish = [&](int node, const Vec<V> &best, int i) {
-            stv_g<V>(p.out + int64_t(node) * p.S + col, best);
-            if (!FWD) {
-                const int rr = i >= 0 ? (i - tid / lpn) / slots : 4;
-                const Vec<V> a = (rr < 4 && i < nst)
-                                     ? (rr == 0   ? pre_at[0]
-                                        : rr == 1 ? pre_at[1]
-                                        : rr == 2 ? pre_at[2]
-                                                  : pre_at[3])
-                                     : ldv_cg<V>(p.other + int64_t(node) * p.S + col);
-                Vec<V> sl;
-#pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
-                    run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
-                }
-                if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
-            }
-        };
-        // gather-reduce of unstaged edges [e, ee) with stride `step` (rare paths)
-        auto tail = [&](int e, int ee, int step, Vec<V> &acc) {   // rare paths
-            for (; e < ee; e += 2 * step) {
-                Vec<V> a[2], dd[2];
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int er = e + r * step;
-                    if (er < ee) {
-                        const int ge = rb + er;
-                        a[r] = gather_val<V, FWD>(p, __ldg(p.nbr + ge), col);
-                        dd[r] = ldv_g<V>(p.d + int64_t(__ldg(p.eid + ge)) * p.S + col);
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    if (e + r * step < ee) {
-#pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            float d1 = dd[r].x[j];
-                            if (CHECK_D) {
-                                bad |= !isfinite(d1);
-                                d1 = canon0(d1);
-                            }
-                            acc.x[j] = combine<FWD>(acc.x[j], relax<FWD>(a[r].x[j], d1));
-                        }
-                    }
-                }
-            }
-        };
-
+        cp_async_wait();
+        __syncwarp();
+        // ---- (4) reduce rows / the part, store ----
         if (part) {
-            // (c1b) one slice of a split row: partial over the staged edges by all slots,
-            // stored to the row's part buffer; the last slice to finish (atomic count)
-            // combines all partials and writes the row -- exact, no float atomics
-            const int node = s_node[0];
-            const int slot = tid / lpn;
-            const int deg = s_rp[1] - s_rp[0];
-            const int nparts = (deg + p.psize - 1) / p.psize;
-            const int pid = meta[MT_QB] + (-s_rp[0]) / p.psize;
             Vec<V> acc;
 #pragma unroll
             for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
-            if (tid < active)
-                for (int e = slot; e < est; e += slots) {
-                    const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
+            for (int k = g; k < E; k += G) {   // the edges this group computed
+                const Vec<V> x = ld_s<V>(s_d + k * SC + gl * V);
 #pragma unroll
-                    for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
-                }
-            stv_s<V>(s_part + int64_t(tid) * V, acc);
-            consumer_sync();
-            if (tid < lpn) {
-                Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
-                for (int s2 = 1; s2 < slots; ++s2) {
-                    const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
-                }
-                if (nparts == 1) {   // the whole row: final value directly
-                    stv_g<V>(p.out + int64_t(node) * p.S + col, best);
-                    if (!FWD) {
-                        const Vec<V> a = ldv_cg<V>(p.other + int64_t(node) * p.S + col);
-                        Vec<V> sl;
-#pragma unroll
-                        for (int j = 0; j < V; ++j) {
-                            sl.x[j] = __fsub_rn(best.x[j], a.x[j]);
-                            run_min.x[j] = fminf(run_min.x[j], sl.x[j]);
-                        }
-                        if (p.slack) stv_g<V>(p.slack + int64_t(node) * p.S + col, sl);
-                    }
-                } else {   // readers combine the partials; finalised after the publish
-                    stv_g<V>(p.part_buf + int64_t(pid) * p.S + col, best);
-                }
+                for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
             }
+#pragma unroll
+            for (int o = LPN; o < 32; o <<= 1)
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    acc.x[j] = combine<FWD>(acc.x[j], __shfl_xor_sync(FULL, acc.x[j], o));
+            if (g == 0) st_relaxed<V>(p.part_buf + int64_t(-dsc.y - 1) * S + col, acc);
         } else {
-            // (c1c) medium rows: every CH-edge chunk pre-reduced in place (partial over
-            // the chunk's first edge) by all threads in parallel
-            if (nmed > 0) {
-                const int items = s_mp[nmed] * lpn;
-                for (int q = tid; q < items; q += NC) {
-                    const int c = q / lpn, l = q - c * lpn;
-                    int lo = 0, hi = nmed - 1;   // last r with s_mp[r] <= c
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (s_mp[mid] <= c) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    const int i = s_mr[lo];
-                    const int eb = s_rp[i] + (c - s_mp[lo]) * CH;
-                    const int ee = min(s_rp[i + 1], eb + CH);
-                    float *dp = s_d + int64_t(eb) * p.S + l * V;
-                    Vec<V> acc = ldv_s<V>(dp);
-                    for (int e = eb + 1; e < ee; ++e) {
-                        const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + l * V);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
-                    }
-                    stv_s<V>(dp, acc);
-                }
-                consumer_sync();
+            if (!FWD && c != run_c) {
+                flush_run();
+                run_c = c;
             }
-            // (c2) rows reduced by their owner lanes; unstaged long rows deferred
-            if (tid < active) {
-                for (int i = tid / lpn; i < nn; i += slots) {
-                    const int eb = rel(i), ee = rel(i + 1);
-                    const int deg = ee - eb;
-                    if (deg > p.split) continue;   // split rows live in part pieces
-                    const bool chunked = deg > CH && ee <= est && nmed > 0 && i < nst;
-                    if (deg > HUB_DEG && ee > est) {
-                        if (lane == 0) {
-                            const int h = atomicAdd(&s_nhub, 1);
-                            if (h < MAX_HUBS) s_hub[h] = i;
-                            else atomicOr(p.err, 0x80000000u);
-                        }
-                        continue;
-                    }
-                    const int node = node_at(i);
-                    Vec<V> best;
-                    if (deg == 0) {
-                        if (FWD) {
-                            const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+            for (int i = g; i < NR; i += G) {
+                const int eb = s_rp[i], ee = s_rp[i + 1];
+                const int node = s_node[i];
+                Vec<V> best;
+                if (ee == eb) {
+                    if (FWD) {
+                        const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
 #pragma unroll
-                            for (int j = 0; j < V; ++j) best.x[j] = a0;
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < V; ++j)
-                                best.x[j] =
-                                    canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
-                        }
+                        for (int j = 0; j < V; ++j) best.x[j] = a0;
                     } else {
 #pragma unroll
-                        for (int j = 0; j < V; ++j) best.x[j] = ident<FWD>();
-                        const int es = min(ee, est);
-                        for (int e = eb; e < es; e += chunked ? CH : 1) {
-                            const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
-#pragma unroll
-                            for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
-                        }
-                        if (ee > es) tail(max(eb, es), ee, 1, best);
+                        for (int j = 0; j < V; ++j)
+                            best.x[j] = canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
                     }
-                    finish(node, best, i);
+                } else {
+                    best = ld_s<V>(s_d + eb * SC + gl * V);
+                    for (int k = eb + 1; k < ee; ++k) {
+                        const Vec<V> x = ld_s<V>(s_d + k * SC + gl * V);
+#pragma unroll
+                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
+                    }
+                }
+                st_relaxed<V>(p.out + int64_t(node) * S + col, best);
+                if (!FWD) {
+                    const Vec<V> av = ld_s<V>(s_at + i * SC + gl * V);
+                    Vec<V> sl;
+#pragma unroll
+                    for (int j = 0; j < V; ++j) {
+                        sl.x[j] = __fsub_rn(best.x[j], av.x[j]);
+                        run.x[j] = fminf(run.x[j], sl.x[j]);
+                    }
+                    if (p.slack) st_plain<V>(p.slack + int64_t(node) * S + col, sl);
                 }
             }
-            consumer_sync();
-            // (c3) unstaged long rows: all slots, strided, shared-memory combine
-            const int nhub = min(s_nhub, MAX_HUBS);
-            for (int h = 0; h < nhub; ++h) {
-                const int i = s_hub[h];
-                const int eb = rel(i), ee = rel(i + 1);
-                const int slot = tid / lpn;
-                Vec<V> acc;
-#pragma unroll
-                for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
-                if (tid < active) {
-                    int e = eb + slot;
-                    for (; e < ee && e < est; e += slots) {
-                        const Vec<V> x = ldv_s<V>(s_d + int64_t(e) * p.S + col);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
-                    }
-                    tail(e, ee, slots, acc);
-                }
-                stv_s<V>(s_part + int64_t(tid) * V, acc);
-                consumer_sync();
-                if (tid < lpn) {
-                    Vec<V> best = ldv_s<V>(s_part + int64_t(tid) * V);
-                    for (int s2 = 1; s2 < slots; ++s2) {
-                        const Vec<V> q = ldv_s<V>(s_part + int64_t(s2 * lpn + tid) * V);
-#pragma unroll
-                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], q.x[j]);
-                    }
-                    finish(node_at(i), best, -1);
-                }
-                consumer_sync();
-            }
         }
-        // (d) publish: every warp releases its stores at gpu scope, the slot goes back
-        // to the producer, and one thread counts the piece after all warps fenced
-        const unsigned long long t_comp = p.trace ? gtimer() : 0;
-        __syncwarp();
-        if (wl == 0) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            mbar_arrive(empty + st);
-        }
-        consumer_sync();
-        if (tid == 0) atomicAdd(p.done + kc, 1);
-        // split rows (>= 2 parts) are finalised by k_finalize_split after the pass;
-        // readers inside the pass combine their partials
-        if (p.trace && tid == 0) {
-            const int r = atomicAdd(p.trace_n, 1);
+        __syncwarp();   // scratch is rewritten by the next task
+        if (p.trace && lane == 0) {
+            const int r = t;
             if (r < p.trace_cap) {
-                unsigned long long *tr = p.trace + int64_t(r) * 8;
-                tr[0] = (unsigned long long)kc;
-                tr[1] = (unsigned long long)b;
-                tr[2] = t_top;
-                tr[3] = t_ready;
-                tr[4] = t_comp;
-                tr[5] = gtimer();
-                tr[6] = (unsigned long long)E;
-                tr[7] = (unsigned long long)nn;
+                unsigned long long *tr = p.trace + int64_t(r) * 4;
+                tr[0] = (unsigned long long)w;
+                tr[1] = tr0;
+                tr[2] = tr1 ? tr1 : tr0;
+                tr[3] = gtimer();
             }
         }
+        X0 = X1;
     }
 
     if (CHECK_D && bad) atomicOr(p.err, ERR_NONFINITE);
     if (!FWD) {
-        if (tid < active) {
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (run_min.x[j] != ident<false>())
-                    atomicMin(s_min + col + j, f2ord(run_min.x[j]));
-        }
-        consumer_sync();
-        for (int s = tid; s < p.S; s += NC)
-            if (s_min[s] != 0x7f800000) atomicMin(p.wns_ord + s, s_min[s]);
+        flush_run();
+        __syncthreads();
+        for (int s = threadIdx.x; s < S; s += blockDim.x)
+            if (s_wmin[s] != 0x7f800000) atomicMin(p.wns_ord + s, s_wmin[s]);
     }
 }
 
-// After a pass: every row cut into >= 2 part pieces gets its value (combine of the
-// partials), its optional slack and its worst-slack contribution.  One warp per
-// split row; the rows are the positions with degree > split and > psize.
+// After a pass: every split row gets its value (combine of its partials), its
+// optional slack and its worst-slack contribution.  One warp per split row.
 template <bool FWD>
 __global__ void k_finalize_split(const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows,
                                  const int32_t *__restrict__ row_ptr,
                                  const int32_t *__restrict__ node_of, const int32_t *__restrict__ q,
-                                 int32_t psize, int32_t S, const float *__restrict__ part_buf,
+                                 int32_t pe, int32_t S, const float *__restrict__ part_buf,
                                  float *__restrict__ out, const float *__restrict__ other,
                                  float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
     const int lane = threadIdx.x & 31;
@@ -794,7 +535,7 @@ __global__ void k_finalize_split(const int32_t *__restrict__ rows, const int32_t
     for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < cnt; r += nw) {
         const int i = rows[r];
         const int d = row_ptr[i + 1] - row_ptr[i];
-        const int np = (d + psize - 1) / psize, qb = q[i];
+        const int np = (d + pe - 1) / pe, qb = q[i];
         const int64_t node = node_of[i];
         for (int s = lane; s < S; s += 32) {
             float v = part_buf[int64_t(qb) * S + s];
@@ -807,61 +548,6 @@ __global__ void k_finalize_split(const int32_t *__restrict__ rows, const int32_t
             }
         }
     }
-}
-
-// positions of the rows cut into >= 2 parts (read through their partials)
-__global__ void k_split_list(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                             int32_t psize, int32_t *__restrict__ rows, int32_t *__restrict__ cnt) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int d = row_ptr[i + 1] - row_ptr[i];
-        if (d > split && d > psize) rows[atomicAdd(cnt, 1)] = int(i);
-    }
-}
-
-// Backward sinks (out-degree 0) do not depend on any level: rat = T_s, their
-// slack and worst-slack contribution, in one bandwidth-bound sweep before the pass.
-template <int V>
-__global__ void k_bwd_sinks(const int32_t *__restrict__ out_ptr, int32_t n, int32_t S,
-                            const float *__restrict__ t_arr, float t_scalar,
-                            const float *__restrict__ at, float *__restrict__ rat,
-                            float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
-    extern __shared__ int32_t s_wmin[];
-    for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
-    __syncthreads();
-    const int lpn = S / V;
-    const int apb = blockDim.x / lpn * lpn;                 // active threads per block
-    const int64_t step = int64_t(gridDim.x) * apb;          // a multiple of lpn: lane fixed
-    const int64_t t0 = blockIdx.x * int64_t(apb) + threadIdx.x;
-    const int lane = int(threadIdx.x % lpn);
-    float mn[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
-    if (int(threadIdx.x) < apb) {
-        for (int64_t t = t0; t < int64_t(n) * lpn; t += step) {
-            const int64_t v = t / lpn;
-            if (out_ptr[v + 1] != out_ptr[v]) continue;
-            const int64_t o = v * S + int64_t(lane) * V;
-            Vec<V> r, a, sl;
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                r.x[j] = canon0(t_arr ? __ldg(t_arr + lane * V + j) : t_scalar);
-            stv_g<V>(rat + o, r);
-            a = ldv_cg<V>(at + o);
-#pragma unroll
-            for (int j = 0; j < V; ++j) {
-                sl.x[j] = __fsub_rn(r.x[j], a.x[j]);
-                mn[j] = fminf(mn[j], sl.x[j]);
-            }
-            if (slack) stv_g<V>(slack + o, sl);
-        }
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-            if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + lane * V + j, f2ord(mn[j]));
-    }
-    __syncthreads();
-    for (int s = threadIdx.x; s < S; s += blockDim.x)
-        if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
 }
 
 __global__ void k_fill_i32(int32_t *p, int32_t v, int64_t count) {
@@ -881,266 +567,205 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
         if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
 }
 
-// ---- piece schedule (per direction; cached per (P, weights, split)) -----------
+// ---- task schedule (per direction; cached per (tw, split, pe)) -------------------
 // Rows of a level are in ascending degree, so the split rows (degree > split) form
-// the tail [le_normal, le) of every level.  Normal rows get weight degree + 1 and
-// are cut into weight-balanced pieces; a split row becomes ceil(deg/split) part
-// pieces of <= split edges each.
-// weight of a row: 2 per edge (delay + gather) + rw for the row itself (forward:
-// the at store; backward: rat store + at read for the slack)
-__global__ void k_piece_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                             int32_t psize, int32_t rw, int32_t *__restrict__ w,
-                             int32_t *__restrict__ parts) {
+// the tail [lo, le) of every level.  A normal row weighs degree + 1; normal task j
+// of a level holds the rows whose weight prefix (from the level start) lies in
+// [j*tw, (j+1)*tw), so it has <= tw rows and <= tw + split - rows edges.  A split
+// row becomes ceil(degree / pe) part tasks of <= pe edges.
+__global__ void k_tb_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
+                          int32_t pe, int32_t *__restrict__ w, int32_t *__restrict__ parts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int d = row_ptr[i + 1] - row_ptr[i];
-        w[i] = d > split ? 0 : 2 * d + rw;
-        parts[i] = d > split ? (d + psize - 1) / psize : 0;
+        w[i] = d > split ? 0 : d + 1;
+        parts[i] = d > split ? (d + pe - 1) / pe : 0;
     }
 }
-__global__ void k_piece_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
-                              const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
-                              int32_t L, int32_t P, int32_t ecap, int32_t ncap, int32_t wt_min,
-                              int32_t split, int32_t rw, int32_t skip0, int32_t *__restrict__ np,
-                              int32_t *__restrict__ npn, int32_t *__restrict__ lsnorm,
-                              int32_t *__restrict__ lenorm) {
+__global__ void k_tb_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
+                           const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
+                           int32_t L, int32_t split, int32_t tw, int32_t fwd,
+                           int32_t *__restrict__ nt, int32_t *__restrict__ ntn,
+                           int32_t *__restrict__ lonorm) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
-        int ls = level_ptr[k];
-        const int le = level_ptr[k + 1];
-        if (skip0) {   // degree-0 rows (backward sinks) are done by k_bwd_sinks
-            int a = ls, z = le;
-            while (a < z) {
-                const int mid = (a + z) >> 1;
-                if (row_ptr[mid + 1] - row_ptr[mid] > 0) z = mid;
-                else a = mid + 1;
-            }
-            ls = a;
-        }
+        const int ls = level_ptr[k], le = level_ptr[k + 1];
         int lo = ls, hi = le;   // first row with degree > split
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
             else lo = mid + 1;
         }
-        const int64_t wk = int64_t(W[lo]) - W[ls];   // 2*edges + rw*rows, normal rows
-        const int64_t nk = lo - ls;
-        const int64_t ek = (wk - rw * nk) / 2;
-        const int parts = Q[le] - Q[ls];
-        int64_t c = 0;
-        if (nk > 0) {
-            // enough pieces to fit a ring slot (3/4 of its edge and row capacity), else
-            // one per CTA left after the part pieces, so a level is a single round
-            const int64_t need = std::max<int64_t>((ek * 4 + 3 * ecap - 1) / (3 * ecap),
-                                                   (nk * 4 + 3 * ncap - 1) / (3 * ncap));
-            c = std::max<int64_t>(need, std::min<int64_t>(std::max(1, P - parts),
-                                                          (wk + wt_min - 1) / wt_min));
-            c = std::max<int64_t>(1, std::min<int64_t>(nk, c));
-        }
-        if (c + parts == 0) c = 1;   // keep one (empty) piece: levels publish in order
-        npn[k] = int(c);
-        lsnorm[k] = ls;
-        lenorm[k] = lo;
-        np[k] = int(c) + parts;
+        const int64_t wk = int64_t(W[lo]) - W[ls];
+        const int c = int((wk + tw - 1) / tw);
+        ntn[k] = c;
+        lonorm[k] = lo;
+        nt[fwd ? k : L - 1 - k] = c + (Q[le] - Q[ls]);
     }
 }
-// normal piece j of level k starts at the first row whose weight prefix reaches j*W_k/np_k
-__global__ void k_piece_fill(const int32_t *__restrict__ lsnorm, const int32_t *__restrict__ W,
-                             const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ off,
-                             const int32_t *__restrict__ npn, const int32_t *__restrict__ lenorm,
-                             int32_t L, int4 *__restrict__ pieces) {
+__global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
+                          const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ doff,
+                          const int32_t *__restrict__ ntn, const int32_t *__restrict__ lonorm,
+                          int32_t L, int32_t tw, int32_t fwd, int4 *__restrict__ desc) {
     for (int k = blockIdx.x; k < L; k += gridDim.x) {
-        const int ls = lsnorm[k], le = lenorm[k];
-        const int np = npn[k];
-        const int64_t w0 = W[ls], wk = int64_t(W[le]) - w0;
+        const int ls = level_ptr[k], lo = lonorm[k];
+        const int nn = ntn[k];
+        const int64_t w0 = W[ls];
+        const int base = doff[fwd ? k : L - 1 - k];
         auto start_of = [&](int jj) {
-            if (jj >= np) return le;
+            if (jj >= nn) return lo;
             if (jj == 0) return ls;
-            const int64_t target = w0 + wk * jj / np;
-            int lo = ls, hi = le;   // first i in [ls, le] with W[i] >= target
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (W[mid] >= target) hi = mid;
-                else lo = mid + 1;
+            const int64_t target = w0 + int64_t(jj) * tw;
+            int a = ls, z = lo;   // first i in [ls, lo] with W[i] >= target
+            while (a < z) {
+                const int mid = (a + z) >> 1;
+                if (W[mid] >= target) z = mid;
+                else a = mid + 1;
             }
-            return lo;
+            return a;
         };
-        for (int j = threadIdx.x; j < np; j += blockDim.x) {
+        for (int j = threadIdx.x; j < nn; j += blockDim.x) {
             const int a = start_of(j), z = start_of(j + 1);
-            pieces[off[k] + j] = make_int4(a, z, row_ptr[a], row_ptr[z]);
+            desc[base + j] = make_int4(a, z, row_ptr[a], row_ptr[z]);
         }
     }
 }
-__global__ void k_piece_parts(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
-                              const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
-                              const int32_t *__restrict__ Q, const int32_t *__restrict__ off,
-                              const int32_t *__restrict__ npn, int32_t n, int32_t split,
-                              int32_t psize, int4 *__restrict__ pieces) {
+__global__ void k_tb_parts(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                           const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
+                           const int32_t *__restrict__ Q, const int32_t *__restrict__ doff,
+                           const int32_t *__restrict__ ntn, int32_t n, int32_t L, int32_t split,
+                           int32_t pe, int32_t fwd, int4 *__restrict__ desc,
+                           int32_t *__restrict__ part_np) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int rb = row_ptr[i], re = row_ptr[i + 1];
         if (re - rb <= split) continue;
         const int k = level[node_of[i]];
-        const int base = off[k] + npn[k] + (Q[i] - Q[level_ptr[k]]);
-        for (int t = 0; rb + t * psize < re; ++t)
-            pieces[base + t] = make_int4(int(i), int(i) + 1, rb + t * psize,
-                                         min(re, rb + (t + 1) * psize));
+        const int base = doff[fwd ? k : L - 1 - k] + ntn[k] + (Q[i] - Q[level_ptr[k]]);
+        const int np = (re - rb + pe - 1) / pe;
+        part_np[Q[i]] = np;
+        for (int t = 0; t < np; ++t)
+            desc[base + t] = make_int4(int(i), -(Q[i] + t + 1), rb + t * pe, min(re, rb + (t + 1) * pe));
     }
 }
-// neighbour ids with split rows encoded as -(first part id + 1), and parts per row
 __global__ void k_pos_of(const int32_t *__restrict__ node_of, int32_t n, int32_t *__restrict__ pos) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
         pos[node_of[i]] = int(i);
 }
-__global__ void k_part_np(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ Q,
-                          int32_t n, int32_t split, int32_t psize, int32_t *__restrict__ part_np) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int d = row_ptr[i + 1] - row_ptr[i];
-        if (d > split) part_np[Q[i]] = (d + psize - 1) / psize;
-    }
-}
 __global__ void k_nbr_enc(const int32_t *__restrict__ nbr, int32_t m, const int32_t *__restrict__ pos,
                           const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ Q,
-                          int32_t split, int32_t psize, int32_t *__restrict__ enc) {
+                          int32_t split, int32_t *__restrict__ enc) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int v = nbr[e];
         const int i = pos[v];
-        const int d = row_ptr[i + 1] - row_ptr[i];
-        // only rows cut into >= 2 parts are read through their partials
-        enc[e] = (d > split && d > psize) ? -(Q[i] + 1) : v;
+        enc[e] = (row_ptr[i + 1] - row_ptr[i] > split) ? -(Q[i] + 1) : v;
     }
 }
+__global__ void k_split_list(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
+                             int32_t *__restrict__ rows, int32_t *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (row_ptr[i + 1] - row_ptr[i] > split) rows[atomicAdd(cnt, 1)] = int(i);
+}
+__global__ void k_tb_totals(const int32_t *__restrict__ doff, const int32_t *__restrict__ Q,
+                            int32_t L, int32_t n, int32_t *__restrict__ out) {
+    out[0] = doff[L];
+    out[1] = Q[n];
+}
+__global__ void k_tb_base(const int32_t *__restrict__ nt, int32_t L, int32_t nch,
+                          int32_t *__restrict__ x) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x)
+        x[k] = nt[k] * nch;
+}
 
-void build_pieces(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *nbr,
-                  int P, int ecap, int ncap, int wt_min, int split, int psize, int rw,
-                  int skip0, PieceSched &ps) {
+template <bool FWD>
+void build_tasks(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *nbr,
+                 int tw, int split, int pe, TaskSched &ts) {
     cudaStream_t s = g.stream;
-    const int32_t n = g.n, L = g.L;
-    DevBuf w, W, q, np, npn, lsnorm, lenorm;
-    DevBuf &Q = ps.q, &off = ps.off, &pieces = ps.pieces;
+    const int32_t n = g.n, L = g.L, m = g.m;
+    DevBuf w, W, pr, ntn, lonorm;
+    DevBuf &Q = ts.q;
     w.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     W.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    pr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     Q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    np.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    npn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    lenorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    lsnorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    off.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    ntn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    lonorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    ts.nt.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    ts.doff.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     HF_CUDA(cudaMemsetAsync(w.as<int32_t>() + n, 0, sizeof(int32_t), s));
-    HF_CUDA(cudaMemsetAsync(q.as<int32_t>() + n, 0, sizeof(int32_t), s));
-    HF_CUDA(cudaMemsetAsync(np.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_piece_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, psize, rw,
-                                                         w.as<int32_t>(), q.as<int32_t>());
+    HF_CUDA(cudaMemsetAsync(pr.as<int32_t>() + n, 0, sizeof(int32_t), s));
+    HF_CUDA(cudaMemsetAsync(ts.nt.as<int32_t>() + L, 0, sizeof(int32_t), s));
+    k_tb_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, pe, w.as<int32_t>(),
+                                                      pr.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(w.as<int32_t>(), W.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    scan_exclusive(q.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    k_piece_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, P, ecap, ncap,
-        wt_min, split, rw, skip0, np.as<int32_t>(), npn.as<int32_t>(), lsnorm.as<int32_t>(),
-        lenorm.as<int32_t>());
+    scan_exclusive(pr.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+    k_tb_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
+        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, split, tw,
+        FWD ? 1 : 0, ts.nt.as<int32_t>(), ntn.as<int32_t>(), lonorm.as<int32_t>());
     HF_CHECK_LAUNCH();
-    scan_exclusive(np.as<int32_t>(), off.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
-    int32_t total = 0;
-    HF_CUDA(cudaMemcpyAsync(&total, off.as<int32_t>() + L, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                            s));
-    HF_CUDA(cudaMemcpyAsync(&ps.nparts, Q.as<int32_t>() + n, sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, s));
+    scan_exclusive(ts.nt.as<int32_t>(), ts.doff.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
+    int32_t *tot = g.d_scalars() + 40;
+    k_tb_totals<<<1, 1, 0, s>>>(ts.doff.as<int32_t>(), Q.as<int32_t>(), L, n, tot);
+    HF_CHECK_LAUNCH();
+    int32_t h_tot[2] = {0, 0};
+    HF_CUDA(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, s));
     HF_CUDA(cudaStreamSynchronize(s));
-    pieces.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
-    k_piece_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
-        lsnorm.as<int32_t>(), W.as<int32_t>(), row_ptr, off.as<int32_t>(),
-        npn.as<int32_t>(), lenorm.as<int32_t>(), L, pieces.as<int4>());
+    const int32_t total = h_tot[0];
+    ts.nparts = h_tot[1];
+    ts.desc.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
+    ts.part_np.alloc(sizeof(int32_t) * size_t(std::max(ts.nparts, 1)), s);
+    k_tb_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
+        g.level_ptr.as<int32_t>(), W.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(),
+        ntn.as<int32_t>(), lonorm.as<int32_t>(), L, tw, FWD ? 1 : 0, ts.desc.as<int4>());
     HF_CHECK_LAUNCH();
-    k_piece_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-        row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q.as<int32_t>(),
-        off.as<int32_t>(), npn.as<int32_t>(), n, split, psize, pieces.as<int4>());
-    HF_CHECK_LAUNCH();
-    // neighbours that are split rows, and the part count of every split row
-    const int32_t m = g.m;
-    ps.nbr_enc.alloc(sizeof(int32_t) * size_t(m > 0 ? m : 1), s);
-    ps.part_np.alloc(sizeof(int32_t) * size_t(std::max(ps.nparts, 1)), s);
-    if (ps.nparts == 0) {
+    g.launches += 6;
+    ts.nbr_enc.alloc(sizeof(int32_t) * size_t(m > 0 ? m : 1), s);
+    if (ts.nparts == 0) {
         if (m)
-            HF_CUDA(cudaMemcpyAsync(ps.nbr_enc.p, nbr, sizeof(int32_t) * size_t(m),
+            HF_CUDA(cudaMemcpyAsync(ts.nbr_enc.p, nbr, sizeof(int32_t) * size_t(m),
                                     cudaMemcpyDeviceToDevice, s));
     } else {
+        k_tb_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q.as<int32_t>(),
+            ts.doff.as<int32_t>(), ntn.as<int32_t>(), n, L, split, pe, FWD ? 1 : 0,
+            ts.desc.as<int4>(), ts.part_np.as<int32_t>());
+        HF_CHECK_LAUNCH();
         DevBuf pos;
         pos.alloc(sizeof(int32_t) * size_t(n), s);
         k_pos_of<<<grid_for(n, 256, g.sms), 256, 0, s>>>(node_of, n, pos.as<int32_t>());
         HF_CHECK_LAUNCH();
-        k_part_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, Q.as<int32_t>(), n, split,
-                                                          psize, ps.part_np.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        ps.split_rows.alloc(sizeof(int32_t) * (size_t(ps.nparts) + 1), s);
-        HF_CUDA(cudaMemsetAsync(ps.split_rows.p, 0, sizeof(int32_t), s));
-        k_split_list<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            row_ptr, n, split, psize, ps.split_rows.as<int32_t>() + 1, ps.split_rows.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
         if (m) {
             k_nbr_enc<<<grid_for(m, 256, g.sms), 256, 0, s>>>(nbr, m, pos.as<int32_t>(), row_ptr,
-                                                              Q.as<int32_t>(), split, psize,
-                                                              ps.nbr_enc.as<int32_t>());
+                                                              Q.as<int32_t>(), split,
+                                                              ts.nbr_enc.as<int32_t>());
             HF_CHECK_LAUNCH();
         }
-        g.launches += 3;
-    }
-    g.launches += 5;
-}
-
-__global__ void k_gather_pieces(const int4 *__restrict__ pieces, const int32_t *__restrict__ idx,
-                                int32_t total, int4 *__restrict__ out) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-         i += int64_t(gridDim.x) * blockDim.x)
-        out[i] = pieces[idx[i]];
-}
-
-// Deal piece j of every level to CTA j mod P and lay each CTA's pieces out
-// contiguously in pass order, so a CTA walks its schedule with sequential loads.
-template <bool FWD> void deal_pieces(Graph &g, PieceSched &ps) {
-    cudaStream_t s = g.stream;
-    const int L = g.L, P = g.sms;
-    std::vector<int32_t> off(size_t(L) + 1);
-    HF_CUDA(cudaMemcpyAsync(off.data(), ps.off.p, sizeof(int32_t) * off.size(),
-                            cudaMemcpyDeviceToHost, s));
-    HF_CUDA(cudaStreamSynchronize(s));
-    const int32_t total = off[L];
-    std::vector<int32_t> cnt(size_t(P) + 1, 0), idx(size_t(std::max(total, 1))),
-        lv(size_t(std::max(total, 1)));
-    for (int k = 0; k < L; ++k)
-        for (int j = 0; j < off[k + 1] - off[k]; ++j) cnt[size_t(j % P) + 1]++;
-    for (int c = 0; c < P; ++c) cnt[c + 1] += cnt[c];
-    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
-    for (int kk = 0; kk < L; ++kk) {
-        const int k = FWD ? kk : L - 1 - kk;
-        for (int j = 0; j < off[k + 1] - off[k]; ++j) {
-            const int c = j % P;
-            idx[cur[c]] = off[k] + j;
-            lv[cur[c]] = k;
-            ++cur[c];
-        }
-    }
-    DevBuf d_idx;
-    d_idx.alloc(sizeof(int32_t) * idx.size(), s);
-    ps.cta_lv.alloc(sizeof(int32_t) * lv.size(), s);
-    ps.cta_off.alloc(sizeof(int32_t) * cnt.size(), s);
-    ps.cta_pc.alloc(sizeof(int4) * idx.size(), s);
-    HF_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), sizeof(int32_t) * idx.size(),
-                            cudaMemcpyHostToDevice, s));
-    HF_CUDA(cudaMemcpyAsync(ps.cta_lv.p, lv.data(), sizeof(int32_t) * lv.size(),
-                            cudaMemcpyHostToDevice, s));
-    HF_CUDA(cudaMemcpyAsync(ps.cta_off.p, cnt.data(), sizeof(int32_t) * cnt.size(),
-                            cudaMemcpyHostToDevice, s));
-    if (total > 0) {
-        k_gather_pieces<<<grid_for(total, 256, g.sms), 256, 0, s>>>(
-            ps.pieces.as<int4>(), d_idx.as<int32_t>(), total, ps.cta_pc.as<int4>());
+        ts.split_rows.alloc(sizeof(int32_t) * (size_t(n) + 1), s);
+        HF_CUDA(cudaMemsetAsync(ts.split_rows.p, 0, sizeof(int32_t), s));
+        k_split_list<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+            row_ptr, n, split, ts.split_rows.as<int32_t>() + 1, ts.split_rows.as<int32_t>());
         HF_CHECK_LAUNCH();
-        g.launches += 1;
+        g.launches += 4;
     }
-    HF_CUDA(cudaStreamSynchronize(s));   // host vectors go out of scope
+    ts.tb_nch = -1;
+}
+
+void task_bases(Graph &g, TaskSched &ts, int nch) {
+    if (ts.tb_nch == nch) return;
+    cudaStream_t s = g.stream;
+    const int32_t L = g.L;
+    DevBuf x;
+    x.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    ts.tb.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    HF_CUDA(cudaMemsetAsync(x.as<int32_t>() + L, 0, sizeof(int32_t), s));
+    k_tb_base<<<grid_for(L, 256, g.sms), 256, 0, s>>>(ts.nt.as<int32_t>(), L, nch, x.as<int32_t>());
+    HF_CHECK_LAUNCH();
+    scan_exclusive(x.as<int32_t>(), ts.tb.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
+    g.launches += 1;
+    ts.tb_nch = nch;
 }
 
 int pick_vec(int32_t S, std::initializer_list<const void *> ptrs) {
@@ -1158,113 +783,133 @@ void prof_record(Graph &g, int idx) {
     if (g.prof) HF_CUDA(cudaEventRecord(g.ev[idx], g.stream));
 }
 
-template <int V, bool FWD, bool CHECK_D, bool VEC16>
-void launch(Graph &g, PassParams &p, size_t smem) {
-    auto kern = k_propagate<V, FWD, CHECK_D, VEC16>;
+int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <int V, int LPN, bool FWD, bool CHECK_D, int RB>
+void launch_flow(Graph &g, FlowParams &p) {
+    auto kern = k_flow<V, LPN, FWD, CHECK_D, RB>;
+    constexpr int SC = V * LPN;
+    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD);
+    const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
     HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem));
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
+    const int cap = env_int("HF_CTAS_PER_SM", 0);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
     void *args[] = {&p};
-    // one CTA per SM; the piece schedule was built for exactly g.sms CTAs.  With
-    // profiling on, events bracket exactly this launch (forward: ev 2/3, backward 5/4).
+    // all warps co-resident (cooperative launch): required by the dataflow wait.
+    // With profiling on, events bracket exactly this launch (forward: ev 2/3,
+    // backward 5/4).
     prof_record(g, FWD ? 2 : 5);
-    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, BLOCK, args, smem, g.stream));
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms * per_sm, FLOW_THREADS, args,
+                                        smem, g.stream));
     prof_record(g, FWD ? 3 : 4);
     g.launches += 1;
 }
 
-constexpr int SMEM_BUDGET = 200 * 1024;
-
-inline float __int_as_float_host(uint32_t b) {
-    float f;
-    memcpy(&f, &b, 4);
-    return f;
+template <bool FWD, bool CHECK_D, int RB> void dispatch_rb(Graph &g, FlowParams &p, int LPN) {
+    switch (LPN) {
+    case 16: launch_flow<4, 16, FWD, CHECK_D, RB>(g, p); break;
+    case 8: launch_flow<4, 8, FWD, CHECK_D, RB>(g, p); break;
+    case 4: launch_flow<4, 4, FWD, CHECK_D, RB>(g, p); break;
+    case 2: launch_flow<4, 2, FWD, CHECK_D, RB>(g, p); break;
+    default: launch_flow<4, 1, FWD, CHECK_D, RB>(g, p); break;
+    }
+}
+template <bool FWD, bool CHECK_D> void dispatch(Graph &g, FlowParams &p, int V, int LPN) {
+    if (V == 4) {
+        if (env_int("HF_RB", 4) == 8) dispatch_rb<FWD, CHECK_D, 8>(g, p, LPN);
+        else dispatch_rb<FWD, CHECK_D, 4>(g, p, LPN);
+    } else if (V == 2) {
+        launch_flow<2, 1, FWD, CHECK_D, 8>(g, p);
+    } else {
+        launch_flow<1, 1, FWD, CHECK_D, 8>(g, p);
+    }
 }
 
-template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) {
-    if (p.S / V > NC) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass (S/V > 512)");
-    // staging capacity per ring slot: ecap edges of S floats (+ id), ncap rows
-    const int fixed = 2 * NBUF * 8 + NC * 4 * 4 + 2 * p.S * 4;
-    const int per_slot = (SMEM_BUDGET - fixed) / NBUF - 2 * MAXMED * 4 - 256;
-    if (per_slot < 2048) fail(HF_ERR_INVALID_ARG, "too many scenarios for one pass");
-    int ecap = std::min(std::min(4096, CH * MAXMED),
-                        std::max(8, (per_slot - 256 * 8) / (4 + 4 * p.S)));
-    int ncap = std::min(2048, std::max(16, (per_slot - ecap * (4 + 4 * p.S)) / 8 - 2));
-    p.ecap = ecap;
-    p.ncap = ncap;
-    const int wt_min = 32;
-    const int split = std::max(32, ecap / 4);
-    p.split = split;
-    p.psize = ecap;
-    PieceSched &ps = FWD ? g.ps_f : g.ps_b;
-    const int32_t want = (ecap * 4096 + ncap) * 8 + (g.sms & 7);
-    if (ps.key != want || !ps.pieces.p) {
-        build_pieces(g, p.row_ptr, p.node_of, p.nbr, g.sms, ecap, ncap, wt_min, split, ecap,
-                     FWD ? 1 : 2, FWD ? 0 : 1, ps);
-        deal_pieces<FWD>(g, ps);
-        ps.key = want;
+// one pass: task schedule, sentinel fill, the dataflow kernel, split-row finalise
+template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) {
+    cudaStream_t s = g.stream;
+    // scenario chunk: SC = V * LPN columns (largest power of two <= HF_SC dividing S)
+    const int sc_max = std::max(1, env_int("HF_SC", 64));
+    int LPN = 1;
+    if (V == 4)
+        while (LPN < 16 && p.S % (V * LPN * 2) == 0 && V * LPN * 2 <= sc_max) LPN *= 2;
+    const int SC = V * LPN, G = 32 / LPN;
+    p.nch = p.S / SC;
+    // task shape: weight tw (rows + edges) per task, rows longer than split edges cut
+    // into parts of pe edges; scratch capacity ecap = tw + split edges, ncap = tw rows
+    const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
+    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 8 : 16));
+    int split = env_int("HF_SPLIT", slots == 2 ? 16 : (G <= 2 ? 8 : 16));
+    tw = std::max(2, std::min(tw, 32 * slots - 1));
+    split = std::max(1, std::min(split, 32 * slots - tw));
+    const int pe = tw + split;
+    p.ecap = tw + split;
+    p.ncap = tw;
+    p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
+    p.poll_all = env_int("HF_POLL_ALL", 1);
+    TaskSched &ts = FWD ? g.ts_f : g.ts_b;
+    const int64_t want = (int64_t(tw) << 20) | (int64_t(split) << 8) | 1;
+    if (ts.key != want || !ts.desc.p) {
+        build_tasks<FWD>(g, p.row_ptr, p.node_of, p.nbr, tw, split, pe, ts);
+        ts.key = want;
     }
-    p.cta_pc = ps.cta_pc.as<int4>();
-    p.cta_lv = ps.cta_lv.as<int32_t>();
-    p.cta_off = ps.cta_off.as<int32_t>();
-    p.piece_off = ps.off.as<int32_t>();
-    p.q = ps.q.as<int32_t>();
-    p.nbr = ps.nbr_enc.as<int32_t>();   // split-row neighbours encoded
-    p.part_np = ps.part_np.as<int32_t>();
-    DevBuf part_buf;
-    if (ps.nparts > 0) {
-        part_buf.alloc(sizeof(float) * size_t(ps.nparts) * p.S, g.stream);
-        p.part_buf = part_buf.as<float>();
-    }
+    task_bases(g, ts, p.nch);
+    p.desc = ts.desc.as<int4>();
+    p.nt = ts.nt.as<int32_t>();
+    p.doff = ts.doff.as<int32_t>();
+    p.tb = ts.tb.as<int32_t>();
+    p.nbr = ts.nbr_enc.as<int32_t>();
+    p.part_np = ts.part_np.as<int32_t>();
     p.L = g.L;
-    const SlotLayout SL = slot_layout(ncap, ecap, p.S);
-    const size_t smem = size_t(NBUF) * SL.bytes + size_t(fixed);
-    g.ws_sync.alloc(sizeof(int32_t) * (size_t(g.L) + 1), g.stream);   // warps published per level
-    HF_CUDA(cudaMemsetAsync(g.ws_sync.p, 0, sizeof(int32_t) * (size_t(g.L) + 1), g.stream));
-    p.done = g.ws_sync.as<int32_t>();
     p.err = g.d_err();
-    // TMA bulk copies need 16-byte rows and 16-byte aligned sources
-    const bool vec16 = (p.S % 4 == 0) && (reinterpret_cast<uintptr_t>(p.d) % 16 == 0);
-    // debugging timeline: HF_TRACE=<file prefix> dumps one record per piece
+    DevBuf part_buf;
+    if (ts.nparts > 0) {
+        part_buf.alloc(sizeof(float) * size_t(ts.nparts) * p.S, s);
+        p.part_buf = part_buf.as<float>();
+        HF_CUDA(cudaMemsetAsync(part_buf.p, 0xff, part_buf.bytes, s));
+    }
+    // the NaN sentinel (all-ones bit pattern): "not yet computed"
+    HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
+    // debugging timeline: HF_TRACE=<file prefix> dumps one record per task
     const char *trace_env = getenv("HF_TRACE");
     DevBuf tbuf;
-    const int tcap = 1 << 20;
+    int32_t ntask = 0;
     if (trace_env) {
-        tbuf.alloc(sizeof(unsigned long long) * 8 * tcap + 16, g.stream);
-        HF_CUDA(cudaMemsetAsync(tbuf.p, 0, 16, g.stream));
-        p.trace_n = reinterpret_cast<int32_t *>(tbuf.as<unsigned char>());
-        p.trace = reinterpret_cast<unsigned long long *>(tbuf.as<unsigned char>() + 16);
-        p.trace_cap = tcap;
+        HF_CUDA(cudaMemcpyAsync(&ntask, p.tb + g.L, 4, cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
+        tbuf.alloc(sizeof(unsigned long long) * 4 * size_t(std::max(ntask, 1)), s);
+        HF_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, s));
+        p.trace = tbuf.as<unsigned long long>();
+        p.trace_cap = ntask;
     }
-#define HF_LAUNCH(VV)                                                            \
-    do {                                                                         \
-        if (check_d && vec16) launch<VV, FWD, true, true>(g, p, smem);           \
-        else if (check_d) launch<VV, FWD, true, false>(g, p, smem);              \
-        else if (vec16) launch<VV, FWD, false, true>(g, p, smem);                \
-        else launch<VV, FWD, false, false>(g, p, smem);                          \
-    } while (0)
-    if (V == 4) HF_LAUNCH(4);
-    else if (V == 2) HF_LAUNCH(2);
-    else HF_LAUNCH(1);
-#undef HF_LAUNCH
-    if (ps.nparts > 0) {
-        k_finalize_split<FWD><<<g.sms, 256, 0, g.stream>>>(
-            ps.split_rows.as<int32_t>() + 1, ps.split_rows.as<int32_t>(), p.row_ptr, p.node_of,
-            p.q, p.psize, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+    if (check_d) dispatch<FWD, true>(g, p, V, LPN);
+    else dispatch<FWD, false>(g, p, V, LPN);
+    if (ts.nparts > 0) {
+        k_finalize_split<FWD><<<g.sms, 256, 0, s>>>(
+            ts.split_rows.as<int32_t>() + 1, ts.split_rows.as<int32_t>(), p.row_ptr, p.node_of,
+            ts.q.as<int32_t>(), pe, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
     if (trace_env) {
-        int32_t cnt = 0;
-        HF_CUDA(cudaMemcpyAsync(&cnt, p.trace_n, 4, cudaMemcpyDeviceToHost, g.stream));
-        HF_CUDA(cudaStreamSynchronize(g.stream));
-        cnt = std::min(cnt, tcap);
-        std::vector<unsigned long long> h(size_t(cnt) * 8);
-        HF_CUDA(cudaMemcpy(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+        // per task: {warp, t_start, t_ready (first gathers complete), t_done} + level
+        std::vector<unsigned long long> h(size_t(ntask) * 4);
+        std::vector<int32_t> tb(size_t(g.L) + 1);
+        HF_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaMemcpyAsync(tb.data(), p.tb, tb.size() * 4, cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
         std::string fn = std::string(trace_env) + (FWD ? "_fwd_S" : "_bwd_S") + std::to_string(p.S) +
                          ".bin";
         if (FILE *f = fopen(fn.c_str(), "wb")) {
+            const int32_t hdr[4] = {ntask, g.L, p.S, int32_t(SC)};
+            fwrite(hdr, 4, 4, f);
+            fwrite(tb.data(), 4, tb.size(), f);
             fwrite(h.data(), 8, h.size(), f);
             fclose(f);
         }
@@ -1277,7 +922,7 @@ template <bool FWD> void run_pass(Graph &g, PassParams &p, bool check_d, int V) 
 void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                     float *at) {
     if (g.n == 0) return;
-    PassParams p{};
+    FlowParams p{};
     const int V = pick_vec(S, {d, at});
     p.row_ptr = g.lo_in_ptr.as<int32_t>();
     p.nbr = g.lo_in_src.as<int32_t>();
@@ -1305,7 +950,7 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         g.launches += 1;
     }
     if (g.n > 0) {
-        PassParams p{};
+        FlowParams p{};
         const int V = pick_vec(S, {d, at, rat, slack});
         p.row_ptr = g.lo_out_ptr.as<int32_t>();
         p.nbr = g.lo_out_dst.as<int32_t>();
@@ -1319,22 +964,6 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         p.out = rat;
         p.slack = slack;
         p.wns_ord = ord;
-        // sinks first (independent of every level); the pass skips them
-        const int lpn = S / V;
-        const int grid = grid_for(int64_t(g.n) * lpn, 512, g.sms);
-        const size_t sm = sizeof(int32_t) * size_t(S);
-        if (sm > 48 * 1024) fail(HF_ERR_INVALID_ARG, "too many scenarios");
-        if (V == 4)
-            k_bwd_sinks<4><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
-                                                 at, rat, slack, ord);
-        else if (V == 2)
-            k_bwd_sinks<2><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
-                                                 at, rat, slack, ord);
-        else
-            k_bwd_sinks<1><<<grid, 512, sm, s>>>(g.out_ptr.as<int32_t>(), g.n, S, t_arr, t_scalar,
-                                                 at, rat, slack, ord);
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
         run_pass<false>(g, p, false, V);
     }
     if (wns_f) {

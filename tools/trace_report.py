@@ -1,8 +1,13 @@
-"""Analyse an HF_TRACE dump: per-level critical path composition.
+"""Analyse an HF_TRACE dump of the dataflow propagation kernel.
 
-record = {level, cta, t_top, t_ready, t_computed, t_published, edges, rows} (ns)
-For the LAST-published piece of every level: wait = ready - previous level done,
-split into 'own' (its CTA still busy: staging / previous piece) and 'wake'.
+File: int32 header {ntask, L, S, SC}, int32 tb[L+1] (first task of pass-level q),
+then per task uint64 {warp, t_start, t_ready, t_done} (globaltimer ns;
+t_ready = first gather batch complete, i.e. its inputs were final).
+
+Per pass-level q: done_q = last t_done of the level.  For the task that finishes
+last, split its time after done_{q-1} into: late start (its warp was still busy
+with an earlier task), wait (inputs not yet visible / gather latency) and
+compute+store (ready -> done).
 """
 import sys
 
@@ -10,41 +15,49 @@ import numpy as np
 
 
 def main(fn):
-    a = np.fromfile(fn, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
-    lv, cta, ttop, trdy, tcmp, tpub, E, nn = a.T
-    fwd = "_fwd" in fn
-    levels = np.unique(lv)
-    order = levels if fwd else levels[::-1]
-    done = {k: tpub[lv == k].max() for k in order}
-    # previous piece end per CTA
-    idx = np.lexsort((ttop, cta))
-    prev_end = np.full(len(a), -1, np.int64)
-    for i0, i1 in zip(idx[:-1], idx[1:]):
-        if cta[i0] == cta[i1]:
-            prev_end[i1] = tpub[i0]
-    rec = []
-    prev = None
-    for k in order:
-        sel = np.nonzero(lv == k)[0]
-        last = sel[np.argmax(tpub[sel])]
-        if prev is not None:
-            d0 = done[prev]
-            rec.append((done[k] - d0, trdy[last] - d0, ttop[last] - d0, tcmp[last] - trdy[last],
-                        tpub[last] - tcmp[last], E[last], nn[last], len(sel)))
-        prev = k
-    r = np.array(rec, dtype=np.float64)
-    span = max(done.values()) - ttop.min()
-    print(f"{fn.split('/')[-1]}: {len(a)} pieces, {len(levels)} levels, {span / 1e3:.0f} us, "
-          f"{span / 1e3 / len(levels):.2f} us/level")
-    names = ["gap", "ready-prevdone", "top-prevdone", "compute", "publish"]
-    for i, nm in enumerate(names):
-        print(f"   last piece {nm:15s} median {np.median(r[:, i]) / 1e3:6.2f} us  "
-              f"p90 {np.percentile(r[:, i], 90) / 1e3:6.2f}")
-    print(f"   last piece edges median {np.median(r[:, 5]):.0f} max {r[:, 5].max():.0f}; "
-          f"all pieces edges median {np.median(E):.0f} max {E.max()}; pieces/level {np.median(r[:, 7]):.0f}")
-    dc = tcmp - trdy
-    print(f"   compute all pieces median {np.median(dc) / 1e3:.2f} us p90 {np.percentile(dc, 90) / 1e3:.2f} "
-          f"max {dc.max() / 1e3:.2f}; heavy (E>ecap?) count {(E > np.median(E) * 1.8).sum()}")
+    raw = np.fromfile(fn, dtype=np.int32)
+    ntask, L, S, SC = (int(x) for x in raw[:4])
+    tb = raw[4:4 + L + 1].astype(np.int64)
+    off = (4 + L + 1) * 4
+    a = np.frombuffer(open(fn, "rb").read()[off:], dtype=np.uint64).reshape(-1, 4).astype(np.int64)
+    a = a[:ntask]
+    w, ts, tr, td = a.T
+    ok = td > 0
+    t0 = ts[ok].min()
+    span = td[ok].max() - t0
+    lvl = np.searchsorted(tb, np.arange(ntask), side="right") - 1
+    done = np.zeros(L, np.int64)
+    for q in range(L):
+        sel = np.arange(tb[q], tb[q + 1])
+        sel = sel[ok[sel]]
+        done[q] = td[sel].max() if len(sel) else (done[q - 1] if q else t0)
+    gaps = np.diff(np.concatenate([[t0], done]))
+    late, wait, comp = [], [], []
+    for q in range(1, L):
+        sel = np.arange(tb[q], tb[q + 1])
+        if len(sel) == 0:
+            continue
+        i = sel[np.argmax(td[sel])]
+        base = done[q - 1]
+        late.append(max(0, ts[i] - base))
+        wait.append(tr[i] - max(ts[i], base))
+        comp.append(td[i] - tr[i])
+    dur = td - ts
+    print(f"{fn}: {ntask} tasks, {L} levels, S={S} SC={SC}, {span / 1e3:.1f} us, "
+          f"{span / 1e3 / L:.2f} us/level")
+    print(f"   level gap        median {np.median(gaps) / 1e3:6.2f} us  p90 {np.percentile(gaps, 90) / 1e3:6.2f}")
+    for nm, v in (("last task late start", late), ("last task wait", wait),
+                  ("last task compute+store", comp)):
+        v = np.array(v) / 1e3
+        print(f"   {nm:24s} median {np.median(v):6.2f} us  p90 {np.percentile(v, 90):6.2f}")
+    print(f"   all tasks: start->ready median {np.median(tr - ts) / 1e3:.2f} us, "
+          f"ready->done median {np.median(td - tr) / 1e3:.2f} us, duration p90 "
+          f"{np.percentile(dur, 90) / 1e3:.2f} us; warps {len(np.unique(w))}")
+    # how far ahead of the front do warps start their tasks?
+    q_of = lvl
+    ahead = ts - np.where(q_of > 0, done[np.maximum(q_of - 1, 0)], t0)
+    print(f"   task start - pred level done: median {np.median(ahead) / 1e3:.2f} us "
+          f"(negative = started before its inputs were complete)")
 
 
 if __name__ == "__main__":
