@@ -182,12 +182,13 @@ struct FlowParams {
 
 // per-warp shared-memory scratch (bytes), identical on host and device
 struct WarpLayout {
-    int d, at, nbr, eid, rp, node, bytes;
+    int d, a, at, nbr, eid, rp, node, bytes;
 };
-__host__ __device__ inline WarpLayout warp_layout(int ecap, int ncap, int SC, bool fwd) {
+__host__ __device__ inline WarpLayout warp_layout(int ecap, int ncap, int SC, bool fwd, bool ga) {
     WarpLayout L;
     int o = 0;
     L.d = o;    o += ecap * SC * 4;
+    L.a = o;    o += ga ? ecap * SC * 4 : 0;
     L.at = o;   o += fwd ? 0 : ncap * SC * 4;
     L.nbr = o;  o += ecap * 4;
     L.eid = o;  o += ecap * 4;
@@ -208,20 +209,23 @@ template <int NSL> struct Idx {
 };
 template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 
-template <int V, int LPN, bool FWD, bool CHECK_D, int RB>
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA>
 __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
     constexpr int SC = V * LPN;   // columns per chunk
     constexpr int G = 32 / LPN;   // lane groups per warp
     constexpr int NSL = idx_slots<LPN>();
-    // RB: gathers in flight per lane per batch
+    // GA: gathers land in shared memory by cp.async (16-byte pieces, V == 4);
+    // else in registers, RB per lane per batch
+    constexpr int RB = V == 4 ? 4 : 8;
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane / LPN, gl = lane % LPN;
     const int S = p.S;
-    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD);
+    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     int32_t *s_wmin = reinterpret_cast<int32_t *>(smem);
     unsigned char *wb = smem + wmin_bytes(S) + wib * WL.bytes;
     float *s_d = reinterpret_cast<float *>(wb + WL.d);
+    float *s_a = reinterpret_cast<float *>(wb + WL.a);
     float *s_at = reinterpret_cast<float *>(wb + WL.at);
     int32_t *s_nbr = reinterpret_cast<int32_t *>(wb + WL.nbr);
     int32_t *s_eid = reinterpret_cast<int32_t *>(wb + WL.eid);
@@ -347,7 +351,73 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         }
         // ---- (3) edge-parallel gathers: x = fl(a[u] +/- d), sentinel-polled ----
         unsigned long long tr1 = 0;
-        for (int k0 = 0; k0 < E; k0 += G * RB) {
+        if constexpr (GA) {
+            // every gathered row piece lands in s_a by cp.async (all edges in flight at
+            // once); pieces still holding the sentinel are re-fetched after a back-off
+            for (int k = g; k < E; k += G) {
+                const int u = s_nbr[k];
+                if (u >= 0) cp_async_v<V>(s_a + k * SC + gl * V, p.out + int64_t(u) * S + col);
+            }
+            cp_async_commit();
+            for (int k = g; k < E; k += G) {   // neighbours cut into parts (rare)
+                const int u = s_nbr[k];
+                if (u < 0) {
+                    const int q0 = -u - 1;
+                    const int np = __ldg(p.part_np + q0);
+                    Vec<V> acc;
+#pragma unroll
+                    for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+                    for (int kk = 0; kk < np; ++kk) {
+                        const float *src = p.part_buf + int64_t(q0 + kk) * S + col;
+                        Vec<V> v = ld_relaxed<V>(src);
+                        int ns = 32;
+                        while (has_nan<V>(v)) {
+                            __nanosleep(ns);
+                            ns = min(ns * 2, p.sleep_max);
+                            v = ld_relaxed<V>(src);
+                        }
+#pragma unroll
+                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], v.x[j]);
+                    }
+                    st_s<V>(s_a + k * SC + gl * V, acc);
+                }
+            }
+            cp_async_wait();
+            int ns = 32;
+            for (;;) {
+                bool miss = false;
+                for (int k = g; k < E; k += G)
+                    if (s_nbr[k] >= 0) miss |= has_nan<V>(ld_s<V>(s_a + k * SC + gl * V));
+                if (!__ballot_sync(FULL, miss)) break;
+                __nanosleep(ns);
+                ns = min(ns * 2, p.sleep_max);
+                for (int k = g; k < E; k += G) {
+                    const int u = s_nbr[k];
+                    if (u >= 0 && has_nan<V>(ld_s<V>(s_a + k * SC + gl * V)))
+                        cp_async_v<V>(s_a + k * SC + gl * V, p.out + int64_t(u) * S + col);
+                }
+                cp_async_commit();
+                cp_async_wait();
+            }
+            if (p.trace) tr1 = gtimer();
+            for (int k = g; k < E; k += G) {
+                float *dp = s_d + k * SC + gl * V;
+                const Vec<V> dv = ld_s<V>(dp);
+                const Vec<V> av = ld_s<V>(s_a + k * SC + gl * V);
+                Vec<V> x;
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    float d1 = dv.x[j];
+                    if (CHECK_D) {
+                        bad |= !isfinite(d1);
+                        d1 = canon0(d1);
+                    }
+                    x.x[j] = relax<FWD>(av.x[j], d1);
+                }
+                st_s<V>(dp, x);
+            }
+        }
+        for (int k0 = 0; !GA && k0 < E; k0 += G * RB) {
             Vec<V> a[RB];
             int uu[RB];
 #pragma unroll
@@ -788,11 +858,11 @@ int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int V, int LPN, bool FWD, bool CHECK_D, int RB>
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA>
 void launch_flow(Graph &g, FlowParams &p) {
-    auto kern = k_flow<V, LPN, FWD, CHECK_D, RB>;
+    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA>;
     constexpr int SC = V * LPN;
-    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD);
+    const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
     HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     int per_sm = 0;
@@ -811,23 +881,23 @@ void launch_flow(Graph &g, FlowParams &p) {
     g.launches += 1;
 }
 
-template <bool FWD, bool CHECK_D, int RB> void dispatch_rb(Graph &g, FlowParams &p, int LPN) {
+template <bool FWD, bool CHECK_D, bool GA> void dispatch_ga(Graph &g, FlowParams &p, int LPN) {
     switch (LPN) {
-    case 16: launch_flow<4, 16, FWD, CHECK_D, RB>(g, p); break;
-    case 8: launch_flow<4, 8, FWD, CHECK_D, RB>(g, p); break;
-    case 4: launch_flow<4, 4, FWD, CHECK_D, RB>(g, p); break;
-    case 2: launch_flow<4, 2, FWD, CHECK_D, RB>(g, p); break;
-    default: launch_flow<4, 1, FWD, CHECK_D, RB>(g, p); break;
+    case 16: launch_flow<4, 16, FWD, CHECK_D, GA>(g, p); break;
+    case 8: launch_flow<4, 8, FWD, CHECK_D, GA>(g, p); break;
+    case 4: launch_flow<4, 4, FWD, CHECK_D, GA>(g, p); break;
+    case 2: launch_flow<4, 2, FWD, CHECK_D, GA>(g, p); break;
+    default: launch_flow<4, 1, FWD, CHECK_D, GA>(g, p); break;
     }
 }
 template <bool FWD, bool CHECK_D> void dispatch(Graph &g, FlowParams &p, int V, int LPN) {
     if (V == 4) {
-        if (env_int("HF_RB", 4) == 8) dispatch_rb<FWD, CHECK_D, 8>(g, p, LPN);
-        else dispatch_rb<FWD, CHECK_D, 4>(g, p, LPN);
+        if (env_int("HF_GA", 0)) dispatch_ga<FWD, CHECK_D, true>(g, p, LPN);
+        else dispatch_ga<FWD, CHECK_D, false>(g, p, LPN);
     } else if (V == 2) {
-        launch_flow<2, 1, FWD, CHECK_D, 8>(g, p);
+        launch_flow<2, 1, FWD, CHECK_D, false>(g, p);
     } else {
-        launch_flow<1, 1, FWD, CHECK_D, 8>(g, p);
+        launch_flow<1, 1, FWD, CHECK_D, false>(g, p);
     }
 }
 
@@ -844,7 +914,7 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     // task shape: weight tw (rows + edges) per task, rows longer than split edges cut
     // into parts of pe edges; scratch capacity ecap = tw + split edges, ncap = tw rows
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
-    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 8 : 16));
+    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 12 : 16));
     int split = env_int("HF_SPLIT", slots == 2 ? 16 : (G <= 2 ? 8 : 16));
     tw = std::max(2, std::min(tw, 32 * slots - 1));
     split = std::max(1, std::min(split, 32 * slots - tw));
