@@ -596,4 +596,18 @@ hf_status hf_profile_read(hf_graph h, float *ms_levelize, float *ms_forward, flo
     });
 }
 
+// Test hook (not part of include/hf.h): exclusive scan of n int32 device values
+// with the library's scan primitive, on the graph's stream.
+hf_status hf_debug_scan(hf_graph h, const int32_t *in_d, int32_t *out_d, int64_t n,
+                        int32_t *total_d) {
+    return guarded([&]() -> hf_status {
+        if (!h) fail(HF_ERR_INVALID_ARG, "graph is NULL");
+        Graph *g = G(h);
+        DeviceGuard dg(g->device);
+        scan_exclusive(in_d, out_d, n, total_d, g->stream, *g);
+        HF_CUDA(cudaStreamSynchronize(g->stream));
+        return HF_OK;
+    });
+}
+
 }  // extern "C"

@@ -87,6 +87,10 @@ struct TaskSched {
     int64_t key = -1;   // (tw, split, pe) the schedule was built for
 };
 
+// rows with more than LO_SPLIT edges sit at the end of their level in the
+// level-ordered CSRs and are cut into part tasks by the propagation passes
+constexpr int LO_SPLIT = 8;
+
 // ---- the graph -------------------------------------------------------------
 struct Graph {
     int device = 0;
@@ -104,14 +108,18 @@ struct Graph {
     int32_t max_level_width = 0;
     // level-ordered ("relabelled") CSR for the propagation passes: row i is node
     // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
-    // Within a level, rows are in ascending degree (per direction): node ids
-    // lo_in_node / lo_out_node.
+    // Within a level, rows of degree <= LO_SPLIT first, then the longer ones, each
+    // run in canonical order (per direction): node ids lo_in_node / lo_out_node.
     DevBuf lo_in_node, lo_in_ptr, lo_in_src, lo_in_eid;
     DevBuf lo_out_node, lo_out_ptr, lo_out_dst, lo_out_eid;
     // task schedules of the dataflow propagation kernels (per direction)
     TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
+    // single-pass scan state (primitives.cu): per-tile words + tile counter
+    DevBuf scan_state;
+    uint64_t scan_base = 0;
+    unsigned scan_epoch = 0;
     // small device scalars: [0] error bits, [1..] scratch
     DevBuf d_small;
     uint32_t *d_err() const { return d_small.as<uint32_t>(); }

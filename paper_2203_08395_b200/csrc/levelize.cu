@@ -275,27 +275,39 @@ __global__ void k_lev_cscatter(const int32_t *__restrict__ in_ptr,
     }
 }
 
-// Level-ordered CSR for the propagation passes.  Rows of one level are ordered
-// by ascending degree (ties by id), separately for fan-in and fan-out, so the
-// heavy rows of a level sit at its end (the piece builder splits them off).
-__global__ void k_deg_keys(const int32_t *__restrict__ level, const int32_t *__restrict__ in_ptr,
-                           const int32_t *__restrict__ out_ptr, int32_t n, int db,
-                           int32_t *__restrict__ kin, int32_t *__restrict__ kout) {
-    const int cap = (1 << db) - 1;
-    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n;
-         v += int64_t(gridDim.x) * blockDim.x) {
-        const int lv = level[v] << db;
-        kin[v] = lv | min(in_ptr[v + 1] - in_ptr[v], cap);
-        kout[v] = lv | min(out_ptr[v + 1] - out_ptr[v], cap);
+// Level-ordered CSR for the propagation passes: flag[i] = row order[i] is long
+// (degree > LO_SPLIT); flag[n] = 0 so the exclusive scan's last entry is the count.
+__global__ void k_lo_flags(const int32_t *__restrict__ order, const int32_t *__restrict__ ptr,
+                           int32_t n, int32_t *__restrict__ flag) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int f = 0;
+        if (i < n) {
+            const int v = order[i];
+            f = ptr[v + 1] - ptr[v] > LO_SPLIT;
+        }
+        flag[i] = f;
     }
 }
-
-__global__ void k_relabel_deg(const int32_t *__restrict__ order, const int32_t *__restrict__ ptr,
-                              int32_t n, int32_t *__restrict__ deg) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+// stable partition of every level run of `order`: short rows, then long rows
+__global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__restrict__ level,
+                           const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ fs,
+                           const int32_t *__restrict__ flag, const int32_t *__restrict__ ptr,
+                           int32_t n, int32_t *__restrict__ lo_node, int32_t *__restrict__ deg) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
          i += int64_t(gridDim.x) * blockDim.x) {
+        if (i == n) {
+            deg[n] = 0;
+            continue;
+        }
         const int v = order[i];
-        deg[i] = ptr[v + 1] - ptr[v];
+        const int k = level[v];
+        const int ls = level_ptr[k], le = level_ptr[k + 1];
+        const int sl = fs[i] - fs[ls];
+        const int nlong = fs[le] - fs[ls];
+        const int pos = flag[i] ? le - nlong + sl : ls + (int(i) - ls) - sl;
+        lo_node[pos] = v;
+        deg[pos] = ptr[v + 1] - ptr[v];
     }
 }
 
@@ -517,17 +529,10 @@ int64_t levelize_device(Graph &g) {
     int32_t w = 0;
     for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
     g.max_level_width = w;
-    // relabel (a4): level-ordered fan-in / fan-out CSR for the propagation passes,
-    // rows of a level in ascending degree
+    // relabel (a4): level-ordered fan-in / fan-out CSR for the propagation passes.
+    // Inside a level the rows with degree <= LO_SPLIT come first, then the longer
+    // rows (the task builder cuts those into parts); both runs keep canonical order.
     {
-        const int lb = bits_for(int64_t(L) - 1);
-        const int db = std::max(0, std::min(12, 31 - lb));
-        DevBuf kin, kout, din, dout, tmp;
-        kin.alloc(sizeof(int32_t) * n, s);
-        kout.alloc(sizeof(int32_t) * n, s);
-        tmp.alloc(sizeof(int32_t) * n, s);
-        din.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        dout.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         g.lo_in_node.alloc(sizeof(int32_t) * n, s);
         g.lo_out_node.alloc(sizeof(int32_t) * n, s);
         g.lo_in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
@@ -536,35 +541,35 @@ int64_t levelize_device(Graph &g) {
         g.lo_in_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
         g.lo_out_dst.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
         g.lo_out_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-        k_deg_keys<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            g.level.as<int32_t>(), g.in_ptr.as<int32_t>(), g.out_ptr.as<int32_t>(), n, db,
-            kin.as<int32_t>(), kout.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        radix_sort_pairs(kin.as<int32_t>(), nullptr, tmp.as<int32_t>(), g.lo_in_node.as<int32_t>(),
-                         n, lb + db, s, g);
-        radix_sort_pairs(kout.as<int32_t>(), nullptr, tmp.as<int32_t>(),
-                         g.lo_out_node.as<int32_t>(), n, lb + db, s, g);
-        HF_CUDA(cudaMemsetAsync(din.as<int32_t>() + n, 0, sizeof(int32_t), s));
-        HF_CUDA(cudaMemsetAsync(dout.as<int32_t>() + n, 0, sizeof(int32_t), s));
-        k_relabel_deg<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            g.lo_in_node.as<int32_t>(), g.in_ptr.as<int32_t>(), n, din.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        k_relabel_deg<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            g.lo_out_node.as<int32_t>(), g.out_ptr.as<int32_t>(), n, dout.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        scan_exclusive(din.as<int32_t>(), g.lo_in_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-        scan_exclusive(dout.as<int32_t>(), g.lo_out_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s,
-                       g);
-        k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            g.lo_in_node.as<int32_t>(), n, g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), nullptr,
-            g.lo_in_ptr.as<int32_t>(), g.lo_in_src.as<int32_t>(), g.lo_in_eid.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            g.lo_out_node.as<int32_t>(), n, g.out_ptr.as<int32_t>(), g.out_dst.as<int32_t>(),
-            g.out_eid.as<int32_t>(), g.lo_out_ptr.as<int32_t>(), g.lo_out_dst.as<int32_t>(),
-            g.lo_out_eid.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        g.launches += 5;
+        DevBuf flag, fs, deg;
+        flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        fs.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        deg.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        for (int dir = 0; dir < 2; ++dir) {
+            const int32_t *ptr = dir == 0 ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>();
+            int32_t *lo_node = dir == 0 ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+            int32_t *lo_ptr = dir == 0 ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+            k_lo_flags<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
+                g.order.as<int32_t>(), ptr, n, flag.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            scan_exclusive(flag.as<int32_t>(), fs.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+            k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
+                g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(),
+                fs.as<int32_t>(), flag.as<int32_t>(), ptr, n, lo_node, deg.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            scan_exclusive(deg.as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, s, g);
+            if (dir == 0)
+                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+                    lo_node, n, g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), nullptr, lo_ptr,
+                    g.lo_in_src.as<int32_t>(), g.lo_in_eid.as<int32_t>());
+            else
+                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+                    lo_node, n, g.out_ptr.as<int32_t>(), g.out_dst.as<int32_t>(),
+                    g.out_eid.as<int32_t>(), lo_ptr, g.lo_out_dst.as<int32_t>(),
+                    g.lo_out_eid.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            g.launches += 3;
+        }
     }
     g.ts_f.key = g.ts_b.key = -1;   // task schedules depend on the levels
     g.L = L;

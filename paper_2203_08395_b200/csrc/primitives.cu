@@ -1,15 +1,13 @@
 // primitives.cu -- device building blocks for graph ingest and levelization:
-// 3-phase exclusive scan, stable LSD radix sort (8-bit digits, warp-match
+// single-pass (decoupled look-back) exclusive scan, stable LSD radix sort (8-bit digits, warp-match
 // ranking), sorted-keys -> CSR offsets, CSR row ids.  All hand-written sm_100a.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace hf {
 
 namespace {
-
-constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_ITEMS = 8;
-constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
 
 // Block-wide exclusive sum of one value per thread; returns prefix, writes total.
 __device__ __forceinline__ int block_exclusive_sum(int v, int *total) {
@@ -41,57 +39,96 @@ __device__ __forceinline__ int block_exclusive_sum(int v, int *total) {
     return r;
 }
 
-__global__ void k_scan_tiles(const int32_t *__restrict__ in, int64_t count,
-                             int32_t *__restrict__ tile_sums) {
-    int64_t base = int64_t(blockIdx.x) * SCAN_TILE + int64_t(threadIdx.x) * SCAN_ITEMS;
-    int s = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j)
-        if (base + j < count) s += in[base + j];
-    int tot;
-    block_exclusive_sum(s, &tot);
-    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+// ---- single-pass scan (decoupled look-back) --------------------------------
+// Tiles take ids in launch order from a monotonic counter (ids of this call start
+// at `base`), so every predecessor tile is already running: no deadlock.  Each
+// tile publishes its aggregate, then its inclusive prefix, as one 64-bit word
+// {tag:32 | value:32} with tag = epoch*4 + kind (1 = aggregate, 2 = inclusive);
+// words of older calls carry an older epoch and read as "not yet published".
+constexpr int LB_BLOCK = 256;
+constexpr int LB_ITEMS = 16;
+constexpr int LB_TILE = LB_BLOCK * LB_ITEMS;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// single block: exclusive scan of tile sums in place (any length), total -> *total
-__global__ void k_scan_partials(int32_t *__restrict__ p, int64_t count, int32_t *total) {
-    int carry = 0;
-    for (int64_t base = 0; base < count; base += SCAN_TILE) {
-        int64_t i0 = base + int64_t(threadIdx.x) * SCAN_ITEMS;
-        int v[SCAN_ITEMS];
-        int s = 0;
+__global__ void __launch_bounds__(LB_BLOCK) k_scan_lookback(
+    const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t count,
+    unsigned long long *__restrict__ state, unsigned *__restrict__ ctr, unsigned base,
+    unsigned epoch, int32_t *__restrict__ total) {
+    __shared__ unsigned s_tile;
+    __shared__ int s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u) - base;
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int64_t i0 = int64_t(tile) * LB_TILE + int64_t(threadIdx.x) * LB_ITEMS;
+    int v[LB_ITEMS];
+    int sum = 0;
+    if (i0 + LB_ITEMS <= count && (reinterpret_cast<uintptr_t>(in + i0) & 15) == 0) {
 #pragma unroll
-        for (int j = 0; j < SCAN_ITEMS; ++j) {
-            v[j] = (i0 + j < count) ? p[i0 + j] : 0;
-            s += v[j];
+        for (int j = 0; j < LB_ITEMS; j += 4) {
+            const int4 q = *reinterpret_cast<const int4 *>(in + i0 + j);
+            v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
         }
-        int tot;
-        int pre = block_exclusive_sum(s, &tot) + carry;
+    } else {
 #pragma unroll
-        for (int j = 0; j < SCAN_ITEMS; ++j) {
-            if (i0 + j < count) p[i0 + j] = pre;
-            pre += v[j];
+        for (int j = 0; j < LB_ITEMS; ++j) v[j] = (i0 + j < count) ? in[i0 + j] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < LB_ITEMS; ++j) sum += v[j];
+    int agg;
+    int pre = block_exclusive_sum(sum, &agg);
+    const unsigned long long tagA = (unsigned long long)(epoch * 4u + 1u) << 32;
+    const unsigned long long tagP = (unsigned long long)(epoch * 4u + 2u) << 32;
+    if (threadIdx.x < 32) {
+        int excl = 0;
+        if (tile == 0) {
+            if (threadIdx.x == 0) st_relaxed_u64(state, tagP | unsigned(agg));
+        } else {
+            if (threadIdx.x == 0) st_relaxed_u64(state + tile, tagA | unsigned(agg));
+            // look back over windows of 32 predecessors
+            int64_t look = int64_t(tile) - 1;
+            const int lane = threadIdx.x;
+            for (;;) {
+                const int64_t j = look - lane;
+                unsigned long long w = 0;
+                unsigned kind = 0;
+                if (j >= 0) {
+                    do {
+                        w = ld_relaxed_u64(state + j);
+                        const unsigned tag = unsigned(w >> 32);
+                        kind = (tag >> 2) == epoch ? (tag & 3u) : 0u;
+                    } while (kind == 0);
+                }
+                // lanes past the first inclusive prefix (in look-back order) are ignored
+                const unsigned pmask = __ballot_sync(0xffffffffu, j >= 0 && kind == 2);
+                const int stop = pmask ? __ffs(pmask) - 1 : 31;
+                int val = (j >= 0 && lane <= stop) ? int(unsigned(w)) : 0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (pmask || look - 32 < 0) break;
+                look -= 32;
+            }
+            if (lane == 0) st_relaxed_u64(state + tile, tagP | unsigned(excl + agg));
         }
-        carry += tot;
-        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_excl = excl;
+            const int64_t last = (count - 1) / LB_TILE;
+            if (total && int64_t(tile) == last) *total = excl + agg;
+        }
     }
-    if (threadIdx.x == 0 && total) *total = carry;
-}
-
-__global__ void k_scan_apply(const int32_t *__restrict__ in, int32_t *__restrict__ out,
-                             int64_t count, const int32_t *__restrict__ tile_pre) {
-    int64_t base = int64_t(blockIdx.x) * SCAN_TILE + int64_t(threadIdx.x) * SCAN_ITEMS;
-    int v[SCAN_ITEMS];
-    int s = 0;
+    __syncthreads();
+    pre += s_excl;
 #pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        v[j] = (base + j < count) ? in[base + j] : 0;
-        s += v[j];
-    }
-    int pre = block_exclusive_sum(s, nullptr) + tile_pre[blockIdx.x];
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        if (base + j < count) out[base + j] = pre;
+    for (int j = 0; j < LB_ITEMS; ++j) {
+        if (i0 + j < count) out[i0 + j] = pre;
         pre += v[j];
     }
 }
@@ -208,16 +245,28 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t count, int32_t *tot
         if (total_d) HF_CUDA(cudaMemsetAsync(total_d, 0, sizeof(int32_t), s));
         return;
     }
-    int64_t tiles = (count + SCAN_TILE - 1) / SCAN_TILE;
-    DevBuf part;
-    part.alloc(sizeof(int32_t) * tiles, s);
-    k_scan_tiles<<<unsigned(tiles), SCAN_BLOCK, 0, s>>>(in, count, part.as<int32_t>());
+    const int64_t tiles = (count + LB_TILE - 1) / LB_TILE;
+    // look-back state: one word per tile + the tile counter, zeroed once on growth
+    const size_t need = sizeof(unsigned long long) * size_t(tiles + 1);
+    if (g.scan_state.bytes < need || g.scan_state.s != s) {
+        g.scan_state.alloc(std::max(need, size_t(8) << 12), s);
+        HF_CUDA(cudaMemsetAsync(g.scan_state.p, 0, g.scan_state.bytes, s));
+        g.scan_base = 0;
+        g.scan_epoch = 0;
+    }
+    if (++g.scan_epoch >= (1u << 29)) {   // tag overflow: start over from a clean state
+        HF_CUDA(cudaMemsetAsync(g.scan_state.p, 0, g.scan_state.bytes, s));
+        g.scan_base = 0;
+        g.scan_epoch = 1;
+    }
+    unsigned long long *st = g.scan_state.as<unsigned long long>();
+    unsigned *ctr = reinterpret_cast<unsigned *>(st);   // word 0 is the tile counter
+    k_scan_lookback<<<unsigned(tiles), LB_BLOCK, 0, s>>>(in, out, count, st + 1, ctr,
+                                                         unsigned(g.scan_base), g.scan_epoch,
+                                                         total_d);
     HF_CHECK_LAUNCH();
-    k_scan_partials<<<1, SCAN_BLOCK, 0, s>>>(part.as<int32_t>(), tiles, total_d);
-    HF_CHECK_LAUNCH();
-    k_scan_apply<<<unsigned(tiles), SCAN_BLOCK, 0, s>>>(in, out, count, part.as<int32_t>());
-    HF_CHECK_LAUNCH();
-    g.launches += 3;
+    g.scan_base += uint64_t(tiles);
+    g.launches += 1;
 }
 
 void radix_sort_pairs(const int32_t *keys_in, const int32_t *vals_in, int32_t *keys_out,

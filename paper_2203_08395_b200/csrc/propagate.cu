@@ -642,7 +642,9 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
 // the tail [lo, le) of every level.  A normal row weighs degree + 1; normal task j
 // of a level holds the rows whose weight prefix (from the level start) lies in
 // [j*tw, (j+1)*tw), so it has <= tw rows and <= tw + split - rows edges.  A split
-// row becomes ceil(degree / pe) part tasks of <= pe edges.
+// row becomes ceil(degree / pe) part tasks of <= pe edges.  A level has
+// floor(start weight of its last normal row / tw) + 1 normal tasks (some may be
+// empty when one row spans several multiples of tw).
 __global__ void k_tb_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
                           int32_t pe, int32_t *__restrict__ w, int32_t *__restrict__ parts) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -665,37 +667,46 @@ __global__ void k_tb_count(const int32_t *__restrict__ level_ptr, const int32_t 
             if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
             else lo = mid + 1;
         }
-        const int64_t wk = int64_t(W[lo]) - W[ls];
-        const int c = int((wk + tw - 1) / tw);
+        // tasks = those some row starts in: the last normal row starts task c - 1
+        const int c = lo > ls ? (W[lo - 1] - W[ls]) / tw + 1 : 0;
         ntn[k] = c;
         lonorm[k] = lo;
         nt[fwd ? k : L - 1 - k] = c + (Q[le] - Q[ls]);
     }
 }
+// normal task j of a level starts at the first row whose weight prefix reaches
+// j*tw: row i (> level start) starts every task j with W[i-1] < w0 + j*tw <= W[i]
+// and ends task j - 1; one thread per row, no search.
 __global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
                           const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ doff,
                           const int32_t *__restrict__ ntn, const int32_t *__restrict__ lonorm,
-                          int32_t L, int32_t tw, int32_t fwd, int4 *__restrict__ desc) {
-    for (int k = blockIdx.x; k < L; k += gridDim.x) {
+                          const int32_t *__restrict__ level, const int32_t *__restrict__ node_of,
+                          int32_t n, int32_t L, int32_t tw, int32_t fwd, int4 *__restrict__ desc) {
+    for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < n;
+         ii += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(ii);
+        const int k = level[node_of[i]];
         const int ls = level_ptr[k], lo = lonorm[k];
+        if (i >= lo) continue;   // long row: part tasks
+        int *d = reinterpret_cast<int *>(desc + doff[fwd ? k : L - 1 - k]);
         const int nn = ntn[k];
-        const int64_t w0 = W[ls];
-        const int base = doff[fwd ? k : L - 1 - k];
-        auto start_of = [&](int jj) {
-            if (jj >= nn) return lo;
-            if (jj == 0) return ls;
-            const int64_t target = w0 + int64_t(jj) * tw;
-            int a = ls, z = lo;   // first i in [ls, lo] with W[i] >= target
-            while (a < z) {
-                const int mid = (a + z) >> 1;
-                if (W[mid] >= target) z = mid;
-                else a = mid + 1;
+        const int w0 = W[ls];
+        const int rp = row_ptr[i];
+        if (i == ls) {
+            d[0] = i;
+            d[2] = rp;
+        } else {
+            const int jlo = (W[i - 1] - w0) / tw + 1, jhi = (W[i] - w0) / tw;
+            for (int j = jlo; j <= jhi; ++j) {
+                d[4 * j] = i;
+                d[4 * j + 2] = rp;
+                d[4 * (j - 1) + 1] = i;
+                d[4 * (j - 1) + 3] = rp;
             }
-            return a;
-        };
-        for (int j = threadIdx.x; j < nn; j += blockDim.x) {
-            const int a = start_of(j), z = start_of(j + 1);
-            desc[base + j] = make_int4(a, z, row_ptr[a], row_ptr[z]);
+        }
+        if (i == lo - 1) {
+            d[4 * (nn - 1) + 1] = lo;
+            d[4 * (nn - 1) + 3] = row_ptr[lo];
         }
     }
 }
@@ -787,9 +798,10 @@ void build_tasks(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const
     ts.nparts = h_tot[1];
     ts.desc.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
     ts.part_np.alloc(sizeof(int32_t) * size_t(std::max(ts.nparts, 1)), s);
-    k_tb_fill<<<int(std::min<int64_t>(L, 65535)), 128, 0, s>>>(
+    k_tb_fill<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
         g.level_ptr.as<int32_t>(), W.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(),
-        ntn.as<int32_t>(), lonorm.as<int32_t>(), L, tw, FWD ? 1 : 0, ts.desc.as<int4>());
+        ntn.as<int32_t>(), lonorm.as<int32_t>(), g.level.as<int32_t>(), node_of, n, L, tw,
+        FWD ? 1 : 0, ts.desc.as<int4>());
     HF_CHECK_LAUNCH();
     g.launches += 6;
     ts.nbr_enc.alloc(sizeof(int32_t) * size_t(m > 0 ? m : 1), s);
@@ -914,10 +926,10 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     // task shape: weight tw (rows + edges) per task, rows longer than split edges cut
     // into parts of pe edges; scratch capacity ecap = tw + split edges, ncap = tw rows
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
+    // split is fixed by the level-ordered CSR layout (long rows at the level's end)
+    const int split = LO_SPLIT;
     int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 12 : 16));
-    int split = env_int("HF_SPLIT", slots == 2 ? 16 : (G <= 2 ? 8 : 16));
-    tw = std::max(2, std::min(tw, 32 * slots - 1));
-    split = std::max(1, std::min(split, 32 * slots - tw));
+    tw = std::max(2, std::min(tw, 32 * slots - split));
     const int pe = tw + split;
     p.ecap = tw + split;
     p.ncap = tw;
@@ -930,6 +942,77 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
         ts.key = want;
     }
     task_bases(g, ts, p.nch);
+    if (getenv("HF_CHECK_TASKS")) {   // debugging: validate every descriptor on the host
+        int32_t total = 0;
+        HF_CUDA(cudaMemcpyAsync(&total, ts.doff.as<int32_t>() + g.L, 4, cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
+        std::vector<int4> h(size_t(std::max(total, 1)));
+        std::vector<int32_t> nt(size_t(g.L) + 1), doff(size_t(g.L) + 1);
+        HF_CUDA(cudaMemcpy(h.data(), ts.desc.p, sizeof(int4) * size_t(total), cudaMemcpyDeviceToHost));
+        HF_CUDA(cudaMemcpy(nt.data(), ts.nt.p, 4 * size_t(g.L), cudaMemcpyDeviceToHost));
+        HF_CUDA(cudaMemcpy(doff.data(), ts.doff.p, 4 * (size_t(g.L) + 1), cudaMemcpyDeviceToHost));
+        int bad = 0;
+        for (int32_t q = 0; q < g.L && bad < 10; ++q)
+            for (int32_t j = doff[q]; j < doff[q + 1] && bad < 10; ++j) {
+                const int4 d = h[size_t(j)];
+                const int E = d.w - d.z, NR = d.y < 0 ? 1 : d.y - d.x;
+                if (E < 0 || E > p.ecap || NR < 0 || NR > p.ncap) {
+                    fprintf(stderr, "bad task q=%d j=%d/%d {%d %d %d %d}\n", q, j - doff[q],
+                            nt[size_t(q)], d.x, d.y, d.z, d.w);
+                    ++bad;
+                }
+            }
+        fprintf(stderr, "checked %d tasks, %d bad (ecap %d ncap %d)\n", total, bad, p.ecap, p.ncap);
+        // host re-derivation of the whole schedule
+        std::vector<int32_t> rp(size_t(g.n) + 1), lp(size_t(g.L) + 1);
+        HF_CUDA(cudaMemcpy(rp.data(), p.row_ptr, 4 * rp.size(), cudaMemcpyDeviceToHost));
+        HF_CUDA(cudaMemcpy(lp.data(), g.level_ptr.p, 4 * lp.size(), cudaMemcpyDeviceToHost));
+        int shown = 0;
+        int32_t qid = 0;
+        for (int32_t qq = 0; qq < g.L && shown < 6; ++qq) {
+            const int k = FWD ? qq : g.L - 1 - qq;
+            const int ls = lp[size_t(k)], le = lp[size_t(k) + 1];
+            int lo = ls;
+            while (lo < le && rp[size_t(lo) + 1] - rp[size_t(lo)] <= split) ++lo;
+            for (int i = lo; i < le; ++i)
+                if (rp[size_t(i) + 1] - rp[size_t(i)] <= split) {
+                    fprintf(stderr, "level %d: short row %d after long rows (lo %d)\n", k, i, lo);
+                    ++shown;
+                    break;
+                }
+            std::vector<int4> ex;
+            int64_t wacc = 0;
+            int cur = -1;
+            for (int i = ls; i < lo; ++i) {
+                const int j = int(wacc / tw);
+                while (cur < j) {
+                    if (cur >= 0) ex.back().y = i, ex.back().w = rp[size_t(i)];
+                    ex.push_back(make_int4(i, 0, rp[size_t(i)], 0));
+                    ++cur;
+                }
+                wacc += rp[size_t(i) + 1] - rp[size_t(i)] + 1;
+            }
+            if (cur >= 0) ex.back().y = lo, ex.back().w = rp[size_t(lo)];
+            for (int i = lo; i < le; ++i) {
+                const int d = rp[size_t(i) + 1] - rp[size_t(i)];
+                for (int t = 0; t * pe < d; ++t)
+                    ex.push_back(make_int4(i, -1, rp[size_t(i)] + t * pe, std::min(rp[size_t(i) + 1], rp[size_t(i)] + (t + 1) * pe)));
+            }
+            if (int(ex.size()) != nt[size_t(qq)] && shown < 6) {
+                fprintf(stderr, "level %d: expected %zu tasks, device %d (ls %d lo %d le %d)\n", k, ex.size(), nt[size_t(qq)], ls, lo, le);
+                ++shown;
+            }
+            for (size_t j = 0; j < ex.size() && j < size_t(nt[size_t(qq)]) && shown < 6; ++j) {
+                const int4 a = ex[j], b = h[size_t(doff[size_t(qq)]) + j];
+                const bool same = a.x == b.x && a.z == b.z && a.w == b.w && (a.y < 0 ? b.y < 0 : a.y == b.y);
+                if (!same) {
+                    fprintf(stderr, "level %d task %zu: expected {%d %d %d %d} got {%d %d %d %d}\n", k, j, a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w);
+                    ++shown;
+                }
+            }
+            qid += nt[size_t(qq)];
+        }
+    }
     p.desc = ts.desc.as<int4>();
     p.nt = ts.nt.as<int32_t>();
     p.doff = ts.doff.as<int32_t>();
