@@ -41,7 +41,7 @@ UNIT = "edges/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="hf", choices=["hf", "reference"])
     p.add_argument("--config", default="C4")
@@ -83,7 +83,7 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks + throttle reasons sampled (NVML, every 100 ms) during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -95,6 +95,29 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        if os.environ.get("HF_BENCH_NO_CLOCKS"):   # diagnostics only
+            return
+        # in-process NVML (light); a spawned nvidia-smi contends for the driver lock
+        # with the timed CUDA calls, so it is only the fallback
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            getr = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                # two cheap queries per sample, 100 ms apart: NVML calls take driver
+                # locks that the timed CUDA calls also need
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = int(getr(h))
+                act = lambda bit: "Active" if r & bit else "Not Active"
+                self.rows.append([str(sm), str(mx), "", hex(r), act(0x8), act(0x40), act(0x20),
+                                  act(0x4)])
+                self._stop.wait(0.1)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -252,6 +275,8 @@ def main():
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
+            if os.environ.get("HF_BENCH_VERBOSE"):
+                print(f"step {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -79,17 +79,15 @@ struct TaskSched {
     DevBuf doff;        // [L+1] first descriptor of pass-level q
     DevBuf tb;          // [L+1] first global task of pass-level q (for tb_nch chunks)
     int32_t tb_nch = -1;
-    DevBuf q;           // [n+1] first part id of every row (exclusive scan of parts)
-    DevBuf part_np;     // [parts] number of parts of the row whose first part id it is
-    DevBuf nbr_enc;     // [m] neighbour ids; split rows as -(first part id + 1)
-    DevBuf split_rows;  // [1 + rows]: count, then positions of split rows
-    int32_t nparts = 0;
-    int64_t key = -1;   // (tw, split, pe) the schedule was built for
+    int64_t key = -1;   // tw the schedule was built for
 };
 
 // rows with more than LO_SPLIT edges sit at the end of their level in the
 // level-ordered CSRs and are cut into part tasks by the propagation passes
 constexpr int LO_SPLIT = 8;
+// a long row is cut into parts of LO_PE edges (part ids: exclusive scan over the
+// level-ordered rows of ceil(degree / LO_PE) for long rows, 0 otherwise)
+constexpr int LO_PE = 20;
 
 // ---- the graph -------------------------------------------------------------
 struct Graph {
@@ -110,8 +108,12 @@ struct Graph {
     // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
     // Within a level, rows of degree <= LO_SPLIT first, then the longer ones, each
     // run in canonical order (per direction): node ids lo_in_node / lo_out_node.
-    DevBuf lo_in_node, lo_in_ptr, lo_in_src, lo_in_eid;
-    DevBuf lo_out_node, lo_out_ptr, lo_out_dst, lo_out_eid;
+    DevBuf lo_in_node, lo_in_ptr, lo_in_nbr, lo_in_eid, lo_in_q, lo_in_np;
+    DevBuf lo_out_node, lo_out_ptr, lo_out_nbr, lo_out_eid, lo_out_q, lo_out_np;
+    // lo_*_nbr: neighbour node id, or -(first part id + 1) when the neighbour's own
+    // row (same direction) is long; lo_*_q: [n+1] first part id of every row;
+    // lo_*_np: parts of the long row whose first part id is the index
+    int32_t nparts_in = 0, nparts_out = 0;
     // task schedules of the dataflow propagation kernels (per direction)
     TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand

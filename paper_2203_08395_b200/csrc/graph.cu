@@ -89,6 +89,19 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
                  const int32_t *fo_ptr, const int32_t *fo_dst, const float *delay) {
     cudaStream_t s = g.stream;
     const int32_t n = g.n, m = g.m;
+    // keep freed device memory in the stream-ordered pool across synchronisations
+    // (the default release threshold 0 hands it back to the driver at every sync,
+    // and the next graph then pays for fresh mappings)
+    {
+        static bool done[64] = {};   // once per device
+        if (g.device >= 0 && g.device < 64 && !done[g.device]) {
+            cudaMemPool_t pool;
+            HF_CUDA(cudaDeviceGetDefaultMemPool(&pool, g.device));
+            uint64_t keep = UINT64_MAX;
+            HF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            done[g.device] = true;
+        }
+    }
     g.d_small.alloc(64 * sizeof(int32_t), s);
     HF_CUDA(cudaMemsetAsync(g.d_small.p, 0, 64 * sizeof(int32_t), s));
     g.in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);

@@ -19,6 +19,8 @@
 // Nodes never resolved (on or below a cycle) are counted -> HF_ERR_CYCLE.
 // Both persistent loops run as cooperative kernels with a grid barrier.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -289,15 +291,18 @@ __global__ void k_lo_flags(const int32_t *__restrict__ order, const int32_t *__r
         flag[i] = f;
     }
 }
-// stable partition of every level run of `order`: short rows, then long rows
+// stable partition of every level run of `order`: short rows, then long rows;
+// also the row position of every node and the part count of every row
 __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__restrict__ level,
                            const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ fs,
                            const int32_t *__restrict__ flag, const int32_t *__restrict__ ptr,
-                           int32_t n, int32_t *__restrict__ lo_node, int32_t *__restrict__ deg) {
+                           int32_t n, int32_t *__restrict__ lo_node, int32_t *__restrict__ deg,
+                           int32_t *__restrict__ parts, int32_t *__restrict__ pos_of) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
          i += int64_t(gridDim.x) * blockDim.x) {
         if (i == n) {
             deg[n] = 0;
+            parts[n] = 0;
             continue;
         }
         const int v = order[i];
@@ -305,18 +310,34 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
         const int ls = level_ptr[k], le = level_ptr[k + 1];
         const int sl = fs[i] - fs[ls];
         const int nlong = fs[le] - fs[ls];
-        const int pos = flag[i] ? le - nlong + sl : ls + (int(i) - ls) - sl;
+        const bool lng = flag[i] != 0;
+        const int pos = lng ? le - nlong + sl : ls + (int(i) - ls) - sl;
+        const int d = ptr[v + 1] - ptr[v];
         lo_node[pos] = v;
-        deg[pos] = ptr[v + 1] - ptr[v];
+        deg[pos] = d;
+        parts[pos] = lng ? (d + LO_PE - 1) / LO_PE : 0;
+        pos_of[v] = pos;
     }
 }
+// parts of every long row, stored at its first part id
+__global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__restrict__ np) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (lo_q[i + 1] != lo_q[i]) np[lo_q[i]] = lo_q[i + 1] - lo_q[i];
+}
 
-// copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid;
-// eid_map == null -> the edge id is the source position itself
+// copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid
+// (eid_map == null -> the edge id is the source position itself); a neighbour u
+// whose own row in this direction is long is written as -(first part id + 1)
+__device__ __forceinline__ int lo_enc(int u, const int32_t *ptr, const int32_t *pos,
+                                      const int32_t *q) {
+    return ptr[u + 1] - ptr[u] > LO_SPLIT ? -(q[pos[u]] + 1) : u;
+}
 __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
                                const int32_t *__restrict__ ptr, const int32_t *__restrict__ a,
                                const int32_t *__restrict__ eid_map,
-                               const int32_t *__restrict__ nptr, int32_t *__restrict__ na,
+                               const int32_t *__restrict__ nptr, const int32_t *__restrict__ pos,
+                               const int32_t *__restrict__ q, int32_t *__restrict__ na,
                                int32_t *__restrict__ neid) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps_total = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -333,7 +354,7 @@ __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
         bool longrow = (e - b) >= 32;
         if (!longrow)
             for (int k = b; k < e; ++k) {
-                na[o + (k - b)] = a[k];
+                na[o + (k - b)] = lo_enc(a[k], ptr, pos, q);
                 neid[o + (k - b)] = eid_map ? eid_map[k] : k;
             }
         unsigned lm = __ballot_sync(0xffffffffu, longrow);
@@ -344,7 +365,7 @@ __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
             int ee = __shfl_sync(0xffffffffu, e, srcl);
             int oo = __shfl_sync(0xffffffffu, o, srcl);
             for (int k = bb + lane; k < ee; k += 32) {
-                na[oo + (k - bb)] = a[k];
+                na[oo + (k - bb)] = lo_enc(a[k], ptr, pos, q);
                 neid[oo + (k - bb)] = eid_map ? eid_map[k] : k;
             }
         }
@@ -385,8 +406,20 @@ __global__ void k_set_scalars(int32_t *sc) {
 // Persistent cooperative grid: at most `cap` CTAs per SM (fewer CTAs = cheaper
 // grid barrier; the per-round work of these loops is small).
 int coop_grid(const void *func, int block, int sms, int cap = 2) {
+    // occupancy queries are cached: driver calls inside the timed step are avoided
+    static std::map<std::pair<const void *, int>, int> cache;
+    static std::mutex mu;
     int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, block, 0));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({func, block});
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, block, 0));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[{func, block}] = per_sm;
+    }
     if (per_sm < 1) fail(HF_ERR_CUDA, "cooperative kernel cannot be resident");
     return std::min(per_sm, cap) * sms;
 }
@@ -522,55 +555,73 @@ int64_t levelize_device(Graph &g) {
     radix_sort_pairs(g.level.as<int32_t>(), nullptr, skeys.as<int32_t>(), g.order.as<int32_t>(),
                      n, bits_for(int64_t(L) - 1), s, g);
     keys_to_ptr(skeys.as<int32_t>(), n, L, g.level_ptr.as<int32_t>(), s, g);
-    g.h_level_ptr.resize(size_t(L) + 1);
-    HF_CUDA(cudaMemcpyAsync(g.h_level_ptr.data(), g.level_ptr.p, sizeof(int32_t) * (L + 1),
-                            cudaMemcpyDeviceToHost, s));
-    HF_CUDA(cudaStreamSynchronize(s));
-    int32_t w = 0;
-    for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
-    g.max_level_width = w;
-    // relabel (a4): level-ordered fan-in / fan-out CSR for the propagation passes.
+    // relabel (a4): level-ordered CSR for the propagation passes.
     // Inside a level the rows with degree <= LO_SPLIT come first, then the longer
-    // rows (the task builder cuts those into parts); both runs keep canonical order.
+    // rows (cut into part tasks by the passes); both runs keep canonical order.
     {
+        const int64_t mm = m > 0 ? m : 1;
         g.lo_in_node.alloc(sizeof(int32_t) * n, s);
         g.lo_out_node.alloc(sizeof(int32_t) * n, s);
         g.lo_in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         g.lo_out_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        g.lo_in_src.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-        g.lo_in_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-        g.lo_out_dst.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-        g.lo_out_eid.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
-        DevBuf flag, fs, deg;
+        g.lo_in_q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        g.lo_out_q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        g.lo_in_nbr.alloc(sizeof(int32_t) * mm, s);
+        g.lo_in_eid.alloc(sizeof(int32_t) * mm, s);
+        g.lo_out_nbr.alloc(sizeof(int32_t) * mm, s);
+        g.lo_out_eid.alloc(sizeof(int32_t) * mm, s);
+        DevBuf flag, fs, deg, parts, pos;
         flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         fs.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         deg.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        parts.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        pos.alloc(sizeof(int32_t) * n, s);
         for (int dir = 0; dir < 2; ++dir) {
-            const int32_t *ptr = dir == 0 ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>();
-            int32_t *lo_node = dir == 0 ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
-            int32_t *lo_ptr = dir == 0 ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+            const bool in = dir == 0;
+            const int32_t *ptr = in ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>();
+            int32_t *lo_node = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+            int32_t *lo_ptr = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+            int32_t *lo_q = in ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
+            DevBuf &np = in ? g.lo_in_np : g.lo_out_np;
             k_lo_flags<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
                 g.order.as<int32_t>(), ptr, n, flag.as<int32_t>());
             HF_CHECK_LAUNCH();
             scan_exclusive(flag.as<int32_t>(), fs.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
             k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
                 g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(),
-                fs.as<int32_t>(), flag.as<int32_t>(), ptr, n, lo_node, deg.as<int32_t>());
+                fs.as<int32_t>(), flag.as<int32_t>(), ptr, n, lo_node, deg.as<int32_t>(),
+                parts.as<int32_t>(), pos.as<int32_t>());
             HF_CHECK_LAUNCH();
             scan_exclusive(deg.as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, s, g);
-            if (dir == 0)
+            scan_exclusive(parts.as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, s, g);
+            // parts of every long row, indexed by its first part id (<= m/9 + m/LO_PE ids)
+            np.alloc(sizeof(int32_t) * size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1), s);
+            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lo_q, n, np.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            if (in)
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-                    lo_node, n, g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), nullptr, lo_ptr,
-                    g.lo_in_src.as<int32_t>(), g.lo_in_eid.as<int32_t>());
+                    lo_node, n, ptr, g.in_src.as<int32_t>(), nullptr, lo_ptr, pos.as<int32_t>(),
+                    lo_q, g.lo_in_nbr.as<int32_t>(), g.lo_in_eid.as<int32_t>());
             else
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-                    lo_node, n, g.out_ptr.as<int32_t>(), g.out_dst.as<int32_t>(),
-                    g.out_eid.as<int32_t>(), lo_ptr, g.lo_out_dst.as<int32_t>(),
+                    lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
+                    pos.as<int32_t>(), lo_q, g.lo_out_nbr.as<int32_t>(),
                     g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
-            g.launches += 3;
+            g.launches += 4;
         }
     }
+    // one host round trip: level_ptr and the part counts of both directions
+    g.h_level_ptr.resize(size_t(L) + 1);
+    HF_CUDA(cudaMemcpyAsync(g.h_level_ptr.data(), g.level_ptr.p, sizeof(int32_t) * (L + 1),
+                            cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaMemcpyAsync(h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaStreamSynchronize(s));
+    g.nparts_in = h_sc[12];
+    g.nparts_out = h_sc[13];
+    int32_t w = 0;
+    for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
+    g.max_level_width = w;
     g.ts_f.key = g.ts_b.key = -1;   // task schedules depend on the levels
     g.L = L;
     g.levelized = true;

@@ -31,9 +31,13 @@
 //     per SC-column chunk); backward fuses slack = rat - at and keeps per-lane
 //     minima, folded per CTA into the worst slack (ordered-int atomicMin).
 //   * Rows cut into parts are read by their consumers as the combine of their
-//     partials (each sentinel-checked); their own rows are written after the
+//     partials (each sentinel-checked; the neighbour id is encoded as
+//     -(first part id + 1), levelize.cu); their own rows are written after the
 //     pass by k_finalize_split.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -130,9 +134,6 @@ template <int V> __device__ __forceinline__ void cp_async_v(float *dst, const fl
                      : "memory");
     }
 }
-__device__ __forceinline__ void cp_async_commit_wait() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -155,7 +156,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct FlowParams {
     // level-ordered CSR of this direction: row i <-> node node_of[i]
     const int32_t *row_ptr;   // [n+1]
-    const int32_t *nbr;       // [m] neighbour node id, split rows as -(first part id + 1)
+    const int32_t *nbr;       // [m] neighbour node id, long rows as -(first part id + 1)
     const int32_t *eid;       // [m] edge id (delay row)
     const int32_t *node_of;   // [n]
     const int4 *desc;         // task descriptors (TaskSched)
@@ -590,31 +591,37 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
     }
 }
 
-// After a pass: every split row gets its value (combine of its partials), its
-// optional slack and its worst-slack contribution.  One warp per split row.
+// After a pass: every long row gets its value (combine of its partials), its
+// optional slack and its worst-slack contribution.  Rows with parts are found
+// from the part-id prefix q; one warp per such row.
 template <bool FWD>
-__global__ void k_finalize_split(const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows,
-                                 const int32_t *__restrict__ row_ptr,
-                                 const int32_t *__restrict__ node_of, const int32_t *__restrict__ q,
-                                 int32_t pe, int32_t S, const float *__restrict__ part_buf,
-                                 float *__restrict__ out, const float *__restrict__ other,
-                                 float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
+__global__ void k_finalize_split(const int32_t *__restrict__ q, int32_t n,
+                                 const int32_t *__restrict__ node_of, int32_t S,
+                                 const float *__restrict__ part_buf, float *__restrict__ out,
+                                 const float *__restrict__ other, float *__restrict__ slack,
+                                 int32_t *__restrict__ wns_ord) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    const int cnt = *nrows;
-    for (int64_t r = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; r < cnt; r += nw) {
-        const int i = rows[r];
-        const int d = row_ptr[i + 1] - row_ptr[i];
-        const int np = (d + pe - 1) / pe, qb = q[i];
-        const int64_t node = node_of[i];
-        for (int s = lane; s < S; s += 32) {
-            float v = part_buf[int64_t(qb) * S + s];
-            for (int k = 1; k < np; ++k) v = combine<FWD>(v, part_buf[int64_t(qb + k) * S + s]);
-            out[node * S + s] = v;
-            if (!FWD) {
-                const float sl = __fsub_rn(v, other[node * S + s]);
-                if (slack) slack[node * S + s] = sl;
-                atomicMin(wns_ord + s, f2ord(sl));
+    for (int64_t base = ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5) * 32; base < n;
+         base += nw * 32) {
+        const int64_t i = base + lane;
+        const bool has = i < n && q[i + 1] != q[i];
+        unsigned mk = __ballot_sync(0xffffffffu, has);
+        while (mk) {
+            const int src = __ffs(mk) - 1;
+            mk &= mk - 1;
+            const int64_t r = base + src;
+            const int qb = q[r], np = q[r + 1] - qb;
+            const int64_t node = node_of[r];
+            for (int s = lane; s < S; s += 32) {
+                float v = part_buf[int64_t(qb) * S + s];
+                for (int k = 1; k < np; ++k) v = combine<FWD>(v, part_buf[int64_t(qb + k) * S + s]);
+                out[node * S + s] = v;
+                if (!FWD) {
+                    const float sl = __fsub_rn(v, other[node * S + s]);
+                    if (slack) slack[node * S + s] = sl;
+                    atomicMin(wns_ord + s, f2ord(sl));
+                }
             }
         }
     }
@@ -637,51 +644,40 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
         if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
 }
 
-// ---- task schedule (per direction; cached per (tw, split, pe)) -------------------
-// Rows of a level are in ascending degree, so the split rows (degree > split) form
-// the tail [lo, le) of every level.  A normal row weighs degree + 1; normal task j
-// of a level holds the rows whose weight prefix (from the level start) lies in
-// [j*tw, (j+1)*tw), so it has <= tw rows and <= tw + split - rows edges.  A split
-// row becomes ceil(degree / pe) part tasks of <= pe edges.  A level has
-// floor(start weight of its last normal row / tw) + 1 normal tasks (some may be
-// empty when one row spans several multiples of tw).
-__global__ void k_tb_rows(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                          int32_t pe, int32_t *__restrict__ w, int32_t *__restrict__ parts) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int d = row_ptr[i + 1] - row_ptr[i];
-        w[i] = d > split ? 0 : d + 1;
-        parts[i] = d > split ? (d + pe - 1) / pe : 0;
-    }
-}
-__global__ void k_tb_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
-                           const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr,
-                           int32_t L, int32_t split, int32_t tw, int32_t fwd,
-                           int32_t *__restrict__ nt, int32_t *__restrict__ ntn,
+// ---- task schedule (per direction; cached per tw) --------------------------------
+// Inside a level the short rows (degree <= LO_SPLIT) come first, then the long ones
+// (levelize.cu).  A short row weighs degree + 1; normal task j of a level holds the
+// rows whose weight prefix from the level start lies in [j*tw, (j+1)*tw), so it has
+// <= tw rows and <= tw + LO_SPLIT - rows edges; the prefix of row i is
+// (row_ptr[i] - row_ptr[ls]) + (i - ls), no scan needed.  A level has
+// floor(prefix of its last short row / tw) + 1 normal tasks (some may be empty when
+// one row spans several multiples of tw).  Long row i becomes parts q[i]..q[i+1]-1
+// of <= LO_PE edges.
+__global__ void k_tb_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ Q,
+                           const int32_t *__restrict__ row_ptr, int32_t L, int32_t tw,
+                           int32_t fwd, int32_t *__restrict__ nt, int32_t *__restrict__ ntn,
                            int32_t *__restrict__ lonorm) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
         const int ls = level_ptr[k], le = level_ptr[k + 1];
-        int lo = ls, hi = le;   // first row with degree > split
+        int lo = ls, hi = le;   // first long row
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (row_ptr[mid + 1] - row_ptr[mid] > split) hi = mid;
+            if (row_ptr[mid + 1] - row_ptr[mid] > LO_SPLIT) hi = mid;
             else lo = mid + 1;
         }
-        // tasks = those some row starts in: the last normal row starts task c - 1
-        const int c = lo > ls ? (W[lo - 1] - W[ls]) / tw + 1 : 0;
+        const int c = lo > ls ? ((row_ptr[lo - 1] - row_ptr[ls]) + (lo - 1 - ls)) / tw + 1 : 0;
         ntn[k] = c;
         lonorm[k] = lo;
         nt[fwd ? k : L - 1 - k] = c + (Q[le] - Q[ls]);
     }
 }
-// normal task j of a level starts at the first row whose weight prefix reaches
-// j*tw: row i (> level start) starts every task j with W[i-1] < w0 + j*tw <= W[i]
-// and ends task j - 1; one thread per row, no search.
-__global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ W,
-                          const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ doff,
-                          const int32_t *__restrict__ ntn, const int32_t *__restrict__ lonorm,
-                          const int32_t *__restrict__ level, const int32_t *__restrict__ node_of,
-                          int32_t n, int32_t L, int32_t tw, int32_t fwd, int4 *__restrict__ desc) {
+// row i (> level start) starts every task j with P(i-1) < j*tw <= P(i) and ends
+// task j - 1 (P = weight prefix); one thread per row, no search
+__global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ row_ptr,
+                          const int32_t *__restrict__ doff, const int32_t *__restrict__ ntn,
+                          const int32_t *__restrict__ lonorm, const int32_t *__restrict__ level,
+                          const int32_t *__restrict__ node_of, int32_t n, int32_t L, int32_t tw,
+                          int32_t fwd, int4 *__restrict__ desc) {
     for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < n;
          ii += int64_t(gridDim.x) * blockDim.x) {
         const int i = int(ii);
@@ -690,13 +686,15 @@ __global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *
         if (i >= lo) continue;   // long row: part tasks
         int *d = reinterpret_cast<int *>(desc + doff[fwd ? k : L - 1 - k]);
         const int nn = ntn[k];
-        const int w0 = W[ls];
+        const int r0 = row_ptr[ls];
         const int rp = row_ptr[i];
         if (i == ls) {
             d[0] = i;
             d[2] = rp;
         } else {
-            const int jlo = (W[i - 1] - w0) / tw + 1, jhi = (W[i] - w0) / tw;
+            const int pprev = (row_ptr[i - 1] - r0) + (i - 1 - ls);
+            const int pcur = (rp - r0) + (i - ls);
+            const int jlo = pprev / tw + 1, jhi = pcur / tw;
             for (int j = jlo; j <= jhi; ++j) {
                 d[4 * j] = i;
                 d[4 * j + 2] = rp;
@@ -713,46 +711,19 @@ __global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *
 __global__ void k_tb_parts(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
                            const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
                            const int32_t *__restrict__ Q, const int32_t *__restrict__ doff,
-                           const int32_t *__restrict__ ntn, int32_t n, int32_t L, int32_t split,
-                           int32_t pe, int32_t fwd, int4 *__restrict__ desc,
-                           int32_t *__restrict__ part_np) {
+                           const int32_t *__restrict__ ntn, int32_t n, int32_t L, int32_t fwd,
+                           int4 *__restrict__ desc) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
+        const int q0 = Q[i], np = Q[i + 1] - q0;
+        if (np == 0) continue;
         const int rb = row_ptr[i], re = row_ptr[i + 1];
-        if (re - rb <= split) continue;
         const int k = level[node_of[i]];
-        const int base = doff[fwd ? k : L - 1 - k] + ntn[k] + (Q[i] - Q[level_ptr[k]]);
-        const int np = (re - rb + pe - 1) / pe;
-        part_np[Q[i]] = np;
+        const int base = doff[fwd ? k : L - 1 - k] + ntn[k] + (q0 - Q[level_ptr[k]]);
         for (int t = 0; t < np; ++t)
-            desc[base + t] = make_int4(int(i), -(Q[i] + t + 1), rb + t * pe, min(re, rb + (t + 1) * pe));
+            desc[base + t] = make_int4(int(i), -(q0 + t + 1), rb + t * LO_PE,
+                                       min(re, rb + (t + 1) * LO_PE));
     }
-}
-__global__ void k_pos_of(const int32_t *__restrict__ node_of, int32_t n, int32_t *__restrict__ pos) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        pos[node_of[i]] = int(i);
-}
-__global__ void k_nbr_enc(const int32_t *__restrict__ nbr, int32_t m, const int32_t *__restrict__ pos,
-                          const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ Q,
-                          int32_t split, int32_t *__restrict__ enc) {
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int v = nbr[e];
-        const int i = pos[v];
-        enc[e] = (row_ptr[i + 1] - row_ptr[i] > split) ? -(Q[i] + 1) : v;
-    }
-}
-__global__ void k_split_list(const int32_t *__restrict__ row_ptr, int32_t n, int32_t split,
-                             int32_t *__restrict__ rows, int32_t *__restrict__ cnt) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        if (row_ptr[i + 1] - row_ptr[i] > split) rows[atomicAdd(cnt, 1)] = int(i);
-}
-__global__ void k_tb_totals(const int32_t *__restrict__ doff, const int32_t *__restrict__ Q,
-                            int32_t L, int32_t n, int32_t *__restrict__ out) {
-    out[0] = doff[L];
-    out[1] = Q[n];
 }
 __global__ void k_tb_base(const int32_t *__restrict__ nt, int32_t L, int32_t nch,
                           int32_t *__restrict__ x) {
@@ -760,77 +731,37 @@ __global__ void k_tb_base(const int32_t *__restrict__ nt, int32_t L, int32_t nch
         x[k] = nt[k] * nch;
 }
 
+// no host round trip: descriptors are sized by the bound (n + m)/tw + L + parts
 template <bool FWD>
-void build_tasks(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *nbr,
-                 int tw, int split, int pe, TaskSched &ts) {
+void build_tasks(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *Q,
+                 int32_t nparts, int tw, TaskSched &ts) {
     cudaStream_t s = g.stream;
     const int32_t n = g.n, L = g.L, m = g.m;
-    DevBuf w, W, pr, ntn, lonorm;
-    DevBuf &Q = ts.q;
-    w.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    W.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    pr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-    Q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    DevBuf ntn, lonorm;
     ntn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     lonorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     ts.nt.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     ts.doff.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    HF_CUDA(cudaMemsetAsync(w.as<int32_t>() + n, 0, sizeof(int32_t), s));
-    HF_CUDA(cudaMemsetAsync(pr.as<int32_t>() + n, 0, sizeof(int32_t), s));
     HF_CUDA(cudaMemsetAsync(ts.nt.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_tb_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(row_ptr, n, split, pe, w.as<int32_t>(),
-                                                      pr.as<int32_t>());
-    HF_CHECK_LAUNCH();
-    scan_exclusive(w.as<int32_t>(), W.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    scan_exclusive(pr.as<int32_t>(), Q.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
     k_tb_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), W.as<int32_t>(), Q.as<int32_t>(), row_ptr, L, split, tw,
-        FWD ? 1 : 0, ts.nt.as<int32_t>(), ntn.as<int32_t>(), lonorm.as<int32_t>());
+        g.level_ptr.as<int32_t>(), Q, row_ptr, L, tw, FWD ? 1 : 0, ts.nt.as<int32_t>(),
+        ntn.as<int32_t>(), lonorm.as<int32_t>());
     HF_CHECK_LAUNCH();
     scan_exclusive(ts.nt.as<int32_t>(), ts.doff.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
-    int32_t *tot = g.d_scalars() + 40;
-    k_tb_totals<<<1, 1, 0, s>>>(ts.doff.as<int32_t>(), Q.as<int32_t>(), L, n, tot);
-    HF_CHECK_LAUNCH();
-    int32_t h_tot[2] = {0, 0};
-    HF_CUDA(cudaMemcpyAsync(h_tot, tot, sizeof(h_tot), cudaMemcpyDeviceToHost, s));
-    HF_CUDA(cudaStreamSynchronize(s));
-    const int32_t total = h_tot[0];
-    ts.nparts = h_tot[1];
-    ts.desc.alloc(sizeof(int4) * size_t(std::max(total, 1)), s);
-    ts.part_np.alloc(sizeof(int32_t) * size_t(std::max(ts.nparts, 1)), s);
+    const int64_t cap = (int64_t(n) + m) / tw + L + nparts + 1;
+    ts.desc.alloc(sizeof(int4) * size_t(cap), s);
     k_tb_fill<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), W.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(),
-        ntn.as<int32_t>(), lonorm.as<int32_t>(), g.level.as<int32_t>(), node_of, n, L, tw,
-        FWD ? 1 : 0, ts.desc.as<int4>());
+        g.level_ptr.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(), ntn.as<int32_t>(),
+        lonorm.as<int32_t>(), g.level.as<int32_t>(), node_of, n, L, tw, FWD ? 1 : 0,
+        ts.desc.as<int4>());
     HF_CHECK_LAUNCH();
-    g.launches += 6;
-    ts.nbr_enc.alloc(sizeof(int32_t) * size_t(m > 0 ? m : 1), s);
-    if (ts.nparts == 0) {
-        if (m)
-            HF_CUDA(cudaMemcpyAsync(ts.nbr_enc.p, nbr, sizeof(int32_t) * size_t(m),
-                                    cudaMemcpyDeviceToDevice, s));
-    } else {
+    g.launches += 2;
+    if (nparts > 0) {
         k_tb_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q.as<int32_t>(),
-            ts.doff.as<int32_t>(), ntn.as<int32_t>(), n, L, split, pe, FWD ? 1 : 0,
-            ts.desc.as<int4>(), ts.part_np.as<int32_t>());
+            row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q,
+            ts.doff.as<int32_t>(), ntn.as<int32_t>(), n, L, FWD ? 1 : 0, ts.desc.as<int4>());
         HF_CHECK_LAUNCH();
-        DevBuf pos;
-        pos.alloc(sizeof(int32_t) * size_t(n), s);
-        k_pos_of<<<grid_for(n, 256, g.sms), 256, 0, s>>>(node_of, n, pos.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        if (m) {
-            k_nbr_enc<<<grid_for(m, 256, g.sms), 256, 0, s>>>(nbr, m, pos.as<int32_t>(), row_ptr,
-                                                              Q.as<int32_t>(), split,
-                                                              ts.nbr_enc.as<int32_t>());
-            HF_CHECK_LAUNCH();
-        }
-        ts.split_rows.alloc(sizeof(int32_t) * (size_t(n) + 1), s);
-        HF_CUDA(cudaMemsetAsync(ts.split_rows.p, 0, sizeof(int32_t), s));
-        k_split_list<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            row_ptr, n, split, ts.split_rows.as<int32_t>() + 1, ts.split_rows.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        g.launches += 4;
+        g.launches += 1;
     }
     ts.tb_nch = -1;
 }
@@ -876,9 +807,22 @@ void launch_flow(Graph &g, FlowParams &p) {
     constexpr int SC = V * LPN;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
-    HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // attribute + occupancy per (kernel, smem, device) once: no driver queries per call
+    static std::map<std::tuple<const void *, size_t, int>, int> cache;
+    static std::mutex mu;
     int per_sm = 0;
-    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
+    const auto key = std::make_tuple((const void *)kern, smem, g.device);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = per_sm;
+    }
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
     const int cap = env_int("HF_CTAS_PER_SM", 0);
     if (cap > 0) per_sm = std::min(per_sm, cap);
@@ -923,107 +867,34 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
         while (LPN < 16 && p.S % (V * LPN * 2) == 0 && V * LPN * 2 <= sc_max) LPN *= 2;
     const int SC = V * LPN, G = 32 / LPN;
     p.nch = p.S / SC;
-    // task shape: weight tw (rows + edges) per task, rows longer than split edges cut
-    // into parts of pe edges; scratch capacity ecap = tw + split edges, ncap = tw rows
+    // task shape: weight tw (rows + edges) per task; rows longer than LO_SPLIT edges
+    // (at the end of their level, levelize.cu) are cut into parts of LO_PE edges;
+    // scratch capacity ecap = tw + LO_SPLIT edges (>= LO_PE), ncap = tw rows
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
-    // split is fixed by the level-ordered CSR layout (long rows at the level's end)
-    const int split = LO_SPLIT;
     int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 12 : 16));
-    tw = std::max(2, std::min(tw, 32 * slots - split));
-    const int pe = tw + split;
-    p.ecap = tw + split;
+    tw = std::max(LO_PE - LO_SPLIT, std::min(tw, 32 * slots - LO_SPLIT));
+    p.ecap = tw + LO_SPLIT;
     p.ncap = tw;
     p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
     p.poll_all = env_int("HF_POLL_ALL", 1);
     TaskSched &ts = FWD ? g.ts_f : g.ts_b;
-    const int64_t want = (int64_t(tw) << 20) | (int64_t(split) << 8) | 1;
-    if (ts.key != want || !ts.desc.p) {
-        build_tasks<FWD>(g, p.row_ptr, p.node_of, p.nbr, tw, split, pe, ts);
-        ts.key = want;
+    const int32_t nparts = FWD ? g.nparts_in : g.nparts_out;
+    const int32_t *Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
+    if (ts.key != tw || !ts.desc.p) {
+        build_tasks<FWD>(g, p.row_ptr, p.node_of, Q, nparts, tw, ts);
+        ts.key = tw;
     }
     task_bases(g, ts, p.nch);
-    if (getenv("HF_CHECK_TASKS")) {   // debugging: validate every descriptor on the host
-        int32_t total = 0;
-        HF_CUDA(cudaMemcpyAsync(&total, ts.doff.as<int32_t>() + g.L, 4, cudaMemcpyDeviceToHost, s));
-        HF_CUDA(cudaStreamSynchronize(s));
-        std::vector<int4> h(size_t(std::max(total, 1)));
-        std::vector<int32_t> nt(size_t(g.L) + 1), doff(size_t(g.L) + 1);
-        HF_CUDA(cudaMemcpy(h.data(), ts.desc.p, sizeof(int4) * size_t(total), cudaMemcpyDeviceToHost));
-        HF_CUDA(cudaMemcpy(nt.data(), ts.nt.p, 4 * size_t(g.L), cudaMemcpyDeviceToHost));
-        HF_CUDA(cudaMemcpy(doff.data(), ts.doff.p, 4 * (size_t(g.L) + 1), cudaMemcpyDeviceToHost));
-        int bad = 0;
-        for (int32_t q = 0; q < g.L && bad < 10; ++q)
-            for (int32_t j = doff[q]; j < doff[q + 1] && bad < 10; ++j) {
-                const int4 d = h[size_t(j)];
-                const int E = d.w - d.z, NR = d.y < 0 ? 1 : d.y - d.x;
-                if (E < 0 || E > p.ecap || NR < 0 || NR > p.ncap) {
-                    fprintf(stderr, "bad task q=%d j=%d/%d {%d %d %d %d}\n", q, j - doff[q],
-                            nt[size_t(q)], d.x, d.y, d.z, d.w);
-                    ++bad;
-                }
-            }
-        fprintf(stderr, "checked %d tasks, %d bad (ecap %d ncap %d)\n", total, bad, p.ecap, p.ncap);
-        // host re-derivation of the whole schedule
-        std::vector<int32_t> rp(size_t(g.n) + 1), lp(size_t(g.L) + 1);
-        HF_CUDA(cudaMemcpy(rp.data(), p.row_ptr, 4 * rp.size(), cudaMemcpyDeviceToHost));
-        HF_CUDA(cudaMemcpy(lp.data(), g.level_ptr.p, 4 * lp.size(), cudaMemcpyDeviceToHost));
-        int shown = 0;
-        int32_t qid = 0;
-        for (int32_t qq = 0; qq < g.L && shown < 6; ++qq) {
-            const int k = FWD ? qq : g.L - 1 - qq;
-            const int ls = lp[size_t(k)], le = lp[size_t(k) + 1];
-            int lo = ls;
-            while (lo < le && rp[size_t(lo) + 1] - rp[size_t(lo)] <= split) ++lo;
-            for (int i = lo; i < le; ++i)
-                if (rp[size_t(i) + 1] - rp[size_t(i)] <= split) {
-                    fprintf(stderr, "level %d: short row %d after long rows (lo %d)\n", k, i, lo);
-                    ++shown;
-                    break;
-                }
-            std::vector<int4> ex;
-            int64_t wacc = 0;
-            int cur = -1;
-            for (int i = ls; i < lo; ++i) {
-                const int j = int(wacc / tw);
-                while (cur < j) {
-                    if (cur >= 0) ex.back().y = i, ex.back().w = rp[size_t(i)];
-                    ex.push_back(make_int4(i, 0, rp[size_t(i)], 0));
-                    ++cur;
-                }
-                wacc += rp[size_t(i) + 1] - rp[size_t(i)] + 1;
-            }
-            if (cur >= 0) ex.back().y = lo, ex.back().w = rp[size_t(lo)];
-            for (int i = lo; i < le; ++i) {
-                const int d = rp[size_t(i) + 1] - rp[size_t(i)];
-                for (int t = 0; t * pe < d; ++t)
-                    ex.push_back(make_int4(i, -1, rp[size_t(i)] + t * pe, std::min(rp[size_t(i) + 1], rp[size_t(i)] + (t + 1) * pe)));
-            }
-            if (int(ex.size()) != nt[size_t(qq)] && shown < 6) {
-                fprintf(stderr, "level %d: expected %zu tasks, device %d (ls %d lo %d le %d)\n", k, ex.size(), nt[size_t(qq)], ls, lo, le);
-                ++shown;
-            }
-            for (size_t j = 0; j < ex.size() && j < size_t(nt[size_t(qq)]) && shown < 6; ++j) {
-                const int4 a = ex[j], b = h[size_t(doff[size_t(qq)]) + j];
-                const bool same = a.x == b.x && a.z == b.z && a.w == b.w && (a.y < 0 ? b.y < 0 : a.y == b.y);
-                if (!same) {
-                    fprintf(stderr, "level %d task %zu: expected {%d %d %d %d} got {%d %d %d %d}\n", k, j, a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w);
-                    ++shown;
-                }
-            }
-            qid += nt[size_t(qq)];
-        }
-    }
     p.desc = ts.desc.as<int4>();
     p.nt = ts.nt.as<int32_t>();
     p.doff = ts.doff.as<int32_t>();
     p.tb = ts.tb.as<int32_t>();
-    p.nbr = ts.nbr_enc.as<int32_t>();
-    p.part_np = ts.part_np.as<int32_t>();
+    p.part_np = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
     p.L = g.L;
     p.err = g.d_err();
     DevBuf part_buf;
-    if (ts.nparts > 0) {
-        part_buf.alloc(sizeof(float) * size_t(ts.nparts) * p.S, s);
+    if (nparts > 0) {
+        part_buf.alloc(sizeof(float) * size_t(nparts) * p.S, s);
         p.part_buf = part_buf.as<float>();
         HF_CUDA(cudaMemsetAsync(part_buf.p, 0xff, part_buf.bytes, s));
     }
@@ -1043,10 +914,9 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     }
     if (check_d) dispatch<FWD, true>(g, p, V, LPN);
     else dispatch<FWD, false>(g, p, V, LPN);
-    if (ts.nparts > 0) {
-        k_finalize_split<FWD><<<g.sms, 256, 0, s>>>(
-            ts.split_rows.as<int32_t>() + 1, ts.split_rows.as<int32_t>(), p.row_ptr, p.node_of,
-            ts.q.as<int32_t>(), pe, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+    if (nparts > 0) {
+        k_finalize_split<FWD><<<grid_for(g.n, 256, g.sms), 256, 0, s>>>(
+            Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
@@ -1078,7 +948,7 @@ void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const flo
     FlowParams p{};
     const int V = pick_vec(S, {d, at});
     p.row_ptr = g.lo_in_ptr.as<int32_t>();
-    p.nbr = g.lo_in_src.as<int32_t>();
+    p.nbr = g.lo_in_nbr.as<int32_t>();
     p.eid = g.lo_in_eid.as<int32_t>();
     p.node_of = g.lo_in_node.as<int32_t>();
     p.S = S;
@@ -1106,7 +976,7 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         FlowParams p{};
         const int V = pick_vec(S, {d, at, rat, slack});
         p.row_ptr = g.lo_out_ptr.as<int32_t>();
-        p.nbr = g.lo_out_dst.as<int32_t>();
+        p.nbr = g.lo_out_nbr.as<int32_t>();
         p.eid = g.lo_out_eid.as<int32_t>();
         p.node_of = g.lo_out_node.as<int32_t>();
         p.S = S;
