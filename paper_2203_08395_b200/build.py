@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(os.path.dirname(HERE), "include"),
+        extra = os.environ.get("HF_NVCC_FLAGS", "").split()
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(os.path.dirname(HERE), "include"),
                "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                             stderr=subprocess.STDOUT, text=True)))
