@@ -180,6 +180,11 @@ hf_status hf_nccl_comm_destroy(void *comm);
 hf_status hf_profile_enable(hf_graph g, int on);
 hf_status hf_profile_read(hf_graph g, float *ms_levelize, float *ms_forward,
                           float *ms_backward, int64_t *kernel_launches);
+/* Milliseconds of the propagation phase of the most recent hf_run_batch call: from
+ * the first propagation kernel to the worst slacks (forward and backward kernels
+ * run concurrently on two streams, then the slack/WNS pass; ms_forward/ms_backward
+ * above are the two kernels' own, overlapping, durations). */
+hf_status hf_profile_read_batch(hf_graph g, float *ms_batch_propagation);
 
 #ifdef __cplusplus
 }

@@ -23,6 +23,8 @@ void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const flo
                     float *at);
 void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, float t_scalar,
                      const float *at, float *rat, float *slack, float *wns_f);
+void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
+                  const float *t_arr, float *at, float *rat, float *slack, float *wns_f);
 void profile_mark(Graph &g, int idx);
 
 // ---- NCCL through dlopen (no link-time dependency) -------------------------
@@ -237,6 +239,12 @@ hf_status hf_graph_destroy(hf_graph h) {
         cudaStreamSynchronize(g->stream);
         for (auto &e : g->ev)
             if (e) cudaEventDestroy(e);
+        if (g->fork) cudaEventDestroy(g->fork);
+        if (g->join) cudaEventDestroy(g->join);
+        if (g->s2) {
+            cudaStreamSynchronize(g->s2);
+            cudaStreamDestroy(g->s2);
+        }
         delete g;   // DevBufs free stream-ordered
         return HF_OK;
     });
@@ -281,11 +289,7 @@ static hf_status levelize_impl(hf_graph h, int32_t *num_levels, int32_t *level, 
         DeviceGuard dg(g->device);
         if (g->prof) profile_mark(*g, 0);
         int64_t unready = levelize_device(*g);
-        if (g->prof) {
-            profile_mark(*g, 1);
-            HF_CUDA(cudaEventSynchronize(g->ev[1]));
-            HF_CUDA(cudaEventElapsedTime(&g->ms_lev, g->ev[0], g->ev[1]));
-        }
+        if (g->prof) profile_mark(*g, 1);   // read (synchronising) by hf_profile_read
         if (unready) {
             fail(HF_ERR_CYCLE, "cycle: " + std::to_string(unready) + " nodes never become ready");
         }
@@ -320,8 +324,10 @@ static void need_levels(Graph *g) {
 static void prof_elapsed(Graph *g) {
     if (!g->prof) return;
     float ms = 0;
+    if (cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]) == cudaSuccess) g->ms_lev = ms;
     if (cudaEventElapsedTime(&ms, g->ev[2], g->ev[3]) == cudaSuccess) g->ms_fwd = ms;
     if (cudaEventElapsedTime(&ms, g->ev[5], g->ev[4]) == cudaSuccess) g->ms_bwd = ms;
+    if (cudaEventElapsedTime(&ms, g->ev[6], g->ev[7]) == cudaSuccess) g->ms_prop = ms;
     cudaGetLastError();   // clear "not recorded" errors
 }
 
@@ -414,8 +420,7 @@ static void batch_core(Graph *g, int32_t S, const float *d_ms, const float *t_d,
         if (g->ws_rat.bytes < nb || g->ws_rat.s != g->stream) g->ws_rat.alloc(nb, g->stream);
         rat_d = g->ws_rat.as<float>();
     }
-    forward_device(*g, d_ms, S, true, at_src_d, at_d);
-    backward_device(*g, d_ms, S, t_d, 0.0f, at_d, rat_d, nullptr, wns_d);
+    batch_device(*g, d_ms, S, true, at_src_d, t_d, at_d, rat_d, nullptr, wns_d);
     if (comm) {
         nccl::load();
         nccl::check(nccl::api.all_gather(wns_d, wns_all_d, size_t(S), nccl::kFloat32, comm,
@@ -592,6 +597,20 @@ hf_status hf_profile_read(hf_graph h, float *ms_levelize, float *ms_forward, flo
         if (ms_forward) *ms_forward = g->ms_fwd;
         if (ms_backward) *ms_backward = g->ms_bwd;
         if (kernel_launches) *kernel_launches = g->launches;
+        return HF_OK;
+    });
+}
+
+hf_status hf_profile_read_batch(hf_graph h, float *ms_batch_propagation) {
+    return guarded([&]() -> hf_status {
+        if (!h) fail(HF_ERR_INVALID_ARG, "graph is NULL");
+        Graph *g = G(h);
+        DeviceGuard dg(g->device);
+        if (g->prof) {
+            HF_CUDA(cudaStreamSynchronize(g->stream));
+            prof_elapsed(g);
+        }
+        if (ms_batch_propagation) *ms_batch_propagation = g->ms_prop;
         return HF_OK;
     });
 }

@@ -205,7 +205,8 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
         e = read_err(g);
         if (e) fail(HF_ERR_BAD_CSR, "fan-out is not the transpose of the fan-in");
     }
-    HF_CUDA(cudaStreamSynchronize(s));
+    // no trailing synchronisation: the fan-out build is stream-ordered before every
+    // later call, and the validation read above already completed the uploads
 }
 
 }  // namespace hf

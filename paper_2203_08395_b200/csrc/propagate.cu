@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         __syncwarp();
         for (int k = g; k < E; k += G)
             cp_async_v<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col);
-        if (!FWD && !part)
+        if (!FWD && !part && p.other)
             for (int i = g; i < NR; i += G)
                 cp_async_v<V>(s_at + i * SC + gl * V, p.other + int64_t(s_node[i]) * S + col);
         cp_async_commit();
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     }
                 }
                 st_relaxed<V>(p.out + int64_t(node) * S + col, best);
-                if (!FWD) {
+                if (!FWD && p.other) {
                     const Vec<V> av = ld_s<V>(s_at + i * SC + gl * V);
                     Vec<V> sl;
 #pragma unroll
@@ -617,7 +617,7 @@ __global__ void k_finalize_split(const int32_t *__restrict__ q, int32_t n,
                 float v = part_buf[int64_t(qb) * S + s];
                 for (int k = 1; k < np; ++k) v = combine<FWD>(v, part_buf[int64_t(qb + k) * S + s]);
                 out[node * S + s] = v;
-                if (!FWD) {
+                if (!FWD && other) {
                     const float sl = __fsub_rn(v, other[node * S + s]);
                     if (slack) slack[node * S + s] = sl;
                     atomicMin(wns_ord + s, f2ord(sl));
@@ -642,6 +642,55 @@ __global__ void k_ord_to_float(const int32_t *__restrict__ k, float *__restrict_
 __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err) {
     for (int i = threadIdx.x; i < S; i += blockDim.x)
         if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
+}
+
+// slack = fl(rat - at) for every node and scenario, the worst slack per scenario
+// (ordered-int atomicMin), optional slack store: the epilogue of the concurrent
+// batch, where the backward kernel runs next to the forward one and never sees at.
+template <int V>
+__global__ void k_slack_wns(const float *__restrict__ at, const float *__restrict__ rat,
+                            float *__restrict__ slack, int32_t n, int32_t S,
+                            int32_t *__restrict__ wns_ord) {
+    extern __shared__ int32_t s_wmin[];
+    for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
+    __syncthreads();
+    const int lpn = S / V;
+    const int apb = blockDim.x / lpn * lpn;             // active threads per block
+    const int64_t step = int64_t(gridDim.x) * apb;      // a multiple of lpn: lane fixed
+    const int lane = int(threadIdx.x % lpn);
+    float mn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+    if (int(threadIdx.x) < apb) {
+        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < int64_t(n) * lpn; t += step) {
+            const int64_t o = (t / lpn) * S + int64_t(lane) * V;
+            Vec<V> a, r, sl;
+            if constexpr (V == 4) {
+                const float4 x = __ldcs(reinterpret_cast<const float4 *>(at + o));
+                const float4 y = __ldcs(reinterpret_cast<const float4 *>(rat + o));
+                a.x[0] = x.x; a.x[1] = x.y; a.x[2] = x.z; a.x[3] = x.w;
+                r.x[0] = y.x; r.x[1] = y.y; r.x[2] = y.z; r.x[3] = y.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    a.x[j] = __ldcs(at + o + j);
+                    r.x[j] = __ldcs(rat + o + j);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                sl.x[j] = __fsub_rn(r.x[j], a.x[j]);
+                mn[j] = fminf(mn[j], sl.x[j]);
+            }
+            if (slack) st_plain<V>(slack + o, sl);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + lane * V + j, f2ord(mn[j]));
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < S; s += blockDim.x)
+        if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
 }
 
 // ---- task schedule (per direction; cached per tw) --------------------------------
@@ -792,8 +841,8 @@ int pick_vec(int32_t S, std::initializer_list<const void *> ptrs) {
     return 1;
 }
 
-void prof_record(Graph &g, int idx) {
-    if (g.prof) HF_CUDA(cudaEventRecord(g.ev[idx], g.stream));
+void prof_record(Graph &g, int idx, cudaStream_t st = nullptr) {
+    if (g.prof) HF_CUDA(cudaEventRecord(g.ev[idx], st ? st : g.stream));
 }
 
 int env_int(const char *name, int dflt) {
@@ -802,7 +851,7 @@ int env_int(const char *name, int dflt) {
 }
 
 template <int V, int LPN, bool FWD, bool CHECK_D, bool GA>
-void launch_flow(Graph &g, FlowParams &p) {
+void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
     auto kern = k_flow<V, LPN, FWD, CHECK_D, GA>;
     constexpr int SC = V * LPN;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
@@ -826,47 +875,90 @@ void launch_flow(Graph &g, FlowParams &p) {
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
     const int cap = env_int("HF_CTAS_PER_SM", 0);
     if (cap > 0) per_sm = std::min(per_sm, cap);
+    if (cap_per_sm > 0) per_sm = std::min(per_sm, cap_per_sm);
     void *args[] = {&p};
     // all warps co-resident (cooperative launch): required by the dataflow wait.
     // With profiling on, events bracket exactly this launch (forward: ev 2/3,
     // backward 5/4).
-    prof_record(g, FWD ? 2 : 5);
+    prof_record(g, FWD ? 2 : 5, st);
     HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms * per_sm, FLOW_THREADS, args,
-                                        smem, g.stream));
-    prof_record(g, FWD ? 3 : 4);
+                                        smem, st));
+    prof_record(g, FWD ? 3 : 4, st);
     g.launches += 1;
 }
 
-template <bool FWD, bool CHECK_D, bool GA> void dispatch_ga(Graph &g, FlowParams &p, int LPN) {
-    switch (LPN) {
-    case 16: launch_flow<4, 16, FWD, CHECK_D, GA>(g, p); break;
-    case 8: launch_flow<4, 8, FWD, CHECK_D, GA>(g, p); break;
-    case 4: launch_flow<4, 4, FWD, CHECK_D, GA>(g, p); break;
-    case 2: launch_flow<4, 2, FWD, CHECK_D, GA>(g, p); break;
-    default: launch_flow<4, 1, FWD, CHECK_D, GA>(g, p); break;
-    }
-}
-template <bool FWD, bool CHECK_D> void dispatch(Graph &g, FlowParams &p, int V, int LPN) {
-    if (V == 4) {
-        if (env_int("HF_GA", 0)) dispatch_ga<FWD, CHECK_D, true>(g, p, LPN);
-        else dispatch_ga<FWD, CHECK_D, false>(g, p, LPN);
-    } else if (V == 2) {
-        launch_flow<2, 1, FWD, CHECK_D, false>(g, p);
-    } else {
-        launch_flow<1, 1, FWD, CHECK_D, false>(g, p);
-    }
+// blocks per SM a kernel can keep resident alone (cached occupancy query)
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA> int occupancy_of(FlowParams &p) {
+    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA>;
+    const WarpLayout WL = warp_layout(p.ecap, p.ncap, V * LPN, FWD, GA);
+    const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
+    static std::map<size_t, int> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(smem);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
+    cache[smem] = per_sm;
+    return per_sm;
 }
 
-// one pass: task schedule, sentinel fill, the dataflow kernel, split-row finalise
-template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) {
+// op = 0: launch, op = 1: return the solo occupancy (blocks per SM)
+template <bool FWD, bool CHECK_D, bool GA>
+int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int op) {
+#define HF_CASE(L)                                                               \
+    case L:                                                                      \
+        if (op) return occupancy_of<4, L, FWD, CHECK_D, GA>(p);                  \
+        launch_flow<4, L, FWD, CHECK_D, GA>(g, p, st, cap);                      \
+        return 0;
+    switch (LPN) {
+        HF_CASE(16)
+        HF_CASE(8)
+        HF_CASE(4)
+        HF_CASE(2)
+    default:
+        HF_CASE(1)
+    }
+#undef HF_CASE
+}
+template <bool FWD, bool CHECK_D>
+int dispatch(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st = nullptr, int cap = 0,
+             int op = 0) {
+    if (!st) st = g.stream;
+    if (V == 4) {
+        if (env_int("HF_GA", 0)) return dispatch_ga<FWD, CHECK_D, true>(g, p, LPN, st, cap, op);
+        return dispatch_ga<FWD, CHECK_D, false>(g, p, LPN, st, cap, op);
+    } else if (V == 2) {
+        if (op) return occupancy_of<2, 1, FWD, CHECK_D, false>(p);
+        launch_flow<2, 1, FWD, CHECK_D, false>(g, p, st, cap);
+    } else {
+        if (op) return occupancy_of<1, 1, FWD, CHECK_D, false>(p);
+        launch_flow<1, 1, FWD, CHECK_D, false>(g, p, st, cap);
+    }
+    return 0;
+}
+
+// host-side state of a prepared pass
+struct PassCtx {
+    int LPN = 1;
+    int32_t nparts = 0;
+    const int32_t *Q = nullptr;
+    DevBuf part_buf;
+};
+
+// task schedule, bases, partial buffer and the sentinel fill of the output (on the
+// graph's stream)
+template <bool FWD> void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx) {
     cudaStream_t s = g.stream;
     // scenario chunk: SC = V * LPN columns (largest power of two <= HF_SC dividing S)
     const int sc_max = std::max(1, env_int("HF_SC", 64));
     int LPN = 1;
     if (V == 4)
         while (LPN < 16 && p.S % (V * LPN * 2) == 0 && V * LPN * 2 <= sc_max) LPN *= 2;
-    const int SC = V * LPN, G = 32 / LPN;
-    p.nch = p.S / SC;
+    const int G = 32 / LPN;
+    cx.LPN = LPN;
+    p.nch = p.S / (V * LPN);
     // task shape: weight tw (rows + edges) per task; rows longer than LO_SPLIT edges
     // (at the end of their level, levelize.cu) are cut into parts of LO_PE edges;
     // scratch capacity ecap = tw + LO_SPLIT edges (>= LO_PE), ncap = tw rows
@@ -878,10 +970,10 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
     p.poll_all = env_int("HF_POLL_ALL", 1);
     TaskSched &ts = FWD ? g.ts_f : g.ts_b;
-    const int32_t nparts = FWD ? g.nparts_in : g.nparts_out;
-    const int32_t *Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
+    cx.nparts = FWD ? g.nparts_in : g.nparts_out;
+    cx.Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
     if (ts.key != tw || !ts.desc.p) {
-        build_tasks<FWD>(g, p.row_ptr, p.node_of, Q, nparts, tw, ts);
+        build_tasks<FWD>(g, p.row_ptr, p.node_of, cx.Q, cx.nparts, tw, ts);
         ts.key = tw;
     }
     task_bases(g, ts, p.nch);
@@ -892,14 +984,35 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     p.part_np = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
     p.L = g.L;
     p.err = g.d_err();
-    DevBuf part_buf;
-    if (nparts > 0) {
-        part_buf.alloc(sizeof(float) * size_t(nparts) * p.S, s);
-        p.part_buf = part_buf.as<float>();
-        HF_CUDA(cudaMemsetAsync(part_buf.p, 0xff, part_buf.bytes, s));
+    if (cx.nparts > 0) {
+        cx.part_buf.alloc(sizeof(float) * size_t(cx.nparts) * p.S, s);
+        p.part_buf = cx.part_buf.as<float>();
+        HF_CUDA(cudaMemsetAsync(cx.part_buf.p, 0xff, cx.part_buf.bytes, s));
     }
     // the NaN sentinel (all-ones bit pattern): "not yet computed"
     HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
+}
+
+// the dataflow kernel and the long-row finalisation, on stream st
+template <bool FWD>
+void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cudaStream_t st,
+                 int cap) {
+    if (check_d) dispatch<FWD, true>(g, p, V, cx.LPN, st, cap);
+    else dispatch<FWD, false>(g, p, V, cx.LPN, st, cap);
+    if (cx.nparts > 0) {
+        k_finalize_split<FWD><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
+            cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+}
+
+// one pass: task schedule, sentinel fill, the dataflow kernel, split-row finalise
+template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) {
+    cudaStream_t s = g.stream;
+    PassCtx cx;
+    prepare_pass<FWD>(g, p, V, cx);
+    const int SC = V * cx.LPN;
     // debugging timeline: HF_TRACE=<file prefix> dumps one record per task
     const char *trace_env = getenv("HF_TRACE");
     DevBuf tbuf;
@@ -912,14 +1025,7 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
         p.trace = tbuf.as<unsigned long long>();
         p.trace_cap = ntask;
     }
-    if (check_d) dispatch<FWD, true>(g, p, V, LPN);
-    else dispatch<FWD, false>(g, p, V, LPN);
-    if (nparts > 0) {
-        k_finalize_split<FWD><<<grid_for(g.n, 256, g.sms), 256, 0, s>>>(
-            Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
-    }
+    launch_pass<FWD>(g, p, check_d, V, cx, s, 0);
     if (trace_env) {
         // per task: {warp, t_start, t_ready (first gathers complete), t_done} + level
         std::vector<unsigned long long> h(size_t(ntask) * 4);
@@ -994,6 +1100,92 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
+}
+
+// Batch: forward then backward (default), or with HF_CONCURRENT=1 both passes at
+// once.  The backward recurrence (rat of sinks = T, rat[u] = min fl(rat[v] - d))
+// does not read at -- only the slack does -- so both dataflow kernels can be
+// resident side by side (each capped at about half the blocks per SM it could hold
+// alone) on two streams, the slack and worst slack following in one streaming pass.
+// Measured on C4 (S = 64): slower (1.48 ms vs 1.32 ms for the phase), because each
+// pass then has half the resident warps and the dataflow needs many warps to keep
+// several levels in flight; kept for the record.
+void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
+                  const float *t_arr, float *at, float *rat, float *slack, float *wns_f) {
+    cudaStream_t s = g.stream;
+    if (!env_int("HF_CONCURRENT", 0) || g.n == 0) {
+        prof_record(g, 6);
+        forward_device(g, d, S, check_d, at_src, at);
+        backward_device(g, d, S, t_arr, 0.0f, at, rat, slack, wns_f);
+        prof_record(g, 7);
+        return;
+    }
+    g.ws_wns.alloc(sizeof(int32_t) * size_t(S), s);
+    int32_t *ord = g.ws_wns.as<int32_t>();
+    k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
+    if (t_arr) {
+        k_check_t<<<1, 256, 0, s>>>(t_arr, S, g.d_err());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+    FlowParams pf{}, pb{};
+    const int V = pick_vec(S, {d, at, rat, slack});
+    pf.row_ptr = g.lo_in_ptr.as<int32_t>();
+    pf.nbr = g.lo_in_nbr.as<int32_t>();
+    pf.eid = g.lo_in_eid.as<int32_t>();
+    pf.node_of = g.lo_in_node.as<int32_t>();
+    pf.S = S;
+    pf.d = d;
+    pf.src_val = at_src;
+    pf.out = at;
+    pb.row_ptr = g.lo_out_ptr.as<int32_t>();
+    pb.nbr = g.lo_out_nbr.as<int32_t>();
+    pb.eid = g.lo_out_eid.as<int32_t>();
+    pb.node_of = g.lo_out_node.as<int32_t>();
+    pb.S = S;
+    pb.d = d;
+    pb.src_val = t_arr;
+    pb.out = rat;
+    pb.other = nullptr;   // no slack inside the pass
+    PassCtx cf, cb;
+    prepare_pass<true>(g, pf, V, cf);
+    prepare_pass<false>(g, pb, V, cb);
+    // blocks per SM for each kernel when both are resident
+    const int of = check_d ? dispatch<true, true>(g, pf, V, cf.LPN, s, 0, 1)
+                           : dispatch<true, false>(g, pf, V, cf.LPN, s, 0, 1);
+    const int ob = dispatch<false, false>(g, pb, V, cb.LPN, s, 0, 1);
+    const int capf = std::max(1, env_int("HF_CAP_F", (of + 1) / 2));
+    const int capb = std::max(1, env_int("HF_CAP_B", ob / 2));
+    if (!g.s2) {
+        HF_CUDA(cudaStreamCreateWithFlags(&g.s2, cudaStreamNonBlocking));
+        HF_CUDA(cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming));
+        HF_CUDA(cudaEventCreateWithFlags(&g.join, cudaEventDisableTiming));
+    }
+    prof_record(g, 6);
+    HF_CUDA(cudaEventRecord(g.fork, s));
+    HF_CUDA(cudaStreamWaitEvent(g.s2, g.fork, 0));
+    launch_pass<false>(g, pb, false, V, cb, g.s2, capb);
+    launch_pass<true>(g, pf, check_d, V, cf, s, capf);
+    HF_CUDA(cudaEventRecord(g.join, g.s2));
+    HF_CUDA(cudaStreamWaitEvent(s, g.join, 0));
+    const int lpn = S / V;
+    const int grid = grid_for(int64_t(g.n) * lpn, 512, g.sms);
+    const size_t sm = sizeof(int32_t) * size_t(S);
+    if (sm > 48 * 1024) fail(HF_ERR_INVALID_ARG, "too many scenarios");
+    if (V == 4) k_slack_wns<4><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
+    else if (V == 2) k_slack_wns<2><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
+    else k_slack_wns<1><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
+    prof_record(g, 7);
+    if (wns_f) {
+        k_ord_to_float<<<1, 256, 0, s>>>(ord, wns_f, S);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+    // cf / cb partial buffers are freed on s, after the join
 }
 
 void profile_mark(Graph &g, int idx) { prof_record(g, idx); }

@@ -29,6 +29,7 @@ EXPORTS = [
     "hf_levelize_d", "hf_propagate_forward", "hf_propagate_forward_d", "hf_propagate_backward",
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
+    "hf_profile_read_batch",
 ]
 
 
@@ -68,6 +69,7 @@ def _load() -> ctypes.CDLL:
         "hf_nccl_comm_destroy": (c_int, [P]),
         "hf_profile_enable": (c_int, [P, c_int]),
         "hf_profile_read": (c_int, [P, P, P, P, P]),
+        "hf_profile_read_batch": (c_int, [P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -263,6 +265,13 @@ def hf_profile_read(g: Graph):
     _check(_lib.hf_profile_read(g.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                 ctypes.byref(k)))
     return a.value, b.value, c.value, k.value
+
+
+def hf_profile_read_batch(g: Graph) -> float:
+    """ms of the propagation phase of the most recent hf_run_batch (fwd || bwd + slack)"""
+    a = ctypes.c_float()
+    _check(_lib.hf_profile_read_batch(g.handle, ctypes.byref(a)))
+    return a.value
 
 
 def hf_version() -> int:

@@ -292,6 +292,23 @@ def test_batch_small(hf, S):
     assert_bits_equal(w, wo, "wns")
 
 
+@pytest.mark.parametrize("S", [3, 64])
+def test_batch_concurrent_passes(hf, S, monkeypatch):
+    # HF_CONCURRENT=1: forward and backward kernels resident side by side on two
+    # streams, slack/WNS in a separate pass -- same bits as the oracle
+    monkeypatch.setenv("HF_CONCURRENT", "1")
+    g = hfgen.config("C3", 0.004)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[1::2] += 2.25
+    w, at, rat = gpu_batch_device(hf, g, D, T, S)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                                 want_at_rat=True)
+    assert_bits_equal(at, ato, "at")
+    assert_bits_equal(rat, rato, "rat")
+    assert_bits_equal(w, wo, "wns")
+
+
 def test_batch_host_api_both_layouts(hf):
     g = hfgen.config("C1")
     S = 6

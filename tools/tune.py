@@ -60,21 +60,23 @@ def main():
             if k not in ("HF_NCCL_LIBRARY",):
                 del os.environ[k]
         os.environ.update(cfg)
-        f, b = [], []
+        f, b, pp = [], [], []
         for r in range(a.reps + 1):
             flush.fill_(1.0)
             hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, at_src, w)
             _, fm, bm, _ = hf.hf_profile_read(G)
+            ph = hf.hf_profile_read_batch(G)
             if r > 0:
                 f.append(fm)
                 b.append(bm)
+                pp.append(ph)
         res = w.cpu().numpy().view(np.uint32).copy()
         same = "" if ref is None else ("" if np.array_equal(ref, res) else "  WNS MISMATCH")
         ref = res if ref is None else ref
-        fm, bm = float(np.median(f)), float(np.median(b))
-        print(f"{' '.join(f'{k}={v}' for k, v in cfg.items()):50s} fwd {fm:7.3f} ms "
-              f"({nb_f / fm / 1e6:6.0f} GB/s) bwd {bm:7.3f} ms ({nb_b / bm / 1e6:6.0f} GB/s) "
-              f"sum {fm + bm:7.3f}{same}", flush=True)
+        fm, bm, pm = float(np.median(f)), float(np.median(b)), float(np.median(pp))
+        print(f"{' '.join(f'{k}={v}' for k, v in cfg.items()):40s} fwd {fm:7.3f} ms "
+              f"bwd {bm:7.3f} ms  phase {pm:7.3f} ms ({(nb_f + nb_b) / pm / 1e6:6.0f} GB/s)"
+              f"{same}", flush=True)
 
 
 if __name__ == "__main__":
