@@ -59,8 +59,12 @@ def _load():
         lib.oracle_backward.argtypes = [i32, i32, P, P, P, ctypes.c_float, P, P, P, P, P]
         lib.oracle_batch.argtypes = [i32, i32, P, P, i32, P, ctypes.c_int, P, P, P, P, P,
                                      ctypes.c_int]
+        lib.oracle_critical_path.argtypes = [i32, i32, P, P, P, ctypes.c_int64, P,
+                                             ctypes.c_float, P, i32, P]
+        lib.oracle_critical_paths.argtypes = [i32, i32, P, P, i32, P, P, P, P, i32, P]
         for f in (lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
-                  lib.oracle_forward, lib.oracle_backward, lib.oracle_batch):
+                  lib.oracle_forward, lib.oracle_backward, lib.oracle_batch,
+                  lib.oracle_critical_path, lib.oracle_critical_paths):
             f.restype = ctypes.c_int
         lib.oracle_fanout.restype = None
         _lib = lib
@@ -186,3 +190,38 @@ def batch(n, m, in_ptr, in_src, delays, t_req, at_src=None, layout: str = "ms",
     if want_at_rat:
         return wns[:S], at_all, rat_all
     return wns[:S]
+
+
+def critical_path(n, m, in_ptr, in_src, delay, at, t_req, max_len=None):
+    """NEXT-1 (reading R17): nodes of the critical path of the worst endpoint,
+    endpoint first, source last (one delay set in fan-in edge order)."""
+    lib = _load()
+    in_ptr, in_src = _i32(in_ptr), _i32(in_src)
+    d = _f32(delay) if m else np.zeros(1, np.float32)
+    at = _f32(at) if n else np.zeros(1, np.float32)
+    max_len = max(1, n if max_len is None else max_len)
+    path = np.zeros(max_len, np.int32)
+    ln = ctypes.c_int32(0)
+    rc = lib.oracle_critical_path(n, m, _p(in_ptr), _p(in_src), _p(d), ctypes.c_int64(1), _p(at),
+                                  ctypes.c_float(t_req), _p(path), max_len, ctypes.byref(ln))
+    if rc:
+        raise OracleError(rc)
+    return path[:ln.value].copy()
+
+
+def critical_paths(n, m, in_ptr, in_src, delays_ms, at_all, t_req, max_len=None):
+    """S scenarios: delays [m][S], at [n][S], t_req[S] -> list of S paths."""
+    lib = _load()
+    in_ptr, in_src = _i32(in_ptr), _i32(in_src)
+    delays_ms = _f32(delays_ms)
+    S = delays_ms.shape[1]
+    at_all = _f32(at_all)
+    t = _f32(np.broadcast_to(np.asarray(t_req, np.float32), (S,)))
+    max_len = max(1, n if max_len is None else max_len)
+    paths = np.zeros((S, max_len), np.int32)
+    lens = np.zeros(S, np.int32)
+    rc = lib.oracle_critical_paths(n, m, _p(in_ptr), _p(in_src), S, _p(delays_ms), _p(at_all),
+                                   _p(t), _p(paths), max_len, _p(lens))
+    if rc:
+        raise OracleError(rc)
+    return [paths[s, :lens[s]].copy() for s in range(S)]

@@ -21,6 +21,7 @@
  *                                                           BASELINE.json:5; reading R3
  *   - slack = fl(rat - at), wns = min slack                  BASELINE.json:5; reading R4
  *   - batched what-if scenarios = independent delay sets     PAPER.md:969-980; BASELINE.json:10
+ *   - critical path of the worst endpoint (argmax trace-back) PAPER.md:1002-1003; reading R17
  *
  * Every function is a direct transcription of SURVEY.md §8(c)'s pseudo-code:
  * FIFO Kahn, then one sequential sweep over the topological order.  Status
@@ -310,4 +311,63 @@ int oracle_batch(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_
     free(th); free(topo); free(level); free(lptr); free(order);
     free(out_ptr); free(out_dst); free(out_eid);
     return OR_OK;
+}
+
+/* ---- NEXT-1: critical-path trace-back -------------------
+ * PAPER.md:1002-1003 ("extract graph information (critical paths, ...)") names the
+ * step; reading R17 fixes it:
+ *   endpoint = the sink (out-degree 0) with the smallest slack fl(T - at[sink]),
+ *              ties by the smallest node id;
+ *   from v = endpoint, step to src(e) for the fan-in edge e of v with
+ *              fl(at[src e] + d[e]) == at[v] (an edge that attains the max),
+ *              ties by the smallest fan-in edge id, until a source (in-degree 0).
+ * path[0] = endpoint ... path[len-1] = the source.  d is read with stride dstride
+ * (1 for one delay set, S for the scenario-minor batch layout).  Returns
+ * OR_INVALID if at is not a forward result of these delays (no attaining edge) or
+ * the path is longer than max_len; n == 0 gives len = 0. */
+int oracle_critical_path(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                         const float *d, int64_t dstride, const float *at, float T,
+                         int32_t *path, int32_t max_len, int32_t *len) {
+    *len = 0;
+    if (n == 0) return OR_OK;
+    int32_t *outdeg = (int32_t *)calloc((size_t)n, sizeof(int32_t));
+    for (int32_t e = 0; e < m; ++e) outdeg[in_src[e]] += 1;
+    T = canon(T);
+    int32_t v = -1;
+    float worst = 0.0f;
+    for (int32_t u = 0; u < n; ++u) {
+        if (outdeg[u] != 0) continue;
+        float s = T - at[u];
+        if (v < 0 || s < worst) { v = u; worst = s; }   /* ascending u: ties keep the smallest */
+    }
+    free(outdeg);
+    if (v < 0) return OR_INVALID;   /* a DAG with n > 0 always has a sink */
+    for (;;) {
+        if (*len >= max_len) return OR_INVALID;
+        path[(*len)++] = v;
+        if (in_ptr[v + 1] == in_ptr[v]) return OR_OK;   /* source */
+        int32_t best = -1;
+        for (int32_t e = in_ptr[v]; e < in_ptr[v + 1] && best < 0; ++e) {
+            float x = at[in_src[e]] + canon(d[(int64_t)e * dstride]);
+            if (x == at[v]) best = e;
+        }
+        if (best < 0) return OR_INVALID;
+        v = in_src[best];
+    }
+}
+
+/* S scenarios: delays [m][S] (scenario-minor), at_all [n][S], t_req[S];
+ * paths [S][max_len], lens[S]. */
+int oracle_critical_paths(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                          int32_t S, const float *delays, const float *at_all, const float *t_req,
+                          int32_t *paths, int32_t max_len, int32_t *lens) {
+    float *at = (float *)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    int rc = OR_OK;
+    for (int32_t s = 0; s < S && rc == OR_OK; ++s) {
+        for (int32_t v = 0; v < n; ++v) at[v] = at_all[(int64_t)v * S + s];
+        rc = oracle_critical_path(n, m, in_ptr, in_src, delays + s, S, at, t_req[s],
+                                  paths + (int64_t)s * max_len, max_len, lens + s);
+    }
+    free(at);
+    return rc;
 }

@@ -4,6 +4,8 @@ Each test ties oracle/ to something other than itself: the paper's worked graphs
 (tests/golden/, cited), closed forms, generator-known levels, brute-force path
 enumeration, exact integer DFS, invariants and metamorphic relations.
 """
+import itertools
+
 import numpy as np
 import pytest
 
@@ -332,3 +334,93 @@ def test_fanout_check_multiset():
     od3 = od.copy()
     od3[op[k]] = (od3[op[k]] + 1) % g.n
     assert oracle.check_fanout(g.n, g.m, g.in_ptr, g.in_src, op, od3) == oracle.BAD_CSR
+
+
+# ---- P11: critical-path trace-back (NEXT-1, reading R17) --------------------------
+def _greedy_int_path(n, src, dst, d_int, a_int, T):
+    """Expected path in exact integer arithmetic: worst sink (T - at, ties by id), then
+    the smallest fan-in edge id attaining the max, independently of the float code."""
+    at = dfs_int_at(n, src, dst, d_int, a_int)
+    outdeg = np.bincount(np.asarray(src, np.int64), minlength=n) if len(src) else np.zeros(n)
+    sinks = [v for v in range(n) if outdeg[v] == 0]
+    v = min(sinks, key=lambda u: (T - at[u], u))
+    ins = [[] for _ in range(n)]
+    for e in range(len(src)):
+        ins[dst[e]].append(e)
+    path = [v]
+    while ins[v]:
+        e = min(e for e in ins[v] if at[src[e]] + d_int[e] == at[v])
+        v = src[e]
+        path.append(v)
+    return path
+
+
+def test_p11_critical_path_integer_ties():
+    # integer delays in [1, 4]: many exact ties, so the tie rules are exercised
+    rng = np.random.default_rng(11)
+    for trial in range(400):
+        n, edges = random_tiny_dag(rng, nmax=10, p=0.5)
+        m = len(edges)
+        in_ptr, in_src, perm = csr_from_edges(n, edges)
+        dst = np.repeat(np.arange(n), np.diff(in_ptr)).astype(np.int64)
+        d_int = rng.integers(1, 5, size=m)
+        a_int = rng.integers(0, 3, size=n)
+        T = 40
+        at = oracle.forward(n, m, in_ptr, in_src, d_int.astype(F32), a_int.astype(F32))
+        got = oracle.critical_path(n, m, in_ptr, in_src, d_int.astype(F32), at, T)
+        exp = _greedy_int_path(n, in_src.tolist(), dst.tolist(), d_int.tolist(), a_int.tolist(), T)
+        assert got.tolist() == exp, trial
+    g = hfgen.config("C1", 0.3)
+    d_int = rng.integers(1, 65, size=g.m)
+    a_int = rng.integers(0, 100, size=g.n)
+    src, dst = g.edges()
+    at = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, d_int.astype(F32), a_int.astype(F32))
+    got = oracle.critical_path(g.n, g.m, g.in_ptr, g.in_src, d_int.astype(F32), at, 10 ** 6)
+    exp = _greedy_int_path(g.n, src.tolist(), dst.tolist(), d_int.tolist(), a_int.tolist(), 10 ** 6)
+    assert got.tolist() == exp
+
+
+def test_p11_critical_path_bruteforce_fp32():
+    # mixed-magnitude fp32 delays: the traced path is a real source -> worst-sink path
+    # whose left-to-right fp32 sum is the brute-force maximum at the endpoint
+    rng = np.random.default_rng(1102)
+    for trial in range(400):
+        n, edges = random_tiny_dag(rng)
+        m = len(edges)
+        d = mixed_delays(rng, m)
+        at_src = mixed_delays(rng, n)
+        T = float(mixed_delays(rng, 1)[0])
+        in_ptr, in_src, perm = csr_from_edges(n, edges)
+        ewd = [(u, v, d[k]) for k, (u, v) in enumerate(edges)]
+        at_b, _ = brute_forward(n, ewd, at_src)
+        at = oracle.forward(n, m, in_ptr, in_src, d[perm], at_src)
+        path = oracle.critical_path(n, m, in_ptr, in_src, d[perm], at, T).tolist()
+        sinks = [v for v in range(n) if all(u != v for u, _ in edges)]
+        exp_end = min(sinks, key=lambda v: (F32(F32(T) - at_b[v]), v))
+        assert path[0] == exp_end, trial
+        assert all(v != path[-1] for _, v in edges), trial          # ends at a source
+        # some choice of parallel edges along the node path attains at_b[endpoint]
+        hops = list(zip(path[1:], path[:-1]))                       # (u, v), source-ward
+        choices = [[d[k] for k, (u, v) in enumerate(edges) if (u, v) == h] for h in hops]
+        assert all(choices), trial
+        best = None
+        for combo in itertools.product(*choices[::-1]):             # source -> endpoint
+            x = F32(at_src[path[-1]]) if at_src[path[-1]] != 0 else F32(0.0)
+            for dk in combo:
+                x = F32(x + F32(dk))
+            best = x if best is None else max(best, x)
+        assert best == at_b[path[0]], trial
+
+
+def test_p11_critical_path_chain():
+    g = hfgen.chain(3000, seed=5, relabel=True)
+    src, dst = g.edges()
+    nxt = np.full(g.n, -1, np.int64)
+    nxt[src] = dst
+    head = int(np.setdiff1d(np.arange(g.n), dst)[0])
+    walk = [head]
+    while nxt[walk[-1]] >= 0:
+        walk.append(int(nxt[walk[-1]]))
+    at = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), None)
+    path = oracle.critical_path(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), at, 1e6)
+    assert path.tolist() == walk[::-1]     # the whole chain, endpoint first
