@@ -164,6 +164,29 @@ hf_status hf_run_batch_d(hf_graph g, int32_t s_local, const float *delays_d, int
                          const float *t_req_d, const float *at_src_d, float *wns_local_d,
                          float *at_d, float *rat_d, void *nccl_comm, float *wns_all_d);
 
+/* NEXT-1: critical-path trace-back (PAPER.md:1002-1003
+ * "extract graph information (critical paths, ...)"; reading R17).
+ * Per scenario s: the endpoint is the sink (out-degree 0) with the smallest slack
+ * fl(T_s - at_s[sink]), ties by the smallest node id; from it the path steps to the
+ * source of the fan-in edge e attaining the max, fl(at_s[src e] + d_s[e]) == at_s[v],
+ * ties by the smallest fan-in edge id, until a source (in-degree 0).
+ * path[s*max_len + i]: i-th node from the endpoint (endpoint first, source last).
+ *
+ * hf_critical_path_d: device pointers, stream-ordered.  delays [m][S] in fan-in
+ *   edge order (NULL: the graph's own delays, S must be 1); at [n][S] must be the
+ *   forward result of those delays (hf_propagate_forward_d / hf_run_batch_d with
+ *   at output); t_req [S] or NULL (t_scalar for all); path [S][max_len];
+ *   path_len [S] receives the length, or -1 when at is not a forward result of the
+ *   delays or the path is longer than max_len (max_len >= number of levels is
+ *   always enough).  The graph need not be levelized.
+ * hf_critical_path: host pointers, one delay set (the graph's), synchronous;
+ *   HF_ERR_INVALID_ARG when path_len would be -1. */
+hf_status hf_critical_path_d(hf_graph g, int32_t S, const float *delays, const float *at,
+                             const float *t_req, float t_scalar, int32_t max_len,
+                             int32_t *path, int32_t *path_len);
+hf_status hf_critical_path(hf_graph g, const float *at, float t_req, int32_t max_len,
+                           int32_t *path, int32_t *path_len);
+
 /* NCCL bootstrap (libnccl.so.2 is loaded on first use).  Rank 0 calls
  * hf_nccl_unique_id and broadcasts the 128 bytes (e.g. over torch.distributed);
  * every rank then calls hf_nccl_comm_init with its rank on its device. */

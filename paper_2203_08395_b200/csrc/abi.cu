@@ -26,6 +26,9 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
 void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                   const float *t_arr, float *at, float *rat, float *slack, float *wns_f);
 void profile_mark(Graph &g, int idx);
+void critical_path_device(Graph &g, int32_t S, const float *d, const float *at,
+                          const float *t_arr, float t_scalar, int32_t max_len, int32_t *path,
+                          int32_t *len);
 
 // ---- NCCL through dlopen (no link-time dependency) -------------------------
 namespace nccl {
@@ -597,6 +600,52 @@ hf_status hf_profile_read(hf_graph h, float *ms_levelize, float *ms_forward, flo
         if (ms_forward) *ms_forward = g->ms_fwd;
         if (ms_backward) *ms_backward = g->ms_bwd;
         if (kernel_launches) *kernel_launches = g->launches;
+        return HF_OK;
+    });
+}
+
+hf_status hf_critical_path_d(hf_graph h, int32_t S, const float *delays_d, const float *at_d,
+                             const float *t_req_d, float t_scalar, int32_t max_len,
+                             int32_t *path_d, int32_t *path_len_d) {
+    return guarded([&]() -> hf_status {
+        if (!h || !at_d || !path_d || !path_len_d)
+            fail(HF_ERR_INVALID_ARG, "graph, at, path or path_len is NULL");
+        if (S < 1 || max_len < 1) fail(HF_ERR_INVALID_ARG, "S and max_len must be >= 1");
+        Graph *g = G(h);
+        DeviceGuard dg(g->device);
+        if (!delays_d && S != 1) fail(HF_ERR_INVALID_ARG, "graph delays need S == 1");
+        critical_path_device(*g, S, delays_d ? delays_d : g->delay.as<float>(), at_d, t_req_d,
+                             t_scalar, max_len, path_d, path_len_d);
+        return HF_OK;
+    });
+}
+
+hf_status hf_critical_path(hf_graph h, const float *at, float t_req, int32_t max_len,
+                           int32_t *path, int32_t *path_len) {
+    return guarded([&]() -> hf_status {
+        if (!h || !at || !path || !path_len)
+            fail(HF_ERR_INVALID_ARG, "graph, at, path or path_len is NULL");
+        if (max_len < 1) fail(HF_ERR_INVALID_ARG, "max_len must be >= 1");
+        if (!std::isfinite(t_req)) fail(HF_ERR_INVALID_ARG, "t_req is not finite");
+        Graph *g = G(h);
+        DeviceGuard dg(g->device);
+        cudaStream_t s = g->stream;
+        DevBuf a, p, l;
+        a.alloc(sizeof(float) * size_t(g->n > 0 ? g->n : 1), s);
+        p.alloc(sizeof(int32_t) * size_t(max_len), s);
+        l.alloc(sizeof(int32_t), s);
+        if (g->n)
+            HF_CUDA(cudaMemcpyAsync(a.p, at, sizeof(float) * g->n, cudaMemcpyHostToDevice, s));
+        critical_path_device(*g, 1, g->delay.as<float>(), a.as<float>(), nullptr, t_req, max_len,
+                             p.as<int32_t>(), l.as<int32_t>());
+        int32_t ln = 0;
+        HF_CUDA(cudaMemcpyAsync(&ln, l.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
+        if (ln < 0) fail(HF_ERR_INVALID_ARG, "at is not a forward result of the graph's delays, "
+                                             "or the critical path is longer than max_len");
+        if (ln)
+            HF_CUDA(cudaMemcpy(path, p.p, sizeof(int32_t) * size_t(ln), cudaMemcpyDeviceToHost));
+        *path_len = ln;
         return HF_OK;
     });
 }

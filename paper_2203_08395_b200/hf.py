@@ -29,7 +29,7 @@ EXPORTS = [
     "hf_levelize_d", "hf_propagate_forward", "hf_propagate_forward_d", "hf_propagate_backward",
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
-    "hf_profile_read_batch",
+    "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d",
 ]
 
 
@@ -70,6 +70,8 @@ def _load() -> ctypes.CDLL:
         "hf_profile_enable": (c_int, [P, c_int]),
         "hf_profile_read": (c_int, [P, P, P, P, P]),
         "hf_profile_read_batch": (c_int, [P, P]),
+        "hf_critical_path_d": (c_int, [P, i32, P, P, P, f32, i32, P, P]),
+        "hf_critical_path": (c_int, [P, P, f32, i32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -219,6 +221,28 @@ def hf_propagate_backward(g: Graph, t_req: float, at, rat, slack=None, wns=None)
         a = _np(at, np.float32)
         _check(_lib.hf_propagate_backward(g.handle, ctypes.c_float(t_req), _ptr(a), _ptr(rat),
                                           _ptr(slack), _ptr(wns)))
+
+
+def hf_critical_path(g: Graph, at, t_req, max_len: int, path=None, path_len=None,
+                     delays=None, s: int = 1):
+    """NEXT-1 critical path of the worst endpoint (reading R17).
+
+    Host: at (numpy [n]) with the graph's delays -> numpy array of node ids (endpoint
+    first).  Device: at [n][S] CUDA tensor, delays [m][S] tensor (or None for the graph's
+    delays, s == 1), t_req [S] tensor or float, path [S][max_len] and path_len [S] int32
+    tensors (stream-ordered; path_len -1 marks an inconsistent at)."""
+    if _is_torch(at):
+        tr = t_req if _is_torch(t_req) else None
+        ts = 0.0 if _is_torch(t_req) else float(t_req)
+        _check(_lib.hf_critical_path_d(g.handle, s, _ptr(delays), _ptr(at), _ptr(tr),
+                                       ctypes.c_float(ts), max_len, _ptr(path), _ptr(path_len)))
+        return path, path_len
+    a = _np(at, np.float32)
+    out = np.zeros(max(1, max_len), np.int32)
+    ln = ctypes.c_int32(0)
+    _check(_lib.hf_critical_path(g.handle, _ptr(a), ctypes.c_float(t_req), max_len, _ptr(out),
+                                 ctypes.byref(ln)))
+    return out[:ln.value].copy()
 
 
 def hf_run_batch(g: Graph, s_local: int, delays, layout: int, t_req, at_src, wns_local,

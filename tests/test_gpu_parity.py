@@ -379,3 +379,77 @@ def test_batch_nccl_gather_single_rank(hf):
         G.close()
     finally:
         hf.hf_nccl_comm_destroy(comm)
+
+
+# ---- NEXT-1: critical-path trace-back (reading R17) -----------------------------------
+def test_critical_path_single_graph(hf):
+    g = hfgen.config("C1")
+    G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=g.delay)
+    L = hf.hf_levelize(G)
+    at = np.zeros(g.n, F32)
+    hf.hf_propagate_forward(G, g.at_src, at)
+    path = hf.hf_critical_path(G, at, g.t_req, L)
+    at_o = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src)
+    assert_bits_equal(at, at_o, "at")
+    exp = oracle.critical_path(g.n, g.m, g.in_ptr, g.in_src, g.delay, at_o, g.t_req)
+    assert path.tolist() == exp.tolist()
+    # an `at` that is not a forward result is rejected, not traced
+    bad = at.copy()
+    bad[exp[0]] += 1.0
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_critical_path(G, bad, g.t_req, L)
+    assert ei.value.status == hf.HF_ERR_INVALID_ARG
+    G.close()
+
+
+def test_critical_path_integer_ties_tiny(hf):
+    rng = np.random.default_rng(311)
+    for trial in range(60):
+        n, edges = random_tiny_dag(rng, nmax=12, p=0.5)
+        m = len(edges)
+        in_ptr, in_src, _ = csr_from_edges(n, edges)
+        d = rng.integers(1, 4, size=m).astype(F32)
+        a_src = rng.integers(0, 3, size=n).astype(F32)
+        G = hf.hf_graph_create(n, m, in_ptr, in_src, delay=d)
+        L = hf.hf_levelize(G)
+        at = np.zeros(max(n, 1), F32)
+        hf.hf_propagate_forward(G, a_src, at)
+        path = hf.hf_critical_path(G, at[:n], 30.0, max(L, 1))
+        at_o = oracle.forward(n, m, in_ptr, in_src, d, a_src)
+        exp = oracle.critical_path(n, m, in_ptr, in_src, d, at_o, 30.0)
+        assert path.tolist() == exp.tolist(), trial
+        G.close()
+
+
+@pytest.mark.parametrize("name,scale,S", [("C3", 0.004, 8), ("C3", 0.004, 64), ("C3", 1.0, 4)])
+def test_critical_path_batch_device(hf, name, scale, S):
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.config(name, scale)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[1::3] -= 7.0
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    L = hf.hf_levelize(G)
+    d = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
+    t = torch.from_numpy(T).to(dev)
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    at = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    rat = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    hf.hf_run_batch(G, S, d, hf.HF_LAYOUT_MS, t, torch.from_numpy(g.at_src).to(dev), w, at=at, rat=rat)
+    path = torch.full((S, L), -7, dtype=torch.int32, device=dev)
+    plen = torch.empty(S, dtype=torch.int32, device=dev)
+    hf.hf_critical_path(G, at, t, L, path, plen, delays=d, s=S)
+    hf.hf_sync(G)
+    at_h = at.cpu().numpy().reshape(g.n, S)
+    _, at_o, _ = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                              want_at_rat=True)
+    assert_bits_equal(at_h, at_o, "at")
+    exp = oracle.critical_paths(g.n, g.m, g.in_ptr, g.in_src, D, at_o, T, max_len=L)
+    got_p, got_l = path.cpu().numpy(), plen.cpu().numpy()
+    for s in range(S):
+        assert got_l[s] == len(exp[s]), s
+        assert got_p[s, :got_l[s]].tolist() == exp[s].tolist(), s
+    G.close()
