@@ -56,6 +56,11 @@ def _load():
         lib.oracle_check_fanout.argtypes = [i32, i32, P, P, P, P]
         lib.oracle_levelize.argtypes = [i32, i32, P, P, P, P, P, P, P, P, P]
         lib.oracle_forward.argtypes = [i32, i32, P, P, P, P, P, P]
+        lib.oracle_forward_mode.argtypes = [i32, i32, P, P, P, P, P, P, ctypes.c_int]
+        lib.oracle_backward_mode.argtypes = [i32, i32, P, P, P, ctypes.c_float, P, P, P, P, P,
+                                             ctypes.c_int]
+        lib.oracle_batch_mode.argtypes = [i32, i32, P, P, i32, P, ctypes.c_int, P, P, P, P, P,
+                                          ctypes.c_int, ctypes.c_int]
         lib.oracle_backward.argtypes = [i32, i32, P, P, P, ctypes.c_float, P, P, P, P, P]
         lib.oracle_batch.argtypes = [i32, i32, P, P, i32, P, ctypes.c_int, P, P, P, P, P,
                                      ctypes.c_int]
@@ -64,7 +69,8 @@ def _load():
         lib.oracle_critical_paths.argtypes = [i32, i32, P, P, i32, P, P, P, P, i32, P]
         for f in (lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
                   lib.oracle_forward, lib.oracle_backward, lib.oracle_batch,
-                  lib.oracle_critical_path, lib.oracle_critical_paths):
+                  lib.oracle_critical_path, lib.oracle_critical_paths, lib.oracle_forward_mode,
+                  lib.oracle_backward_mode, lib.oracle_batch_mode):
             f.restype = ctypes.c_int
         lib.oracle_fanout.restype = None
         _lib = lib
@@ -138,22 +144,27 @@ def levelize(n, m, in_ptr, in_src) -> Levels:
                   topo[:n].copy(), L.value)
 
 
-def forward(n, m, in_ptr, in_src, delay, at_src=None, lv: Optional[Levels] = None):
-    """at[n] = max-plus arrival times (at_src None => +0 at sources; delay None => +0)."""
+def forward(n, m, in_ptr, in_src, delay, at_src=None, lv: Optional[Levels] = None,
+            early: bool = False):
+    """at[n] = max-plus arrival times (at_src None => +0 at sources; delay None => +0);
+    early=True: min-plus (hold-analysis arrival, NEXT-2, reading R18)."""
     lib = _load()
     in_ptr, in_src = _i32(in_ptr), _i32(in_src)
     lv = lv or levelize(n, m, in_ptr, in_src)
     d = None if delay is None else _f32(delay)
     a = None if at_src is None else _f32(at_src)
     at = np.zeros(max(n, 1), np.float32)
-    rc = lib.oracle_forward(n, m, _p(in_ptr), _p(in_src), _p(d), _p(a), _p(lv.topo), _p(at))
+    rc = lib.oracle_forward_mode(n, m, _p(in_ptr), _p(in_src), _p(d), _p(a), _p(lv.topo),
+                                 _p(at), int(early))
     if rc:
         raise OracleError(rc)
     return at[:n]
 
 
-def backward(n, m, in_ptr, in_src, delay, t_req, at, lv: Optional[Levels] = None):
-    """(rat[n], slack[n], wns) by min-plus over fan-out; T at every sink."""
+def backward(n, m, in_ptr, in_src, delay, t_req, at, lv: Optional[Levels] = None,
+             early: bool = False):
+    """(rat[n], slack[n], wns) by min-plus over fan-out; T at every sink.
+    early=True: max-plus, slack = at - rat (hold mode, NEXT-2, reading R18)."""
     lib = _load()
     in_ptr, in_src = _i32(in_ptr), _i32(in_src)
     lv = lv or levelize(n, m, in_ptr, in_src)
@@ -162,15 +173,16 @@ def backward(n, m, in_ptr, in_src, delay, t_req, at, lv: Optional[Levels] = None
     rat = np.zeros(max(n, 1), np.float32)
     slack = np.zeros(max(n, 1), np.float32)
     wns = ctypes.c_float(0.0)
-    rc = lib.oracle_backward(n, m, _p(in_ptr), _p(in_src), _p(d), ctypes.c_float(t_req),
-                             _p(lv.topo), _p(at), _p(rat), _p(slack), ctypes.byref(wns))
+    rc = lib.oracle_backward_mode(n, m, _p(in_ptr), _p(in_src), _p(d), ctypes.c_float(t_req),
+                                  _p(lv.topo), _p(at), _p(rat), _p(slack), ctypes.byref(wns),
+                                  int(early))
     if rc:
         raise OracleError(rc)
     return rat[:n], slack[:n], np.float32(wns.value)
 
 
 def batch(n, m, in_ptr, in_src, delays, t_req, at_src=None, layout: str = "ms",
-          threads: int = 1, want_at_rat: bool = False):
+          threads: int = 1, want_at_rat: bool = False, early: bool = False):
     """S scenarios: delays [m][S] ("ms") or [S][m] ("sm"); t_req[S].
     Returns wns[S] (and at[n][S], rat[n][S] if want_at_rat)."""
     lib = _load()
@@ -182,9 +194,9 @@ def batch(n, m, in_ptr, in_src, delays, t_req, at_src=None, layout: str = "ms",
     wns = np.zeros(max(S, 1), np.float32)
     at_all = np.zeros((n, S), np.float32) if want_at_rat else None
     rat_all = np.zeros((n, S), np.float32) if want_at_rat else None
-    rc = lib.oracle_batch(n, m, _p(in_ptr), _p(in_src), S, _p(delays),
-                          0 if layout == "sm" else 1, _p(t), _p(a), _p(wns), _p(at_all),
-                          _p(rat_all), threads)
+    rc = lib.oracle_batch_mode(n, m, _p(in_ptr), _p(in_src), S, _p(delays),
+                               0 if layout == "sm" else 1, _p(t), _p(a), _p(wns), _p(at_all),
+                               _p(rat_all), threads, int(early))
     if rc:
         raise OracleError(rc)
     if want_at_rat:

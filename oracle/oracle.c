@@ -22,6 +22,8 @@
  *   - slack = fl(rat - at), wns = min slack                  BASELINE.json:5; reading R4
  *   - batched what-if scenarios = independent delay sets     PAPER.md:969-980; BASELINE.json:10
  *   - critical path of the worst endpoint (argmax trace-back) PAPER.md:1002-1003; reading R17
+ *   - early (hold) mode: min-plus forward, max-plus backward, slack = at - rat
+ *                                                           PAPER.md:972-974 ("analysis mode"); reading R18
  *
  * Every function is a direct transcription of SURVEY.md §8(c)'s pseudo-code:
  * FIFO Kahn, then one sequential sweep over the topological order.  Status
@@ -152,12 +154,13 @@ int oracle_levelize(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *
     return rc;
 }
 
-/* Forward max-plus over the topological order.  at_src may be NULL (=> +0).
- * delay[m] indexed by fan-in position; stride = distance between consecutive
- * edges' delays (1 for a single delay set, S for the [m][S] layout). */
+/* Forward max-plus (late mode) or min-plus (early mode, NEXT-2) over the
+ * topological order.  at_src may be NULL (=> +0).  delay[m] indexed by fan-in
+ * position; stride = distance between consecutive edges' delays (1 for a single
+ * delay set, S for the [m][S] layout). */
 static void forward_pass(int32_t n, const int32_t *in_ptr, const int32_t *in_src,
                          const float *delay, int64_t stride, const float *at_src,
-                         const int32_t *topo, float *at) {
+                         const int32_t *topo, float *at, int early) {
     for (int32_t i = 0; i < n; ++i) {
         int32_t v = topo[i];
         if (in_ptr[v + 1] == in_ptr[v]) {
@@ -167,17 +170,18 @@ static void forward_pass(int32_t n, const int32_t *in_ptr, const int32_t *in_src
         float best = 0.0f;
         for (int32_t e = in_ptr[v]; e < in_ptr[v + 1]; ++e) {
             float x = at[in_src[e]] + canon(delay[(int64_t)e * stride]);
-            if (e == in_ptr[v] || x > best) best = x;     /* '>' keeps first */
+            if (e == in_ptr[v] || (early ? x < best : x > best)) best = x;   /* keeps first */
         }
         at[v] = best;
     }
 }
 
-/* Backward min-plus over the reversed topological order, then slack and WNS. */
+/* Backward min-plus (late) or max-plus (early) over the reversed topological
+ * order, then slack (late: rat - at; early / hold: at - rat) and its minimum. */
 static float backward_pass(int32_t n, const int32_t *out_ptr, const int32_t *out_dst,
                            const int32_t *out_eid, const float *delay, int64_t stride,
                            float t_req, const int32_t *topo, const float *at, float *rat,
-                           float *slack) {
+                           float *slack, int early) {
     float T = canon(t_req);
     for (int32_t i = n - 1; i >= 0; --i) {
         int32_t u = topo[i];
@@ -188,13 +192,13 @@ static float backward_pass(int32_t n, const int32_t *out_ptr, const int32_t *out
         float best = 0.0f;
         for (int32_t k = out_ptr[u]; k < out_ptr[u + 1]; ++k) {
             float x = rat[out_dst[k]] - canon(delay[(int64_t)out_eid[k] * stride]);
-            if (k == out_ptr[u] || x < best) best = x;
+            if (k == out_ptr[u] || (early ? x > best : x < best)) best = x;
         }
         rat[u] = best;
     }
     float wns = INFINITY;
     for (int32_t v = 0; v < n; ++v) {
-        float s = rat[v] - at[v];
+        float s = early ? at[v] - rat[v] : rat[v] - at[v];
         if (slack) slack[v] = s;
         if (s < wns) wns = s;
     }
@@ -207,25 +211,30 @@ static int all_finite(const float *x, int64_t count) {
     return 1;
 }
 
-/* Single-graph forward: at[n]. */
-int oracle_forward(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
-                   const float *delay, const float *at_src, const int32_t *topo, float *at) {
+/* Single-graph forward: at[n] (early != 0: min-plus, the hold-analysis arrival). */
+int oracle_forward_mode(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                        const float *delay, const float *at_src, const int32_t *topo, float *at,
+                        int early) {
     if (delay && !all_finite(delay, m)) return OR_INVALID;
     if (at_src && !all_finite(at_src, n)) return OR_INVALID;
     static const float zero = 0.0f;
     if (!delay) {
         /* NULL delays => +0 on every edge */
-        forward_pass(n, in_ptr, in_src, &zero, 0, at_src, topo, at);
+        forward_pass(n, in_ptr, in_src, &zero, 0, at_src, topo, at, early);
         return OR_OK;
     }
-    forward_pass(n, in_ptr, in_src, delay, 1, at_src, topo, at);
+    forward_pass(n, in_ptr, in_src, delay, 1, at_src, topo, at, early);
     return OR_OK;
 }
+int oracle_forward(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                   const float *delay, const float *at_src, const int32_t *topo, float *at) {
+    return oracle_forward_mode(n, m, in_ptr, in_src, delay, at_src, topo, at, 0);
+}
 
-/* Single-graph backward: rat[n], slack[n] (nullable), *wns. */
-int oracle_backward(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
-                    const float *delay, float t_req, const int32_t *topo, const float *at,
-                    float *rat, float *slack, float *wns) {
+/* Single-graph backward: rat[n], slack[n] (nullable), *wns (early: hold mode). */
+int oracle_backward_mode(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                         const float *delay, float t_req, const int32_t *topo, const float *at,
+                         float *rat, float *slack, float *wns, int early) {
     if (delay && !all_finite(delay, m)) return OR_INVALID;
     if (!isfinite(t_req)) return OR_INVALID;
     int32_t *out_ptr = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
@@ -234,10 +243,15 @@ int oracle_backward(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *
     oracle_fanout(n, m, in_ptr, in_src, out_ptr, out_dst, out_eid);
     static const float zero = 0.0f;
     float w = backward_pass(n, out_ptr, out_dst, out_eid, delay ? delay : &zero,
-                            delay ? 1 : 0, t_req, topo, at, rat, slack);
+                            delay ? 1 : 0, t_req, topo, at, rat, slack, early);
     if (wns) *wns = w;
     free(out_ptr); free(out_dst); free(out_eid);
     return OR_OK;
+}
+int oracle_backward(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                    const float *delay, float t_req, const int32_t *topo, const float *at,
+                    float *rat, float *slack, float *wns) {
+    return oracle_backward_mode(n, m, in_ptr, in_src, delay, t_req, topo, at, rat, slack, wns, 0);
 }
 
 /* ---- batched scenarios: the same passes per delay set --------------------- */
@@ -246,6 +260,7 @@ typedef struct {
     const int32_t *in_ptr, *in_src, *out_ptr, *out_dst, *out_eid, *topo;
     const float *delays, *t_req, *at_src;
     int layout;              /* 0: [S][m]; 1: [m][S] */
+    int early;               /* NEXT-2 hold mode */
     float *wns, *at_all, *rat_all;   /* at_all/rat_all: [n][S] or NULL */
     int32_t next;            /* next scenario (guarded by mu) */
     pthread_mutex_t mu;
@@ -262,9 +277,9 @@ static void *batch_worker(void *arg) {
         if (s >= J->S) break;
         const float *d = J->layout == 0 ? J->delays + (int64_t)s * J->m : J->delays + s;
         int64_t stride = J->layout == 0 ? 1 : J->S;
-        forward_pass(J->n, J->in_ptr, J->in_src, d, stride, J->at_src, J->topo, at);
+        forward_pass(J->n, J->in_ptr, J->in_src, d, stride, J->at_src, J->topo, at, J->early);
         J->wns[s] = backward_pass(J->n, J->out_ptr, J->out_dst, J->out_eid, d, stride,
-                                  J->t_req[s], J->topo, at, rat, NULL);
+                                  J->t_req[s], J->topo, at, rat, NULL, J->early);
         if (J->at_all)
             for (int32_t v = 0; v < J->n; ++v) J->at_all[(int64_t)v * J->S + s] = at[v];
         if (J->rat_all)
@@ -277,9 +292,10 @@ static void *batch_worker(void *arg) {
 /* S scenarios over one graph: wns[S] (+ optional at_all/rat_all [n][S]).
  * threads > 1 only splits scenarios across pthreads (timing); results do not
  * depend on it. */
-int oracle_batch(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
-                 int32_t S, const float *delays, int layout, const float *t_req,
-                 const float *at_src, float *wns, float *at_all, float *rat_all, int threads) {
+int oracle_batch_mode(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                      int32_t S, const float *delays, int layout, const float *t_req,
+                      const float *at_src, float *wns, float *at_all, float *rat_all, int threads,
+                      int early) {
     int rc = oracle_check_csr(n, m, in_ptr, in_src);
     if (rc) return rc;
     if (!all_finite(delays, (int64_t)m * S) || !all_finite(t_req, S)) return OR_INVALID;
@@ -299,7 +315,7 @@ int oracle_batch(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_
     J.n = n; J.m = m; J.S = S; J.in_ptr = in_ptr; J.in_src = in_src;
     J.out_ptr = out_ptr; J.out_dst = out_dst; J.out_eid = out_eid; J.topo = topo;
     J.delays = delays; J.t_req = t_req; J.at_src = at_src; J.layout = layout;
-    J.wns = wns; J.at_all = at_all; J.rat_all = rat_all; J.next = 0;
+    J.wns = wns; J.at_all = at_all; J.rat_all = rat_all; J.next = 0; J.early = early;
     pthread_mutex_init(&J.mu, NULL);
     if (threads < 1) threads = 1;
     if (threads > S) threads = S > 0 ? S : 1;
@@ -311,6 +327,12 @@ int oracle_batch(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_
     free(th); free(topo); free(level); free(lptr); free(order);
     free(out_ptr); free(out_dst); free(out_eid);
     return OR_OK;
+}
+int oracle_batch(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                 int32_t S, const float *delays, int layout, const float *t_req,
+                 const float *at_src, float *wns, float *at_all, float *rat_all, int threads) {
+    return oracle_batch_mode(n, m, in_ptr, in_src, S, delays, layout, t_req, at_src, wns, at_all,
+                             rat_all, threads, 0);
 }
 
 /* ---- NEXT-1: critical-path trace-back -------------------

@@ -89,8 +89,9 @@ def brute_paths(n, edges_with_delay):
     return [paths_to(v) for v in range(n)]
 
 
-def brute_forward(n, edges_with_delay, at_src):
-    """at[v] = max over source->v paths of the left-to-right fp32 path sum (P6)."""
+def brute_forward(n, edges_with_delay, at_src, early=False):
+    """at[v] = max (early: min) over source->v paths of the left-to-right fp32 path
+    sum (P6, P12)."""
     allp = brute_paths(n, edges_with_delay)
     at = np.zeros(n, F32)
     level = np.zeros(n, np.int64)
@@ -103,15 +104,16 @@ def brute_forward(n, edges_with_delay, at_src):
                 x = F32(0.0)
             for k in p:
                 x = F32(x + F32(edges_with_delay[k][2]))
-            if best is None or x > best:
+            if best is None or (x < best if early else x > best):
                 best = x
         at[v] = best
         level[v] = max(len(p) for p in allp[v])
     return at, level
 
 
-def brute_backward(n, edges_with_delay, T):
-    """rat[u] = min over u->sink paths of fp32 differences applied from the sink (P6)."""
+def brute_backward(n, edges_with_delay, T, early=False):
+    """rat[u] = min (early: max) over u->sink paths of fp32 differences applied from
+    the sink (P6, P12)."""
     outs = [[] for _ in range(n)]
     for k, (u, v, _) in enumerate(edges_with_delay):
         outs[u].append(k)
@@ -137,7 +139,7 @@ def brute_backward(n, edges_with_delay, T):
             x = F32(T)
             for k in reversed(p):
                 x = F32(x - F32(edges_with_delay[k][2]))
-            if best is None or x < best:
+            if best is None or (x > best if early else x < best):
                 best = x
         rat[u] = best
     return rat

@@ -424,3 +424,61 @@ def test_p11_critical_path_chain():
     at = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), None)
     path = oracle.critical_path(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), at, 1e6)
     assert path.tolist() == walk[::-1]     # the whole chain, endpoint first
+
+
+# ---- P12: early (hold) mode -- min-plus forward, max-plus backward (NEXT-2, R18) ----
+def test_p12_early_mode_bruteforce_tiny_dags():
+    rng = np.random.default_rng(1203)
+    for trial in range(800):
+        n, edges = random_tiny_dag(rng)
+        m = len(edges)
+        d = mixed_delays(rng, m)
+        at_src = mixed_delays(rng, n)
+        T = float(mixed_delays(rng, 1)[0])
+        in_ptr, in_src, perm = csr_from_edges(n, edges)
+        ewd = [(u, v, d[k]) for k, (u, v) in enumerate(edges)]
+        at_b, _ = brute_forward(n, ewd, at_src, early=True)
+        rat_b = brute_backward(n, ewd, T, early=True)
+        at = oracle.forward(n, m, in_ptr, in_src, d[perm], at_src, early=True)
+        assert np.array_equal(at.view(np.uint32), at_b.view(np.uint32)), trial
+        rat, slack, wns = oracle.backward(n, m, in_ptr, in_src, d[perm], T, at, early=True)
+        assert np.array_equal(rat.view(np.uint32), rat_b.view(np.uint32)), trial
+        s_b = (at_b - rat_b).astype(F32)                       # hold slack = at - rat
+        assert np.array_equal(slack.view(np.uint32), s_b.view(np.uint32)), trial
+        assert wns == s_b.min()
+
+
+def test_p12_early_late_duality():
+    # min(x) = -max(-x) and round-to-nearest is sign-symmetric, so the early passes
+    # on (d, at_src, T) are the negated late passes on (-d, -at_src, -T), exactly
+    g = hfgen.config("C1")
+    lv = oracle.levelize(g.n, g.m, g.in_ptr, g.in_src)
+    a_e = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, lv, early=True)
+    a_l = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, -g.delay, -g.at_src, lv)
+    assert np.array_equal(a_e, -a_l)
+    r_e, s_e, w_e = oracle.backward(g.n, g.m, g.in_ptr, g.in_src, g.delay, g.t_req, a_e, lv,
+                                    early=True)
+    r_l, s_l, w_l = oracle.backward(g.n, g.m, g.in_ptr, g.in_src, -g.delay, -g.t_req, a_l, lv)
+    assert np.array_equal(r_e, -r_l)
+    assert np.array_equal(s_e, s_l)                            # fl(at - rat) = fl(rat_l - at_l)
+    assert w_e == w_l
+    # and the two modes differ on this graph (a dropped mode switch fails here)
+    a_late = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, lv)
+    assert (a_e < a_late).any() and (a_e <= a_late).all()
+
+
+def test_p12_early_unit_delay_is_bfs_distance():
+    g = hfgen.config("C3", 0.01)
+    src, dst = g.edges()
+    # shortest number of edges from any source: plain BFS fixpoint over the edge list
+    indeg = np.bincount(dst, minlength=g.n)
+    dist = np.where(indeg == 0, 0, np.iinfo(np.int64).max // 2)
+    while True:
+        cand = np.full(g.n, np.iinfo(np.int64).max // 2)
+        np.minimum.at(cand, dst, dist[src] + 1)
+        new = np.where(indeg == 0, 0, cand)
+        if np.array_equal(new, dist):
+            break
+        dist = new
+    at = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), None, early=True)
+    assert np.array_equal(at, dist.astype(F32))
