@@ -93,6 +93,18 @@ hf_status hf_graph_create_d(int32_t n, int32_t m, const int32_t *fanin_ptr_d,
 hf_status hf_graph_destroy(hf_graph g);
 /* Re-target the graph's work to another stream on the same device. */
 hf_status hf_graph_set_stream(hf_graph g, void *cuda_stream);
+/* Analysis mode of the propagation calls that follow (NEXT-2, SURVEY.md §8(f);
+ * PAPER.md:972-974 "analysis mode"; reading R18).  HF_MODE_LATE (default,
+ * setup analysis): at = max-plus over fan-in, rat = min-plus over fan-out, slack =
+ * fl(rat - at).  HF_MODE_EARLY (hold analysis): at = min over fan-in of
+ * fl(at[u] + d), rat = max over fan-out of fl(rat[v] - d) (T at sinks), slack =
+ * fl(at - rat); wns is the minimum slack in both modes.  Affects
+ * hf_propagate_forward/backward[_d] and hf_run_batch[_d]; hf_critical_path[_d] is
+ * defined for late mode only (HF_ERR_INVALID_ARG in early mode).  mode other than
+ * 0/1 -> HF_ERR_INVALID_ARG. */
+#define HF_MODE_LATE 0
+#define HF_MODE_EARLY 1
+hf_status hf_graph_set_mode(hf_graph g, int mode);
 /* n, m and (after hf_levelize) the number of levels L; any pointer may be NULL.
  * num_levels = -1 while not levelized. */
 hf_status hf_graph_info(hf_graph g, int32_t *n, int32_t *m, int32_t *num_levels);

@@ -264,6 +264,16 @@ hf_status hf_graph_set_stream(hf_graph h, void *stream) {
     });
 }
 
+hf_status hf_graph_set_mode(hf_graph h, int mode) {
+    return guarded([&]() -> hf_status {
+        if (!h) fail(HF_ERR_INVALID_ARG, "graph is NULL");
+        if (mode != HF_MODE_LATE && mode != HF_MODE_EARLY)
+            fail(HF_ERR_INVALID_ARG, "mode must be HF_MODE_LATE or HF_MODE_EARLY");
+        G(h)->early = mode == HF_MODE_EARLY;
+        return HF_OK;
+    });
+}
+
 hf_status hf_graph_info(hf_graph h, int32_t *n, int32_t *m, int32_t *num_levels) {
     return guarded([&]() -> hf_status {
         if (!h) fail(HF_ERR_INVALID_ARG, "graph is NULL");
@@ -613,6 +623,7 @@ hf_status hf_critical_path_d(hf_graph h, int32_t S, const float *delays_d, const
         if (S < 1 || max_len < 1) fail(HF_ERR_INVALID_ARG, "S and max_len must be >= 1");
         Graph *g = G(h);
         DeviceGuard dg(g->device);
+        if (g->early) fail(HF_ERR_INVALID_ARG, "the critical path is defined in late mode only");
         if (!delays_d && S != 1) fail(HF_ERR_INVALID_ARG, "graph delays need S == 1");
         critical_path_device(*g, S, delays_d ? delays_d : g->delay.as<float>(), at_d, t_req_d,
                              t_scalar, max_len, path_d, path_len_d);
@@ -629,6 +640,7 @@ hf_status hf_critical_path(hf_graph h, const float *at, float t_req, int32_t max
         if (!std::isfinite(t_req)) fail(HF_ERR_INVALID_ARG, "t_req is not finite");
         Graph *g = G(h);
         DeviceGuard dg(g->device);
+        if (g->early) fail(HF_ERR_INVALID_ARG, "the critical path is defined in late mode only");
         cudaStream_t s = g->stream;
         DevBuf a, p, l;
         a.alloc(sizeof(float) * size_t(g->n > 0 ? g->n : 1), s);

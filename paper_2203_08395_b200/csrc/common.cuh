@@ -98,6 +98,10 @@ struct Graph {
     // CSR fan-in (edge id = fan-in position), fan-out, per-edge data
     DevBuf in_ptr, in_src, in_dst, delay;
     DevBuf out_ptr, out_dst, out_eid;
+    // analysis mode (NEXT-2, reading R18): false = late (setup: max-plus forward,
+    // min-plus backward, slack rat - at); true = early (hold: min-plus forward,
+    // max-plus backward, slack at - rat)
+    bool early = false;
     // levelization
     bool levelized = false;
     int32_t L = -1;

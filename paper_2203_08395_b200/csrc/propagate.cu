@@ -210,8 +210,10 @@ template <int NSL> struct Idx {
 };
 template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA>
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
 __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
+    // MX: the pass combines with max (late forward, early backward), else min
+    constexpr bool MX = FWD != EARLY;
     constexpr int SC = V * LPN;   // columns per chunk
     constexpr int G = 32 / LPN;   // lane groups per warp
     constexpr int NSL = idx_slots<LPN>();
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     const int np = __ldg(p.part_np + q0);
                     Vec<V> acc;
 #pragma unroll
-                    for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+                    for (int j = 0; j < V; ++j) acc.x[j] = ident<MX>();
                     for (int kk = 0; kk < np; ++kk) {
                         const float *src = p.part_buf + int64_t(q0 + kk) * S + col;
                         Vec<V> v = ld_relaxed<V>(src);
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                             v = ld_relaxed<V>(src);
                         }
 #pragma unroll
-                        for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], v.x[j]);
+                        for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v.x[j]);
                     }
                     st_s<V>(s_a + k * SC + gl * V, acc);
                 }
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     const int q0 = -uu[r] - 1;
                     const int np = __ldg(p.part_np + q0);
 #pragma unroll
-                    for (int j = 0; j < V; ++j) a[r].x[j] = ident<FWD>();
+                    for (int j = 0; j < V; ++j) a[r].x[j] = ident<MX>();
                     for (int k = 0; k < np; ++k) {
                         const float *src = p.part_buf + int64_t(q0 + k) * S + col;
                         Vec<V> v = ld_relaxed<V>(src);
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                             v = ld_relaxed<V>(src);
                         }
 #pragma unroll
-                        for (int j = 0; j < V; ++j) a[r].x[j] = combine<FWD>(a[r].x[j], v.x[j]);
+                        for (int j = 0; j < V; ++j) a[r].x[j] = combine<MX>(a[r].x[j], v.x[j]);
                     }
                 }
             }
@@ -516,17 +518,17 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         if (part) {
             Vec<V> acc;
 #pragma unroll
-            for (int j = 0; j < V; ++j) acc.x[j] = ident<FWD>();
+            for (int j = 0; j < V; ++j) acc.x[j] = ident<MX>();
             for (int k = g; k < E; k += G) {   // the edges this group computed
                 const Vec<V> x = ld_s<V>(s_d + k * SC + gl * V);
 #pragma unroll
-                for (int j = 0; j < V; ++j) acc.x[j] = combine<FWD>(acc.x[j], x.x[j]);
+                for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], x.x[j]);
             }
 #pragma unroll
             for (int o = LPN; o < 32; o <<= 1)
 #pragma unroll
                 for (int j = 0; j < V; ++j)
-                    acc.x[j] = combine<FWD>(acc.x[j], __shfl_xor_sync(FULL, acc.x[j], o));
+                    acc.x[j] = combine<MX>(acc.x[j], __shfl_xor_sync(FULL, acc.x[j], o));
             if (g == 0) st_relaxed<V>(p.part_buf + int64_t(-dsc.y - 1) * S + col, acc);
         } else {
             if (!FWD && c != run_c) {
@@ -552,7 +554,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     for (int k = eb + 1; k < ee; ++k) {
                         const Vec<V> x = ld_s<V>(s_d + k * SC + gl * V);
 #pragma unroll
-                        for (int j = 0; j < V; ++j) best.x[j] = combine<FWD>(best.x[j], x.x[j]);
+                        for (int j = 0; j < V; ++j) best.x[j] = combine<MX>(best.x[j], x.x[j]);
                     }
                 }
                 st_relaxed<V>(p.out + int64_t(node) * S + col, best);
@@ -561,7 +563,9 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     Vec<V> sl;
 #pragma unroll
                     for (int j = 0; j < V; ++j) {
-                        sl.x[j] = __fsub_rn(best.x[j], av.x[j]);
+                        // late slack rat - at; early (hold) slack at - rat
+                        sl.x[j] = EARLY ? __fsub_rn(av.x[j], best.x[j])
+                                        : __fsub_rn(best.x[j], av.x[j]);
                         run.x[j] = fminf(run.x[j], sl.x[j]);
                     }
                     if (p.slack) st_plain<V>(p.slack + int64_t(node) * S + col, sl);
@@ -594,7 +598,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 // After a pass: every long row gets its value (combine of its partials), its
 // optional slack and its worst-slack contribution.  Rows with parts are found
 // from the part-id prefix q; one warp per such row.
-template <bool FWD>
+template <bool FWD, bool EARLY>
 __global__ void k_finalize_split(const int32_t *__restrict__ q, int32_t n,
                                  const int32_t *__restrict__ node_of, int32_t S,
                                  const float *__restrict__ part_buf, float *__restrict__ out,
@@ -615,10 +619,12 @@ __global__ void k_finalize_split(const int32_t *__restrict__ q, int32_t n,
             const int64_t node = node_of[r];
             for (int s = lane; s < S; s += 32) {
                 float v = part_buf[int64_t(qb) * S + s];
-                for (int k = 1; k < np; ++k) v = combine<FWD>(v, part_buf[int64_t(qb + k) * S + s]);
+                for (int k = 1; k < np; ++k)
+                    v = combine<FWD != EARLY>(v, part_buf[int64_t(qb + k) * S + s]);
                 out[node * S + s] = v;
                 if (!FWD && other) {
-                    const float sl = __fsub_rn(v, other[node * S + s]);
+                    const float sl = EARLY ? __fsub_rn(other[node * S + s], v)
+                                           : __fsub_rn(v, other[node * S + s]);
                     if (slack) slack[node * S + s] = sl;
                     atomicMin(wns_ord + s, f2ord(sl));
                 }
@@ -647,7 +653,7 @@ __global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err)
 // slack = fl(rat - at) for every node and scenario, the worst slack per scenario
 // (ordered-int atomicMin), optional slack store: the epilogue of the concurrent
 // batch, where the backward kernel runs next to the forward one and never sees at.
-template <int V>
+template <int V, bool EARLY>
 __global__ void k_slack_wns(const float *__restrict__ at, const float *__restrict__ rat,
                             float *__restrict__ slack, int32_t n, int32_t S,
                             int32_t *__restrict__ wns_ord) {
@@ -679,7 +685,7 @@ __global__ void k_slack_wns(const float *__restrict__ at, const float *__restric
             }
 #pragma unroll
             for (int j = 0; j < V; ++j) {
-                sl.x[j] = __fsub_rn(r.x[j], a.x[j]);
+                sl.x[j] = EARLY ? __fsub_rn(a.x[j], r.x[j]) : __fsub_rn(r.x[j], a.x[j]);
                 mn[j] = fminf(mn[j], sl.x[j]);
             }
             if (slack) st_plain<V>(slack + o, sl);
@@ -850,9 +856,9 @@ int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA>
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
 void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
-    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA>;
+    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA, EARLY>;
     constexpr int SC = V * LPN;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
@@ -888,8 +894,9 @@ void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
 }
 
 // blocks per SM a kernel can keep resident alone (cached occupancy query)
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA> int occupancy_of(FlowParams &p) {
-    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA>;
+template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
+int occupancy_of(FlowParams &p) {
+    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA, EARLY>;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, V * LPN, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
     static std::map<size_t, int> cache;
@@ -905,12 +912,12 @@ template <int V, int LPN, bool FWD, bool CHECK_D, bool GA> int occupancy_of(Flow
 }
 
 // op = 0: launch, op = 1: return the solo occupancy (blocks per SM)
-template <bool FWD, bool CHECK_D, bool GA>
+template <bool FWD, bool CHECK_D, bool GA, bool EARLY>
 int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int op) {
 #define HF_CASE(L)                                                               \
     case L:                                                                      \
-        if (op) return occupancy_of<4, L, FWD, CHECK_D, GA>(p);                  \
-        launch_flow<4, L, FWD, CHECK_D, GA>(g, p, st, cap);                      \
+        if (op) return occupancy_of<4, L, FWD, CHECK_D, GA, EARLY>(p);           \
+        launch_flow<4, L, FWD, CHECK_D, GA, EARLY>(g, p, st, cap);               \
         return 0;
     switch (LPN) {
         HF_CASE(16)
@@ -922,21 +929,28 @@ int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int 
     }
 #undef HF_CASE
 }
+template <bool FWD, bool CHECK_D, bool EARLY>
+int dispatch_mode(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st, int cap, int op) {
+    if (V == 4) {
+        // the cp.async-gather variant (HF_GA=1, measured slower) exists for late mode only
+        if (!EARLY && env_int("HF_GA", 0))
+            return dispatch_ga<FWD, CHECK_D, true, false>(g, p, LPN, st, cap, op);
+        return dispatch_ga<FWD, CHECK_D, false, EARLY>(g, p, LPN, st, cap, op);
+    } else if (V == 2) {
+        if (op) return occupancy_of<2, 1, FWD, CHECK_D, false, EARLY>(p);
+        launch_flow<2, 1, FWD, CHECK_D, false, EARLY>(g, p, st, cap);
+    } else {
+        if (op) return occupancy_of<1, 1, FWD, CHECK_D, false, EARLY>(p);
+        launch_flow<1, 1, FWD, CHECK_D, false, EARLY>(g, p, st, cap);
+    }
+    return 0;
+}
 template <bool FWD, bool CHECK_D>
 int dispatch(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st = nullptr, int cap = 0,
              int op = 0) {
     if (!st) st = g.stream;
-    if (V == 4) {
-        if (env_int("HF_GA", 0)) return dispatch_ga<FWD, CHECK_D, true>(g, p, LPN, st, cap, op);
-        return dispatch_ga<FWD, CHECK_D, false>(g, p, LPN, st, cap, op);
-    } else if (V == 2) {
-        if (op) return occupancy_of<2, 1, FWD, CHECK_D, false>(p);
-        launch_flow<2, 1, FWD, CHECK_D, false>(g, p, st, cap);
-    } else {
-        if (op) return occupancy_of<1, 1, FWD, CHECK_D, false>(p);
-        launch_flow<1, 1, FWD, CHECK_D, false>(g, p, st, cap);
-    }
-    return 0;
+    if (g.early) return dispatch_mode<FWD, CHECK_D, true>(g, p, V, LPN, st, cap, op);
+    return dispatch_mode<FWD, CHECK_D, false>(g, p, V, LPN, st, cap, op);
 }
 
 // host-side state of a prepared pass
@@ -1000,8 +1014,12 @@ void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cuda
     if (check_d) dispatch<FWD, true>(g, p, V, cx.LPN, st, cap);
     else dispatch<FWD, false>(g, p, V, cx.LPN, st, cap);
     if (cx.nparts > 0) {
-        k_finalize_split<FWD><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
-            cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+        if (g.early)
+            k_finalize_split<FWD, true><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
+                cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+        else
+            k_finalize_split<FWD, false><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
+                cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
@@ -1174,9 +1192,15 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
     const int grid = grid_for(int64_t(g.n) * lpn, 512, g.sms);
     const size_t sm = sizeof(int32_t) * size_t(S);
     if (sm > 48 * 1024) fail(HF_ERR_INVALID_ARG, "too many scenarios");
-    if (V == 4) k_slack_wns<4><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
-    else if (V == 2) k_slack_wns<2><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
-    else k_slack_wns<1><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);
+#define HF_SLACK(VV)                                                                     \
+    do {                                                                                 \
+        if (g.early) k_slack_wns<VV, true><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord); \
+        else k_slack_wns<VV, false><<<grid, 512, sm, s>>>(at, rat, slack, g.n, S, ord);  \
+    } while (0)
+    if (V == 4) HF_SLACK(4);
+    else if (V == 2) HF_SLACK(2);
+    else HF_SLACK(1);
+#undef HF_SLACK
     HF_CHECK_LAUNCH();
     g.launches += 1;
     prof_record(g, 7);

@@ -29,7 +29,7 @@ EXPORTS = [
     "hf_levelize_d", "hf_propagate_forward", "hf_propagate_forward_d", "hf_propagate_backward",
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
-    "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d",
+    "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d", "hf_graph_set_mode",
 ]
 
 
@@ -54,6 +54,7 @@ def _load() -> ctypes.CDLL:
         "hf_graph_create_d": (c_int, [i32, i32, P, P, P, P, P, c_int, P, P]),
         "hf_graph_destroy": (c_int, [P]),
         "hf_graph_set_stream": (c_int, [P, P]),
+        "hf_graph_set_mode": (c_int, [P, c_int]),
         "hf_graph_info": (c_int, [P, P, P, P]),
         "hf_sync": (c_int, [P]),
         "hf_levelize": (c_int, [P, P, P, P, P]),
@@ -221,6 +222,14 @@ def hf_propagate_backward(g: Graph, t_req: float, at, rat, slack=None, wns=None)
         a = _np(at, np.float32)
         _check(_lib.hf_propagate_backward(g.handle, ctypes.c_float(t_req), _ptr(a), _ptr(rat),
                                           _ptr(slack), _ptr(wns)))
+
+
+HF_MODE_LATE, HF_MODE_EARLY = 0, 1
+
+
+def hf_graph_set_mode(g: Graph, mode: int):
+    """HF_MODE_LATE (setup, default) or HF_MODE_EARLY (hold) for later propagation calls."""
+    _check(_lib.hf_graph_set_mode(g.handle, mode))
 
 
 def hf_critical_path(g: Graph, at, t_req, max_len: int, path=None, path_len=None,

@@ -453,3 +453,92 @@ def test_critical_path_batch_device(hf, name, scale, S):
         assert got_l[s] == len(exp[s]), s
         assert got_p[s, :got_l[s]].tolist() == exp[s].tolist(), s
     G.close()
+
+
+# ---- NEXT-2: early (hold) mode (reading R18) --------------------------------------------
+def _single_mode(hf, g, early, T):
+    G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=g.delay)
+    hf.hf_graph_set_mode(G, hf.HF_MODE_EARLY if early else hf.HF_MODE_LATE)
+    hf.hf_levelize(G)
+    at = np.zeros(g.n, F32)
+    hf.hf_propagate_forward(G, g.at_src, at)
+    rat, slack, wns = np.zeros(g.n, F32), np.zeros(g.n, F32), np.zeros(1, F32)
+    hf.hf_propagate_backward(G, T, at, rat, slack, wns)
+    G.close()
+    return at, rat, slack, wns[0]
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C3", 0.01), ("C5", 0.002)])
+def test_early_mode_single(hf, name, scale):
+    g = hfgen.config(name, scale)
+    T = np.float32(-3.75)   # hold requirement
+    at, rat, slack, wns = _single_mode(hf, g, True, T)
+    lv = oracle.levelize(g.n, g.m, g.in_ptr, g.in_src)
+    at_o = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, lv, early=True)
+    rat_o, slack_o, wns_o = oracle.backward(g.n, g.m, g.in_ptr, g.in_src, g.delay, T, at_o, lv,
+                                            early=True)
+    assert_bits_equal(at, at_o, "at_early")
+    assert_bits_equal(rat, rat_o, "rat_early")
+    assert_bits_equal(slack, slack_o, "hold slack")
+    assert_bits_equal(wns, wns_o, "hold wns")
+
+
+def test_early_mode_tiny_and_switching(hf):
+    rng = np.random.default_rng(1812)
+    for trial in range(60):
+        n, edges = random_tiny_dag(rng, nmax=12)
+        m = len(edges)
+        in_ptr, in_src, _ = csr_from_edges(n, edges)
+        d = mixed_delays(rng, m)
+        a_src = mixed_delays(rng, n)
+        T = float(mixed_delays(rng, 1)[0])
+        G = hf.hf_graph_create(n, m, in_ptr, in_src, delay=d)
+        hf.hf_levelize(G)
+        for early in (True, False, True):          # the mode switch takes effect per call
+            hf.hf_graph_set_mode(G, hf.HF_MODE_EARLY if early else hf.HF_MODE_LATE)
+            at = np.zeros(max(n, 1), F32)
+            hf.hf_propagate_forward(G, a_src, at)
+            rat, slack, wns = np.zeros(max(n, 1), F32), np.zeros(max(n, 1), F32), np.zeros(1, F32)
+            hf.hf_propagate_backward(G, T, at[:n], rat, slack, wns)
+            at_o = oracle.forward(n, m, in_ptr, in_src, d, a_src, early=early)
+            rat_o, slack_o, wns_o = oracle.backward(n, m, in_ptr, in_src, d, T, at_o, early=early)
+            assert_bits_equal(at[:n], at_o, f"at {trial} {early}")
+            assert_bits_equal(rat[:n], rat_o, f"rat {trial} {early}")
+            assert_bits_equal(slack[:n], slack_o, f"slack {trial} {early}")
+            assert_bits_equal(wns[0], wns_o, f"wns {trial} {early}")
+        G.close()
+
+
+@pytest.mark.parametrize("S,concurrent", [(8, "0"), (64, "0"), (64, "1"), (3, "0")])
+def test_early_mode_batch(hf, S, concurrent, monkeypatch):
+    import torch
+    monkeypatch.setenv("HF_CONCURRENT", concurrent)
+    dev = torch.device("cuda:0")
+    g = hfgen.config("C3", 0.004)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, -2.5, F32)
+    T[::3] = 1.0
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_graph_set_mode(G, hf.HF_MODE_EARLY)
+    hf.hf_levelize(G)
+    d = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
+    t = torch.from_numpy(T).to(dev)
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    at = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    rat = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    hf.hf_run_batch(G, S, d, hf.HF_LAYOUT_MS, t, torch.from_numpy(g.at_src).to(dev), w, at=at, rat=rat)
+    hf.hf_sync(G)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                                 want_at_rat=True, early=True)
+    assert_bits_equal(at.cpu().numpy().reshape(g.n, S), ato, "at_early")
+    assert_bits_equal(rat.cpu().numpy().reshape(g.n, S), rato, "rat_early")
+    assert_bits_equal(w.cpu().numpy(), wo, "hold wns")
+    # the critical path is a late-mode notion
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_critical_path(G, np.zeros(g.n, F32), 0.0, 4)
+    assert ei.value.status == hf.HF_ERR_INVALID_ARG
+    with pytest.raises(hf.HFError):
+        hf.hf_graph_set_mode(G, 7)
+    G.close()
