@@ -116,8 +116,10 @@ struct Graph {
     DevBuf lo_out_node, lo_out_ptr, lo_out_nbr, lo_out_eid, lo_out_q, lo_out_np;
     // lo_*_nbr: neighbour node id, or -(first part id + 1) when the neighbour's own
     // row (same direction) is long; lo_*_q: [n+1] first part id of every row;
-    // lo_*_np: parts of the long row whose first part id is the index
+    // lo_*_np: parts of the long row whose first part id is the index, then that row
     int32_t nparts_in = 0, nparts_out = 0;
+    // lo_*_np holds [np_cap] part counts (0 except at first part ids) then [np_cap] rows
+    int32_t np_cap_in = 0, np_cap_out = 0;
     // task schedules of the dataflow propagation kernels (per direction)
     TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand

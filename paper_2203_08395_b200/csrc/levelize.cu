@@ -320,10 +320,14 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
     }
 }
 // parts of every long row, stored at its first part id
-__global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__restrict__ np) {
+__global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__restrict__ np,
+                        int32_t *__restrict__ prow) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
-        if (lo_q[i + 1] != lo_q[i]) np[lo_q[i]] = lo_q[i + 1] - lo_q[i];
+        if (lo_q[i + 1] != lo_q[i]) {
+            np[lo_q[i]] = lo_q[i + 1] - lo_q[i];
+            prow[lo_q[i]] = int32_t(i);
+        }
 }
 
 // copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid
@@ -595,8 +599,12 @@ int64_t levelize_device(Graph &g) {
             scan_exclusive(deg.as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, s, g);
             scan_exclusive(parts.as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, s, g);
             // parts of every long row, indexed by its first part id (<= m/9 + m/LO_PE ids)
-            np.alloc(sizeof(int32_t) * size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1), s);
-            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lo_q, n, np.as<int32_t>());
+            const size_t npcap = size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1);
+            np.alloc(sizeof(int32_t) * npcap * 2, s);   // [np | row] by first part id
+            HF_CUDA(cudaMemsetAsync(np.p, 0, sizeof(int32_t) * npcap, s));
+            (in ? g.np_cap_in : g.np_cap_out) = int32_t(npcap);
+            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lo_q, n, np.as<int32_t>(),
+                                                            np.as<int32_t>() + npcap);
             HF_CHECK_LAUNCH();
             if (in)
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(

@@ -596,40 +596,72 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 }
 
 // After a pass: every long row gets its value (combine of its partials), its
-// optional slack and its worst-slack contribution.  Rows with parts are found
-// from the part-id prefix q; one warp per such row.
-template <bool FWD, bool EARLY>
-__global__ void k_finalize_split(const int32_t *__restrict__ q, int32_t n,
-                                 const int32_t *__restrict__ node_of, int32_t S,
+// optional slack and its worst-slack contribution.  One thread per (first part id,
+// V-wide column vector): all long rows and columns in parallel, the partials of a
+// row loaded four at a time; worst slack folded per block (ordered-int atomicMin).
+template <bool FWD, bool EARLY, int V>
+__global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32_t *__restrict__ prow,
+                                 int32_t nparts, const int32_t *__restrict__ node_of, int32_t S,
                                  const float *__restrict__ part_buf, float *__restrict__ out,
                                  const float *__restrict__ other, float *__restrict__ slack,
                                  int32_t *__restrict__ wns_ord) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t base = ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5) * 32; base < n;
-         base += nw * 32) {
-        const int64_t i = base + lane;
-        const bool has = i < n && q[i + 1] != q[i];
-        unsigned mk = __ballot_sync(0xffffffffu, has);
-        while (mk) {
-            const int src = __ffs(mk) - 1;
-            mk &= mk - 1;
-            const int64_t r = base + src;
-            const int qb = q[r], np = q[r + 1] - qb;
-            const int64_t node = node_of[r];
-            for (int s = lane; s < S; s += 32) {
-                float v = part_buf[int64_t(qb) * S + s];
-                for (int k = 1; k < np; ++k)
-                    v = combine<FWD != EARLY>(v, part_buf[int64_t(qb + k) * S + s]);
-                out[node * S + s] = v;
-                if (!FWD && other) {
-                    const float sl = EARLY ? __fsub_rn(other[node * S + s], v)
-                                           : __fsub_rn(v, other[node * S + s]);
-                    if (slack) slack[node * S + s] = sl;
-                    atomicMin(wns_ord + s, f2ord(sl));
+    constexpr bool MX = FWD != EARLY;
+    extern __shared__ int32_t s_wmin[];
+    const bool do_slack = !FWD && other;
+    if (do_slack) {
+        for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
+        __syncthreads();
+    }
+    const int lpn = S / V;
+    const int apb = blockDim.x / lpn * lpn;            // active threads per block
+    const int64_t step = int64_t(gridDim.x) * apb;     // a multiple of lpn: lane fixed
+    const int lane = int(threadIdx.x % lpn);
+    const int64_t col = int64_t(lane) * V;
+    float mn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+    if (int(threadIdx.x) < apb) {
+        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < int64_t(nparts) * lpn;
+             t += step) {
+            const int64_t p = t / lpn;
+            const int np = np_arr[p];
+            if (np == 0) continue;   // not the first part of a row
+            const int64_t node = node_of[prow[p]];
+            const float *base = part_buf + p * S + col;
+            Vec<V> acc = ld_relaxed<V>(base);
+            for (int k = 1; k < np; k += 4) {
+                Vec<V> v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k + u < np) v[u] = ld_relaxed<V>(base + int64_t(k + u) * S);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k + u < np)
+#pragma unroll
+                        for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v[u].x[j]);
+            }
+            st_plain<V>(out + node * S + col, acc);
+            if (do_slack) {
+                const Vec<V> a = ld_relaxed<V>(other + node * S + col);
+                Vec<V> sl;
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    sl.x[j] = EARLY ? __fsub_rn(a.x[j], acc.x[j]) : __fsub_rn(acc.x[j], a.x[j]);
+                    mn[j] = fminf(mn[j], sl.x[j]);
                 }
+                if (slack) st_plain<V>(slack + node * S + col, sl);
             }
         }
+    }
+    if (do_slack) {
+        if (int(threadIdx.x) < apb)
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (mn[j] != __int_as_float(0x7f800000))
+                    atomicMin(s_wmin + col + j, f2ord(mn[j]));
+        __syncthreads();
+        for (int s = threadIdx.x; s < S; s += blockDim.x)
+            if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
     }
 }
 
@@ -1014,12 +1046,25 @@ void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cuda
     if (check_d) dispatch<FWD, true>(g, p, V, cx.LPN, st, cap);
     else dispatch<FWD, false>(g, p, V, cx.LPN, st, cap);
     if (cx.nparts > 0) {
-        if (g.early)
-            k_finalize_split<FWD, true><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
-                cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
-        else
-            k_finalize_split<FWD, false><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(
-                cx.Q, g.n, p.node_of, p.S, p.part_buf, p.out, p.other, p.slack, p.wns_ord);
+        const int32_t *npa = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
+        const int32_t *prow = npa + (FWD ? g.np_cap_in : g.np_cap_out);
+        const int lpn = p.S / V;
+        const int grid = grid_for(int64_t(cx.nparts) * lpn, 256, g.sms);
+        const size_t sm = sizeof(int32_t) * size_t(p.S);
+#define HF_FIN(EE, VV)                                                                    \
+    k_finalize_split<FWD, EE, VV><<<grid, 256, sm, st>>>(npa, prow, cx.nparts, p.node_of, p.S, \
+                                                          p.part_buf, p.out, p.other, p.slack, \
+                                                          p.wns_ord)
+        if (g.early) {
+            if (V == 4) HF_FIN(true, 4);
+            else if (V == 2) HF_FIN(true, 2);
+            else HF_FIN(true, 1);
+        } else {
+            if (V == 4) HF_FIN(false, 4);
+            else if (V == 2) HF_FIN(false, 2);
+            else HF_FIN(false, 1);
+        }
+#undef HF_FIN
         HF_CHECK_LAUNCH();
         g.launches += 1;
     }
