@@ -67,7 +67,8 @@ def _load():
         lib.oracle_critical_path.argtypes = [i32, i32, P, P, P, ctypes.c_int64, P,
                                              ctypes.c_float, P, i32, P]
         lib.oracle_critical_paths.argtypes = [i32, i32, P, P, i32, P, P, P, P, i32, P]
-        for f in (lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
+        lib.oracle_mis.argtypes = [i32, i32, P, P, P, P]
+        for f in (lib.oracle_mis, lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
                   lib.oracle_forward, lib.oracle_backward, lib.oracle_batch,
                   lib.oracle_critical_path, lib.oracle_critical_paths, lib.oracle_forward_mode,
                   lib.oracle_backward_mode, lib.oracle_batch_mode):
@@ -237,3 +238,17 @@ def critical_paths(n, m, in_ptr, in_src, delays_ms, at_all, t_req, max_len=None)
     if rc:
         raise OracleError(rc)
     return [paths[s, :lens[s]].copy() for s in range(S)]
+
+
+def mis(n, m, in_ptr, in_src, prio):
+    """NEXT-4 (reading R19): lexicographically-first maximal independent set of the
+    undirected graph of the edges, vertices visited by increasing (prio, id).
+    Returns uint8 in_set[n]."""
+    lib = _load()
+    in_ptr, in_src = _i32(in_ptr), _i32(in_src)
+    pr = _i32(prio) if n else np.zeros(1, np.int32)
+    out = np.zeros(max(n, 1), np.uint8)
+    rc = lib.oracle_mis(n, m, _p(in_ptr), _p(in_src), _p(pr), _p(out))
+    if rc:
+        raise OracleError(rc)
+    return out[:n].copy()

@@ -22,6 +22,8 @@
  *   - slack = fl(rat - at), wns = min slack                  BASELINE.json:5; reading R4
  *   - batched what-if scenarios = independent delay sets     PAPER.md:969-980; BASELINE.json:10
  *   - critical path of the worst endpoint (argmax trace-back) PAPER.md:1002-1003; reading R17
+ *   - greedy MIS by priority (Blelloch's lexicographically-first MIS)
+ *                                                           PAPER.md:1141-1150; reading R19
  *   - early (hold) mode: min-plus forward, max-plus backward, slack = at - rat
  *                                                           PAPER.md:972-974 ("analysis mode"); reading R18
  *
@@ -392,4 +394,42 @@ int oracle_critical_paths(int32_t n, int32_t m, const int32_t *in_ptr, const int
     }
     free(at);
     return rc;
+}
+
+/* ---- NEXT-4: greedy maximal independent set -------------
+ * the detailed-placement workload extracts "a maximal
+ * independent set ... using Blelloch's Algorithm" (blelloch2012greedy), whose
+ * result is the lexicographically-first MIS for a priority order.
+ * reading R19: the graph is the undirected graph of the DAG's edges; vertices are
+ * visited by increasing key (prio[v], v); v joins the set iff none of its
+ * neighbours visited earlier joined.  in_set[v] = 1 / 0.  Sequential definition,
+ * O(n log n + m). */
+static const int32_t *g_prio;
+static int cmp_prio(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    if (g_prio[x] != g_prio[y]) return g_prio[x] < g_prio[y] ? -1 : 1;
+    return (x > y) - (x < y);
+}
+int oracle_mis(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+               const int32_t *prio, uint8_t *in_set) {
+    int rc = oracle_check_csr(n, m, in_ptr, in_src);
+    if (rc) return rc;
+    int32_t *out_ptr = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int32_t *out_dst = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    int32_t *out_eid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    oracle_fanout(n, m, in_ptr, in_src, out_ptr, out_dst, out_eid);
+    int32_t *vis = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    for (int32_t v = 0; v < n; ++v) vis[v] = v;
+    g_prio = prio;
+    qsort(vis, (size_t)n, sizeof(int32_t), cmp_prio);
+    for (int32_t v = 0; v < n; ++v) in_set[v] = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        int32_t v = vis[i];
+        int blocked = 0;
+        for (int32_t e = in_ptr[v]; e < in_ptr[v + 1] && !blocked; ++e) blocked = in_set[in_src[e]];
+        for (int32_t k = out_ptr[v]; k < out_ptr[v + 1] && !blocked; ++k) blocked = in_set[out_dst[k]];
+        in_set[v] = (uint8_t)!blocked;   /* later neighbours are still 0 here */
+    }
+    free(vis); free(out_ptr); free(out_dst); free(out_eid);
+    return OR_OK;
 }

@@ -482,3 +482,67 @@ def test_p12_early_unit_delay_is_bfs_distance():
         dist = new
     at = oracle.forward(g.n, g.m, g.in_ptr, g.in_src, np.ones(g.m, F32), None, early=True)
     assert np.array_equal(at, dist.astype(F32))
+
+
+# ---- P13: greedy MIS (NEXT-4, reading R19) ----------------------------------------
+def _lexfirst_mis_bruteforce(n, und_edges, key):
+    """Enumerate all independent sets that are maximal; the lexicographically-first
+    one visits vertices by increasing key and prefers membership."""
+    order = sorted(range(n), key=lambda v: key[v])
+    adj = [set() for _ in range(n)]
+    for u, v in und_edges:
+        adj[u].add(v)
+        adj[v].add(u)
+    best = None
+    for mask in range(1 << n):
+        S = [v for v in range(n) if mask >> v & 1]
+        if any(u in adj[v] for v in S for u in S):
+            continue
+        if any(all(u not in adj[v] for u in S) for v in range(n) if not mask >> v & 1):
+            continue                                          # not maximal
+        vec = tuple(mask >> v & 1 for v in order)
+        if best is None or vec > best[0]:
+            best = (vec, mask)
+    return np.array([best[1] >> v & 1 for v in range(n)], np.uint8)
+
+
+def test_p13_mis_bruteforce_tiny():
+    rng = np.random.default_rng(1313)
+    for trial in range(300):
+        n, edges = random_tiny_dag(rng, nmax=9, p=0.35)
+        in_ptr, in_src, _ = csr_from_edges(n, edges)
+        prio = rng.integers(0, 4, size=n).astype(np.int32)   # ties broken by id
+        got = oracle.mis(n, len(edges), in_ptr, in_src, prio)
+        exp = _lexfirst_mis_bruteforce(n, edges, [(int(prio[v]), v) for v in range(n)])
+        assert np.array_equal(got, exp), trial
+
+
+def test_p13_mis_characterisation_large():
+    # independent, and every excluded vertex has an earlier (prio, id) neighbour in
+    # the set: the two properties single out the lexicographically-first MIS
+    g = hfgen.config("C3", 0.05)
+    prio = np.random.default_rng(5).permutation(g.n).astype(np.int32)
+    s = oracle.mis(g.n, g.m, g.in_ptr, g.in_src, prio)
+    src, dst = g.edges()
+    assert not (s[src] & s[dst]).any()                        # independent
+    key = prio.astype(np.int64) * g.n + np.arange(g.n)
+    earlier_in = np.zeros(g.n, bool)
+    for a, b in ((src, dst), (dst, src)):                     # a's neighbour b
+        hit = (key[b] < key[a]) & (s[b] == 1)
+        earlier_in[a[hit]] = True
+    assert np.array_equal(s == 0, earlier_in)
+
+
+def test_p13_mis_closed_forms():
+    k = 101
+    in_ptr, in_src, _ = csr_from_edges(k, [(i, i + 1) for i in range(k - 1)])   # a path
+    up = oracle.mis(k, k - 1, in_ptr, in_src, np.arange(k, dtype=np.int32))
+    assert np.array_equal(np.nonzero(up)[0], np.arange(0, k, 2))
+    down = oracle.mis(k, k - 1, in_ptr, in_src, np.arange(k, dtype=np.int32)[::-1].copy())
+    assert np.array_equal(np.nonzero(down)[0], np.arange(k - 1, -1, -2)[::-1])
+    star = [(0, i) for i in range(1, 20)]                      # centre 0
+    in_ptr, in_src, _ = csr_from_edges(20, star)
+    first = oracle.mis(20, 19, in_ptr, in_src, np.arange(20, dtype=np.int32))
+    assert np.nonzero(first)[0].tolist() == [0]
+    last = oracle.mis(20, 19, in_ptr, in_src, np.r_[99, np.arange(1, 20)].astype(np.int32))
+    assert np.nonzero(last)[0].tolist() == list(range(1, 20))
