@@ -199,6 +199,17 @@ hf_status hf_critical_path_d(hf_graph g, int32_t S, const float *delays, const f
 hf_status hf_critical_path(hf_graph g, const float *at, float t_req, int32_t max_len,
                            int32_t *path, int32_t *path_len);
 
+/* NEXT-4: greedy maximal independent set (PAPER.md:1141-1150
+ * "a parallel maximal independent set finding step using Blelloch's Algorithm";
+ * DESIGN.md reading R19).  The graph is the undirected graph of the DAG's edges;
+ * the result is the lexicographically-first MIS for the vertex order (prio[v], v):
+ * v is in the set iff none of its neighbours earlier in that order is.
+ * prio [n] int32 keys (ties broken by node id); in_set [n] bytes, 1 = in the set.
+ * hf_mis_d: device pointers, stream-ordered.  hf_mis: host pointers, synchronous.
+ * The graph need not be levelized. */
+hf_status hf_mis_d(hf_graph g, const int32_t *prio, uint8_t *in_set);
+hf_status hf_mis(hf_graph g, const int32_t *prio, uint8_t *in_set);
+
 /* NCCL bootstrap (libnccl.so.2 is loaded on first use).  Rank 0 calls
  * hf_nccl_unique_id and broadcasts the 128 bytes (e.g. over torch.distributed);
  * every rank then calls hf_nccl_comm_init with its rank on its device. */

@@ -26,6 +26,7 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
 void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                   const float *t_arr, float *at, float *rat, float *slack, float *wns_f);
 void profile_mark(Graph &g, int idx);
+void mis_device(Graph &g, const int32_t *prio, uint8_t *in_set);
 void critical_path_device(Graph &g, int32_t S, const float *d, const float *at,
                           const float *t_arr, float t_scalar, int32_t max_len, int32_t *path,
                           int32_t *len);
@@ -659,6 +660,36 @@ hf_status hf_critical_path(hf_graph h, const float *at, float t_req, int32_t max
             HF_CUDA(cudaMemcpy(path, p.p, sizeof(int32_t) * size_t(ln), cudaMemcpyDeviceToHost));
         *path_len = ln;
         return HF_OK;
+    });
+}
+
+hf_status hf_mis_d(hf_graph h, const int32_t *prio_d, uint8_t *in_set_d) {
+    return guarded([&]() -> hf_status {
+        if (!h || !in_set_d) fail(HF_ERR_INVALID_ARG, "graph or in_set is NULL");
+        Graph *g = G(h);
+        if (g->n && !prio_d) fail(HF_ERR_INVALID_ARG, "prio is NULL");
+        DeviceGuard dg(g->device);
+        mis_device(*g, prio_d, in_set_d);
+        return HF_OK;
+    });
+}
+
+hf_status hf_mis(hf_graph h, const int32_t *prio, uint8_t *in_set) {
+    return guarded([&]() -> hf_status {
+        if (!h || !in_set) fail(HF_ERR_INVALID_ARG, "graph or in_set is NULL");
+        Graph *g = G(h);
+        if (g->n && !prio) fail(HF_ERR_INVALID_ARG, "prio is NULL");
+        DeviceGuard dg(g->device);
+        cudaStream_t s = g->stream;
+        if (g->n == 0) return HF_OK;
+        DevBuf pr, out;
+        pr.alloc(sizeof(int32_t) * size_t(g->n), s);
+        out.alloc(size_t(g->n), s);
+        HF_CUDA(cudaMemcpyAsync(pr.p, prio, sizeof(int32_t) * g->n, cudaMemcpyHostToDevice, s));
+        mis_device(*g, pr.as<int32_t>(), out.as<uint8_t>());
+        HF_CUDA(cudaMemcpyAsync(in_set, out.p, size_t(g->n), cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
+        return latch(*g);
     });
 }
 

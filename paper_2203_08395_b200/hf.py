@@ -30,6 +30,7 @@ EXPORTS = [
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
     "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d", "hf_graph_set_mode",
+    "hf_mis", "hf_mis_d",
 ]
 
 
@@ -55,6 +56,8 @@ def _load() -> ctypes.CDLL:
         "hf_graph_destroy": (c_int, [P]),
         "hf_graph_set_stream": (c_int, [P, P]),
         "hf_graph_set_mode": (c_int, [P, c_int]),
+        "hf_mis": (c_int, [P, P, P]),
+        "hf_mis_d": (c_int, [P, P, P]),
         "hf_graph_info": (c_int, [P, P, P, P]),
         "hf_sync": (c_int, [P]),
         "hf_levelize": (c_int, [P, P, P, P, P]),
@@ -252,6 +255,19 @@ def hf_critical_path(g: Graph, at, t_req, max_len: int, path=None, path_len=None
     _check(_lib.hf_critical_path(g.handle, _ptr(a), ctypes.c_float(t_req), max_len, _ptr(out),
                                  ctypes.byref(ln)))
     return out[:ln.value].copy()
+
+
+def hf_mis(g: Graph, prio, in_set=None):
+    """NEXT-4 greedy MIS (reading R19).  Host: prio numpy int32 [n] -> uint8 [n].
+    Device: prio int32 CUDA tensor, in_set uint8 CUDA tensor (stream-ordered)."""
+    if _is_torch(prio):
+        _check(_lib.hf_mis_d(g.handle, _ptr(prio), _ptr(in_set)))
+        return in_set
+    p = _np(prio, np.int32)
+    n = p.shape[0]
+    out = np.zeros(max(n, 1), np.uint8)
+    _check(_lib.hf_mis(g.handle, _ptr(p), _ptr(out)))
+    return out[:n]
 
 
 def hf_run_batch(g: Graph, s_local: int, delays, layout: int, t_req, at_src, wns_local,

@@ -542,3 +542,41 @@ def test_early_mode_batch(hf, S, concurrent, monkeypatch):
     with pytest.raises(hf.HFError):
         hf.hf_graph_set_mode(G, 7)
     G.close()
+
+
+# ---- NEXT-4: greedy MIS (reading R19) ------------------------------------------------
+@pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C3", 0.02), ("C3", 1.0), ("C2-random", 0.1),
+                                        ("C5", 0.01)])
+def test_mis_matches_oracle(hf, name, scale):
+    g = hfgen.config(name, scale)
+    prio = np.random.default_rng(44).permutation(g.n).astype(np.int32)
+    G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src)
+    got = hf.hf_mis(G, prio)
+    G.close()
+    exp = oracle.mis(g.n, g.m, g.in_ptr, g.in_src, prio)
+    assert np.array_equal(got, exp), (name, int((got != exp).sum()))
+
+
+def test_mis_ties_tiny_and_device_api(hf):
+    import torch
+    rng = np.random.default_rng(4404)
+    for trial in range(80):
+        n, edges = random_tiny_dag(rng, nmax=14, p=0.4)
+        m = len(edges)
+        in_ptr, in_src, _ = csr_from_edges(n, edges)
+        prio = rng.integers(0, 3, size=n).astype(np.int32)      # many ties: broken by id
+        G = hf.hf_graph_create(n, m, in_ptr, in_src)
+        got = hf.hf_mis(G, prio)
+        exp = oracle.mis(n, m, in_ptr, in_src, prio)
+        assert np.array_equal(got, exp), trial
+        G.close()
+    g = hfgen.config("C1")
+    dev = torch.device("cuda:0")
+    prio = np.random.default_rng(7).permutation(g.n).astype(np.int32)
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), stream=torch.cuda.current_stream())
+    out = torch.empty(g.n, dtype=torch.uint8, device=dev)
+    hf.hf_mis(G, torch.from_numpy(prio).to(dev), out)
+    hf.hf_sync(G)
+    assert np.array_equal(out.cpu().numpy(), oracle.mis(g.n, g.m, g.in_ptr, g.in_src, prio))
+    G.close()
