@@ -333,16 +333,19 @@ __global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__
 // copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid
 // (eid_map == null -> the edge id is the source position itself); a neighbour u
 // whose own row in this direction is long is written as -(first part id + 1)
-__device__ __forceinline__ int lo_enc(int u, const int32_t *ptr, const int32_t *pos,
-                                      const int32_t *q) {
-    return ptr[u + 1] - ptr[u] > LO_SPLIT ? -(q[pos[u]] + 1) : u;
+// neighbour encoding of every node, once per node: its id, or -(first part id + 1)
+// when its own row (this direction) is long; the relabel then reads one value per edge
+__global__ void k_lo_enc(const int32_t *__restrict__ ptr, const int32_t *__restrict__ pos,
+                         const int32_t *__restrict__ q, int32_t n, int32_t *__restrict__ enc) {
+    for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < n;
+         u += int64_t(gridDim.x) * blockDim.x)
+        enc[u] = ptr[u + 1] - ptr[u] > LO_SPLIT ? -(q[pos[u]] + 1) : int32_t(u);
 }
 __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
                                const int32_t *__restrict__ ptr, const int32_t *__restrict__ a,
                                const int32_t *__restrict__ eid_map,
-                               const int32_t *__restrict__ nptr, const int32_t *__restrict__ pos,
-                               const int32_t *__restrict__ q, int32_t *__restrict__ na,
-                               int32_t *__restrict__ neid) {
+                               const int32_t *__restrict__ nptr, const int32_t *__restrict__ enc,
+                               int32_t *__restrict__ na, int32_t *__restrict__ neid) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps_total = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t wbase = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
@@ -358,7 +361,7 @@ __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
         bool longrow = (e - b) >= 32;
         if (!longrow)
             for (int k = b; k < e; ++k) {
-                na[o + (k - b)] = lo_enc(a[k], ptr, pos, q);
+                na[o + (k - b)] = enc[a[k]];
                 neid[o + (k - b)] = eid_map ? eid_map[k] : k;
             }
         unsigned lm = __ballot_sync(0xffffffffu, longrow);
@@ -369,7 +372,7 @@ __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
             int ee = __shfl_sync(0xffffffffu, e, srcl);
             int oo = __shfl_sync(0xffffffffu, o, srcl);
             for (int k = bb + lane; k < ee; k += 32) {
-                na[oo + (k - bb)] = lo_enc(a[k], ptr, pos, q);
+                na[oo + (k - bb)] = enc[a[k]];
                 neid[oo + (k - bb)] = eid_map ? eid_map[k] : k;
             }
         }
@@ -574,12 +577,13 @@ int64_t levelize_device(Graph &g) {
         g.lo_in_eid.alloc(sizeof(int32_t) * mm, s);
         g.lo_out_nbr.alloc(sizeof(int32_t) * mm, s);
         g.lo_out_eid.alloc(sizeof(int32_t) * mm, s);
-        DevBuf flag, fs, deg, parts, pos;
+        DevBuf flag, fs, deg, parts, pos, enc;
         flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         fs.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         deg.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         parts.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
         pos.alloc(sizeof(int32_t) * n, s);
+        enc.alloc(sizeof(int32_t) * n, s);
         for (int dir = 0; dir < 2; ++dir) {
             const bool in = dir == 0;
             const int32_t *ptr = in ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>();
@@ -606,15 +610,17 @@ int64_t levelize_device(Graph &g) {
             k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lo_q, n, np.as<int32_t>(),
                                                             np.as<int32_t>() + npcap);
             HF_CHECK_LAUNCH();
+            k_lo_enc<<<grid_for(n, 256, g.sms), 256, 0, s>>>(ptr, pos.as<int32_t>(), lo_q, n,
+                                                             enc.as<int32_t>());
+            HF_CHECK_LAUNCH();
             if (in)
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-                    lo_node, n, ptr, g.in_src.as<int32_t>(), nullptr, lo_ptr, pos.as<int32_t>(),
-                    lo_q, g.lo_in_nbr.as<int32_t>(), g.lo_in_eid.as<int32_t>());
+                    lo_node, n, ptr, g.in_src.as<int32_t>(), nullptr, lo_ptr, enc.as<int32_t>(),
+                    g.lo_in_nbr.as<int32_t>(), g.lo_in_eid.as<int32_t>());
             else
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
                     lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
-                    pos.as<int32_t>(), lo_q, g.lo_out_nbr.as<int32_t>(),
-                    g.lo_out_eid.as<int32_t>());
+                    enc.as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
             g.launches += 4;
         }
