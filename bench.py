@@ -162,6 +162,15 @@ def cpu_baseline(g, D_host, T, at_src, sample_note):
             "sample": sample_note, "seconds": round(dt, 3)}
 
 
+def arm_config(args, g, S, S_total, world):
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": f"{args.config}: levelized circuit DAG n={g.n} m={g.m} D={g.depth}, "
+                        f"{S} scenarios/GPU, create+levelize+fwd+bwd+wns per step",
+            "n": g.n, "m": g.m, "levels": g.depth, "scenarios_per_gpu": S,
+            "scenarios_total": S_total, "parallelism": f"scenario-shard x{world}",
+            "l2": "flushed between steps (2x L2 write) and inputs > L2"}
+
+
 def run_reference(args):
     """The oracle as the reference arm (this tier has no installable reference)."""
     ws, rank, _ = dist_env()
@@ -180,14 +189,16 @@ def run_reference(args):
         oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=cores)
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
     v = 2.0 * g.m * S_ref / dt
-    sample = (f"{args.config}: n={g.n} m={g.m}, {S_ref} of the scenarios per step, "
-              f"oracle levelize+fwd+bwd, {cores} threads")
+    sample = (f"{args.config}: n={g.n} m={g.m}, a bounded sample: {S_ref} of the scenarios per "
+              f"step (value = 2*m*{S_ref} / step time), oracle levelize+fwd+bwd+wns, "
+              f"{cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} (oracle sample)", "n": g.n, "m": g.m,
-                       "scenarios_per_step": S_ref},
+            "config": arm_config(args, g, args.scenarios if args.scaling == "weak"
+                                 else args.scenarios // max(ws, 1),
+                                 args.scenarios * (ws if args.scaling == "weak" else 1), ws),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -370,11 +381,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: levelized circuit DAG n={n} m={m} D={g.depth}, "
-                                   f"{S} scenarios/GPU, create+levelize+fwd+bwd+wns per step",
-                       "n": n, "m": m, "levels": g.depth, "scenarios_per_gpu": S,
-                       "scenarios_total": S_total, "parallelism": f"scenario-shard x{world}",
-                       "l2": "flushed between steps (2x L2 write) and inputs > L2"},
+            "config": arm_config(args, g, S, S_total, world),
             "phases_ms": {"levelize": lev_ms / K, "propagation_phase": phase_ms / K,
                           "forward_kernel": fwd_ms / K, "backward_kernel": bwd_ms / K,
                           "other": ms_step - (lev_ms + phase_ms) / K},
