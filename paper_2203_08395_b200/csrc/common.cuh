@@ -106,8 +106,6 @@ struct Graph {
     bool levelized = false;
     int32_t L = -1;
     DevBuf level, level_ptr, order;
-    std::vector<int32_t> h_level_ptr;
-    int32_t max_level_width = 0;
     // level-ordered ("relabelled") CSR for the propagation passes: row i is node
     // order[i]; eid = original edge id (delay row).  Built by hf_levelize.
     // Within a level, rows of degree <= LO_SPLIT first, then the longer ones, each
@@ -117,9 +115,11 @@ struct Graph {
     // lo_*_nbr: neighbour node id, or -(first part id + 1) when the neighbour's own
     // row (same direction) is long; lo_*_q: [n+1] first part id of every row;
     // lo_*_np: parts of the long row whose first part id is the index, then that row
-    int32_t nparts_in = 0, nparts_out = 0;
-    // lo_*_np holds [np_cap] part counts (0 except at first part ids) then [np_cap] rows
+    // part ids per direction: at most np_cap (host bound); the exact counts live on
+    // the device (nparts_d[0] fan-in, nparts_d[1] fan-out).  lo_*_np holds [np_cap]
+    // part counts (0 except at first part ids) then [np_cap] rows
     int32_t np_cap_in = 0, np_cap_out = 0;
+    const int32_t *nparts_d = nullptr;
     // task schedules of the dataflow propagation kernels (per direction)
     TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand

@@ -444,9 +444,7 @@ int64_t levelize_device(Graph &g) {
     g.level_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
     if (n == 0) {
         HF_CUDA(cudaMemsetAsync(g.level_ptr.p, 0, sizeof(int32_t), s));
-        g.h_level_ptr.assign(1, 0);
         g.L = 0;
-        g.max_level_width = 0;
         g.levelized = true;
         HF_CUDA(cudaStreamSynchronize(s));
         return 0;
@@ -625,17 +623,9 @@ int64_t levelize_device(Graph &g) {
             g.launches += 4;
         }
     }
-    // one host round trip: level_ptr and the part counts of both directions
-    g.h_level_ptr.resize(size_t(L) + 1);
-    HF_CUDA(cudaMemcpyAsync(g.h_level_ptr.data(), g.level_ptr.p, sizeof(int32_t) * (L + 1),
-                            cudaMemcpyDeviceToHost, s));
-    HF_CUDA(cudaMemcpyAsync(h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, s));
-    HF_CUDA(cudaStreamSynchronize(s));
-    g.nparts_in = h_sc[12];
-    g.nparts_out = h_sc[13];
-    int32_t w = 0;
-    for (int32_t k = 0; k < L; ++k) w = std::max(w, g.h_level_ptr[k + 1] - g.h_level_ptr[k]);
-    g.max_level_width = w;
+    // no second host round trip: the passes size the part buffers by the bound
+    // np_cap and read the exact part counts (sc[12], sc[13]) on the device
+    g.nparts_d = sc + 12;
     g.ts_f.key = g.ts_b.key = -1;   // task schedules depend on the levels
     g.L = L;
     g.levelized = true;

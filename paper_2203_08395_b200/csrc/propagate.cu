@@ -665,6 +665,13 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
     }
 }
 
+__global__ void k_fill_parts(uint32_t *buf, const int32_t *count, int32_t S) {
+    const int64_t total = int64_t(*count) * S;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x)
+        buf[i] = 0xffffffffu;
+}
+
 __global__ void k_fill_i32(int32_t *p, int32_t v, int64_t count) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -1016,7 +1023,8 @@ template <bool FWD> void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &c
     p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
     p.poll_all = env_int("HF_POLL_ALL", 1);
     TaskSched &ts = FWD ? g.ts_f : g.ts_b;
-    cx.nparts = FWD ? g.nparts_in : g.nparts_out;
+    cx.nparts = FWD ? g.np_cap_in : g.np_cap_out;   // bound; exact count on the device
+    const int32_t *nparts_dev = g.nparts_d + (FWD ? 0 : 1);
     cx.Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
     if (ts.key != tw || !ts.desc.p) {
         build_tasks<FWD>(g, p.row_ptr, p.node_of, cx.Q, cx.nparts, tw, ts);
@@ -1033,7 +1041,11 @@ template <bool FWD> void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &c
     if (cx.nparts > 0) {
         cx.part_buf.alloc(sizeof(float) * size_t(cx.nparts) * p.S, s);
         p.part_buf = cx.part_buf.as<float>();
-        HF_CUDA(cudaMemsetAsync(cx.part_buf.p, 0xff, cx.part_buf.bytes, s));
+        // NaN sentinel over the partials actually used (count read on the device)
+        k_fill_parts<<<grid_for(int64_t(cx.nparts) * p.S / 4 + 1, 256, g.sms), 256, 0, s>>>(
+            reinterpret_cast<uint32_t *>(p.part_buf), nparts_dev, p.S);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
     }
     // the NaN sentinel (all-ones bit pattern): "not yet computed"
     HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
