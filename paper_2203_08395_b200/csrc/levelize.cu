@@ -169,29 +169,52 @@ __device__ __forceinline__ void warp_append_chunks(int cnt, int start, int node,
     for (int t = 0; t < cnt; ++t) list[base + t] = make_int2(start + t * KCH, node);
 }
 
+// warp-aggregated append with a 64-bit {arrivals:32 | count:32} round word: the
+// count lives in the low half, so the barrier's spin read also returns the size
+__device__ __forceinline__ void warp_append_chunks64(int cnt, int start, int node, int2 *list,
+                                                     unsigned long long *word) {
+    const int lane = threadIdx.x & 31;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    int base = 0;
+    if (lane == 31) base = int(unsigned(atomicAdd(word, (unsigned long long)total)));
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+    for (int t = 0; t < cnt; ++t) list[base + t] = make_int2(start + t * KCH, node);
+}
+
 // Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w) over the
 // contracted edges r -> j (cdst, cw), released by the atomic join counter cnt[j].
 // A frontier entry is one contracted edge {edge, source node}: every lane does
 // exactly one relaxation per round, so hub fan-outs are spread over the whole GPU.
+// Round r+1's frontier is counted in the low half of the 64-bit word W[(r+1) % 3]
+// and the grid barrier ending round r adds its arrivals to the high half, so one
+// acquire read gives both "everyone arrived" and the next frontier size; the
+// out-edge range of the target is loaded before the join-counter decrement returns.
 __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__restrict__ cdst,
                            const int32_t *__restrict__ cw, int32_t *__restrict__ cnt,
                            int32_t *__restrict__ lev, int2 *__restrict__ fr_a,
-                           int2 *__restrict__ fr_b, int32_t *sc, GridBar *bar,
+                           int2 *__restrict__ fr_b, int32_t *sc, unsigned long long *W,
                            unsigned long long *trace) {
+    __shared__ int s_size;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     // consecutive warp slots land on different SMs, so a small frontier is spread
     // over the whole GPU instead of the first few CTAs
     const int64_t wid = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
     int2 *lists[2] = {fr_a, fr_b};
-    unsigned bar_target = 0;
+    int size = reinterpret_cast<volatile int32_t *>(sc)[SC_FR + 0];   // seeded frontier
     for (int r = 0;; ++r) {
-        volatile int32_t *vsc = sc;
-        const int size = vsc[SC_FR + r % 3];
         if (size == 0) break;
-        if (blockIdx.x == 0 && threadIdx.x == 0) vsc[SC_FR + (r + 2) % 3] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) W[(r + 2) % 3] = 0ull;
         const int2 *in = lists[r & 1];
         int2 *out = lists[(r + 1) & 1];
+        unsigned long long *wn = W + (r + 1) % 3;
         if (trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 4096) {
             trace[3 * r] = lev_gtimer();
             trace[3 * r + 2] = (unsigned long long)size;
@@ -204,16 +227,32 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
                 k = __ldg(cdst + en.x);
                 const int w = __ldg(cw + en.x);
                 const int lj = __ldcg(lev + en.y);
+                const int ks = __ldg(cptr + k), ke = __ldg(cptr + k + 1);   // speculative
                 atomicMax(lev + k, lj + w);
                 if (atomicSub(cnt + k, 1) == 1) {   // k ready: queue its out-edges
-                    kstart = __ldg(cptr + k);
-                    nch = __ldg(cptr + k + 1) - kstart;
+                    kstart = ks;
+                    nch = ke - ks;
                 }
             }
-            warp_append_chunks(nch, kstart, k, out, sc + SC_FR + (r + 1) % 3);
+            warp_append_chunks64(nch, kstart, k, out, wn);
         }
         if (trace && blockIdx.x == 0 && threadIdx.x == 0 && r < 4096) trace[3 * r + 1] = lev_gtimer();
-        grid_sync(bar, bar_target);
+        // grid barrier fused with the next frontier's size
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(wn),
+                         "l"(1ull << 32)
+                         : "memory");
+            unsigned long long v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(wn) : "memory");
+                if ((v >> 32) >= gridDim.x) break;
+                __nanosleep(20);
+            }
+            s_size = int(unsigned(v));
+        }
+        __syncthreads();
+        size = s_size;
     }
 }
 
@@ -517,11 +556,13 @@ int64_t levelize_device(Graph &g) {
         HF_CUDA(cudaMemsetAsync(sc + SC_FR + 1, 0, sizeof(int32_t), s));   // round 0 appends here
         const int block = 1024;
         int grid = coop_grid((const void *)k_lev_kahn, block, g.sms, 1);
-        HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(GridBar), s));
+        DevBuf wbuf;   // three 64-bit round words {arrivals | frontier size}
+        wbuf.alloc(sizeof(unsigned long long) * 3, s);
+        HF_CUDA(cudaMemsetAsync(wbuf.p, 0, sizeof(unsigned long long) * 3, s));
         const int32_t *cp = cptr.as<int32_t>(), *cd = cdst.as<int32_t>(), *cwp = cw.as<int32_t>();
         int32_t *cn = cnt.as<int32_t>(), *lv = lev.as<int32_t>();
         int2 *fa = ea.as<int2>(), *fb = eb2.as<int2>();
-        GridBar *barp = bar.as<GridBar>();
+        unsigned long long *wp = wbuf.as<unsigned long long>();
         const char *trace_env = getenv("HF_TRACE");
         DevBuf tb;
         unsigned long long *tr = nullptr;
@@ -530,7 +571,7 @@ int64_t levelize_device(Graph &g) {
             HF_CUDA(cudaMemsetAsync(tb.p, 0, sizeof(unsigned long long) * 3 * 4096, s));
             tr = tb.as<unsigned long long>();
         }
-        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &barp, &tr};
+        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &wp, &tr};
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn, grid, block, args, 0, s));
         g.launches += 1;
         if (trace_env) {
