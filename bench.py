@@ -20,6 +20,7 @@ the timed region.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -289,6 +290,10 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = 0.0
+    # no Python garbage collection inside the timed region (a collection pause would
+    # leave the GPU idle between the step's host round trips)
+    gc.collect()
+    gc.disable()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)                       # L2 flush between timed steps (untimed)
@@ -302,6 +307,7 @@ def main():
             finish(G, True)
             if os.environ.get("HF_BENCH_VERBOSE"):
                 print(f"step {e0.elapsed_time(e1):.3f} ms", file=sys.stderr)
+    gc.enable()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

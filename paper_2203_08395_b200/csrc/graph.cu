@@ -1,5 +1,7 @@
 // graph.cu -- hf_graph_create: validate CSR fan-in, canonicalise delays, derive
 // (or verify) the fan-out CSR and out_eid on the device.  SURVEY.md §8(a) a1.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace hf {
@@ -99,6 +101,20 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
             HF_CUDA(cudaDeviceGetDefaultMemPool(&pool, g.device));
             uint64_t keep = UINT64_MAX;
             HF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+            // map a working set into the pool once (1/8 of the device memory, at most
+            // 24 GiB): later graphs carve their buffers from it instead of growing the
+            // pool (a growth maps new memory: milliseconds on the host, mid-step)
+            size_t free_b = 0, total_b = 0;
+            HF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            const size_t want = std::min<size_t>(total_b / 8, size_t(24) << 30);
+            if (want < free_b / 2) {
+                void *blk = nullptr;
+                if (cudaMallocAsync(&blk, want, s) == cudaSuccess) {
+                    cudaFreeAsync(blk, s);
+                    HF_CUDA(cudaStreamSynchronize(s));
+                }
+                cudaGetLastError();
+            }
             done[g.device] = true;
         }
     }
