@@ -309,6 +309,23 @@ def test_batch_concurrent_passes(hf, S, monkeypatch):
     assert_bits_equal(w, wo, "wns")
 
 
+@pytest.mark.parametrize("knob", ["HF_GA", "HF_POLL_ALL"])
+def test_batch_kernel_variants(hf, knob, monkeypatch):
+    # the measured-and-rejected kernel variants kept as switches:
+    # cp.async gathers into shared memory (HF_GA=1), one-lane polling (HF_POLL_ALL=0)
+    monkeypatch.setenv(knob, "1" if knob == "HF_GA" else "0")
+    S = 64
+    g = hfgen.config("C3", 0.004)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    w, at, rat = gpu_batch_device(hf, g, D, T, S)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                                 want_at_rat=True)
+    assert_bits_equal(at, ato, "at")
+    assert_bits_equal(rat, rato, "rat")
+    assert_bits_equal(w, wo, "wns")
+
+
 def test_batch_host_api_both_layouts(hf):
     g = hfgen.config("C1")
     S = 6
