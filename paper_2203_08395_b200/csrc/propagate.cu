@@ -51,6 +51,9 @@ namespace hf {
 namespace {
 
 constexpr int NWARP = 4;              // warps per CTA
+#ifndef PW_BWD
+#define PW_BWD 4                      // backward: partials of a long neighbour in flight
+#endif
 constexpr int FLOW_THREADS = NWARP * 32;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -438,17 +441,33 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     const int np = __ldg(p.part_np + q0);
 #pragma unroll
                     for (int j = 0; j < V; ++j) a[r].x[j] = ident<MX>();
-                    for (int k = 0; k < np; ++k) {
+                    // PW partials in flight per step (a long row has up to
+                    // ceil(degree / LO_PE) of them; backward rows are the long ones,
+                    // the wide forward kernel keeps one to stay within its register budget)
+                    constexpr int PW = (FWD && V == 4) ? 1 : PW_BWD;
+                    for (int k = 0; k < np; k += PW) {
                         const float *src = p.part_buf + int64_t(q0 + k) * S + col;
-                        Vec<V> v = ld_relaxed<V>(src);
-                        int ns = 32;
-                        while (has_nan<V>(v)) {
-                            __nanosleep(ns);
-                            ns = min(ns * 2, p.sleep_max);
-                            v = ld_relaxed<V>(src);
+                        Vec<V> v[PW];
+#pragma unroll
+                        for (int t = 0; t < PW; ++t) {
+                            if (k + t < np) {
+                                v[t] = ld_relaxed<V>(src + int64_t(t) * S);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < V; ++j) v[t].x[j] = ident<MX>();
+                            }
                         }
 #pragma unroll
-                        for (int j = 0; j < V; ++j) a[r].x[j] = combine<MX>(a[r].x[j], v.x[j]);
+                        for (int t = 0; t < PW; ++t) {
+                            int ns = 32;
+                            while (has_nan<V>(v[t])) {
+                                __nanosleep(ns);
+                                ns = min(ns * 2, p.sleep_max);
+                                v[t] = ld_relaxed<V>(src + int64_t(t) * S);
+                            }
+#pragma unroll
+                            for (int j = 0; j < V; ++j) a[r].x[j] = combine<MX>(a[r].x[j], v[t].x[j]);
+                        }
                     }
                 }
             }
