@@ -243,12 +243,6 @@ hf_status hf_graph_destroy(hf_graph h) {
         cudaStreamSynchronize(g->stream);
         for (auto &e : g->ev)
             if (e) cudaEventDestroy(e);
-        if (g->fork) cudaEventDestroy(g->fork);
-        if (g->join) cudaEventDestroy(g->join);
-        if (g->s2) {
-            cudaStreamSynchronize(g->s2);
-            cudaStreamDestroy(g->s2);
-        }
         delete g;   // DevBufs free stream-ordered
         return HF_OK;
     });

@@ -135,9 +135,6 @@ struct Graph {
     // profiling
     bool prof = false;
     cudaEvent_t ev[8] = {};   // 0/1 levelize, 2/3 forward, 5/4 backward, 6/7 batch phase
-    // second stream + fork/join events of the concurrent batch (propagate.cu)
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
     float ms_lev = 0, ms_fwd = 0, ms_bwd = 0, ms_prop = 0;
     bool lev_timed = false, prop_timed = false;
     int64_t launches = 0;

@@ -380,6 +380,9 @@ __global__ void k_lo_enc(const int32_t *__restrict__ ptr, const int32_t *__restr
          u += int64_t(gridDim.x) * blockDim.x)
         enc[u] = ptr[u + 1] - ptr[u] > LO_SPLIT ? -(q[pos[u]] + 1) : int32_t(u);
 }
+// A warp copies the rows of 32 consecutive output positions as one flattened edge
+// range: every output store is coalesced and every lane does one edge per step (a
+// lane finds its row by a shuffle binary search over the warp's row offsets).
 __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
                                const int32_t *__restrict__ ptr, const int32_t *__restrict__ a,
                                const int32_t *__restrict__ eid_map,
@@ -389,30 +392,37 @@ __global__ void k_relabel_rows(const int32_t *__restrict__ order, int32_t n,
     const int64_t nwarps_total = (int64_t(gridDim.x) * blockDim.x) >> 5;
     for (int64_t wbase = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32;
          wbase < n; wbase += nwarps_total * 32) {
-        int64_t i = wbase + lane;
-        int b = 0, e = 0, o = 0;
+        const int64_t i = wbase + lane;
+        int b = 0, len = 0;
         if (i < n) {
-            int v = order[i];
+            const int v = order[i];
             b = ptr[v];
-            e = ptr[v + 1];
-            o = nptr[i];
+            len = ptr[v + 1] - b;
         }
-        bool longrow = (e - b) >= 32;
-        if (!longrow)
-            for (int k = b; k < e; ++k) {
-                na[o + (k - b)] = enc[a[k]];
-                neid[o + (k - b)] = eid_map ? eid_map[k] : k;
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int excl = incl - len;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int o0 = nptr[wbase];
+        for (int base = 0; base < total; base += 32) {
+            const int p = base + lane;
+            // last row r with excl[r] <= p (empty rows share their successor's offset)
+            int r = 0;
+#pragma unroll
+            for (int st = 16; st; st >>= 1) {
+                const int c = r + st;
+                if (__shfl_sync(0xffffffffu, excl, c) <= p) r = c;
             }
-        unsigned lm = __ballot_sync(0xffffffffu, longrow);
-        while (lm) {
-            int srcl = __ffs(lm) - 1;
-            lm &= lm - 1;
-            int bb = __shfl_sync(0xffffffffu, b, srcl);
-            int ee = __shfl_sync(0xffffffffu, e, srcl);
-            int oo = __shfl_sync(0xffffffffu, o, srcl);
-            for (int k = bb + lane; k < ee; k += 32) {
-                na[oo + (k - bb)] = enc[a[k]];
-                neid[oo + (k - bb)] = eid_map ? eid_map[k] : k;
+            const int er = __shfl_sync(0xffffffffu, excl, r);
+            const int br = __shfl_sync(0xffffffffu, b, r);
+            if (p < total) {
+                const int k = br + (p - er);
+                na[o0 + p] = enc[a[k]];
+                neid[o0 + p] = eid_map ? eid_map[k] : k;
             }
         }
     }

@@ -90,6 +90,12 @@ template <int V> __device__ __forceinline__ void st_relaxed(float *p, const Vec<
         asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v.x[0]) : "memory");
     }
 }
+template <int V> __device__ __forceinline__ Vec<V> nan_vec() {
+    Vec<V> r;
+#pragma unroll
+    for (int j = 0; j < V; ++j) r.x[j] = __int_as_float(-1);   // the all-ones NaN sentinel
+    return r;
+}
 template <int V> __device__ __forceinline__ void st_plain(float *p, const Vec<V> &v) {
     if constexpr (V == 4) {
         *reinterpret_cast<float4 *>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
@@ -175,6 +181,8 @@ struct FlowParams {
     float t_scalar;           // backward: T when t_req is null
     const float *other;       // backward: at (for slack)
     float *out;               // forward: at; backward: rat
+    float *prefill;           // forward, optional: the backward output (rat), NaN-filled
+                              // row by row as the forward writes its own rows
     float *slack;             // backward, optional [n][S]
     int32_t *wns_ord;         // backward: [S] ordered-int minima
     uint32_t *err;
@@ -577,6 +585,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     }
                 }
                 st_relaxed<V>(p.out + int64_t(node) * S + col, best);
+                if (FWD && p.prefill) st_plain<V>(p.prefill + int64_t(node) * S + col, nan_vec<V>());
                 if (!FWD && p.other) {
                     const Vec<V> av = ld_s<V>(s_at + i * SC + gl * V);
                     Vec<V> sl;
@@ -623,7 +632,7 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
                                  int32_t nparts, const int32_t *__restrict__ node_of, int32_t S,
                                  const float *__restrict__ part_buf, float *__restrict__ out,
                                  const float *__restrict__ other, float *__restrict__ slack,
-                                 int32_t *__restrict__ wns_ord) {
+                                 int32_t *__restrict__ wns_ord, float *__restrict__ prefill) {
     constexpr bool MX = FWD != EARLY;
     extern __shared__ int32_t s_wmin[];
     const bool do_slack = !FWD && other;
@@ -660,6 +669,7 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
                         for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v[u].x[j]);
             }
             st_plain<V>(out + node * S + col, acc);
+            if (FWD && prefill) st_plain<V>(prefill + node * S + col, nan_vec<V>());
             if (do_slack) {
                 const Vec<V> a = ld_relaxed<V>(other + node * S + col);
                 Vec<V> sl;
@@ -1021,7 +1031,8 @@ struct PassCtx {
 
 // task schedule, bases, partial buffer and the sentinel fill of the output (on the
 // graph's stream)
-template <bool FWD> void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx) {
+template <bool FWD>
+void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = true) {
     cudaStream_t s = g.stream;
     // scenario chunk: SC = V * LPN columns (largest power of two <= HF_SC dividing S)
     const int sc_max = std::max(1, env_int("HF_SC", 64));
@@ -1067,7 +1078,7 @@ template <bool FWD> void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &c
         g.launches += 1;
     }
     // the NaN sentinel (all-ones bit pattern): "not yet computed"
-    HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
+    if (fill_out) HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
 }
 
 // the dataflow kernel and the long-row finalisation, on stream st
@@ -1085,7 +1096,7 @@ void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cuda
 #define HF_FIN(EE, VV)                                                                    \
     k_finalize_split<FWD, EE, VV><<<grid, 256, sm, st>>>(npa, prow, cx.nparts, p.node_of, p.S, \
                                                           p.part_buf, p.out, p.other, p.slack, \
-                                                          p.wns_ord)
+                                                          p.wns_ord, p.prefill)
         if (g.early) {
             if (V == 4) HF_FIN(true, 4);
             else if (V == 2) HF_FIN(true, 2);
@@ -1204,14 +1215,92 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
 // Measured on C4 (S = 64): slower (1.48 ms vs 1.32 ms for the phase), because each
 // pass then has half the resident warps and the dataflow needs many warps to keep
 // several levels in flight; kept for the record.
+// second stream + fork/join events for the batch, one set per host thread and
+// device, created once and kept for the process (creating them per graph cost
+// ~70 us of host time per create/levelize/batch step)
+struct Side {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static Side &side_of(Graph &g) {
+    thread_local Side sides[64];
+    Side &x = sides[g.device & 63];
+    if (!x.s2) {
+        HF_CUDA(cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking));
+        HF_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+        HF_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+    }
+    return x;
+}
+
 void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                   const float *t_arr, float *at, float *rat, float *slack, float *wns_f) {
     cudaStream_t s = g.stream;
-    if (!env_int("HF_CONCURRENT", 0) || g.n == 0) {
+    if (g.n == 0 || getenv("HF_TRACE") || env_int("HF_BATCH_PLAIN", 0)) {
         prof_record(g, 6);
         forward_device(g, d, S, check_d, at_src, at);
         backward_device(g, d, S, t_arr, 0.0f, at, rat, slack, wns_f);
         prof_record(g, 7);
+        return;
+    }
+    if (!env_int("HF_CONCURRENT", 0)) {
+        // Forward then backward, with the set-up of both passes overlapped: the
+        // sentinel fill of `at` runs on a second stream while this stream builds both
+        // task schedules, and the forward kernel NaN-fills each rat row as it writes
+        // the at row (so the backward needs no fill of its own).
+        Side &sd = side_of(g);
+        prof_record(g, 6);
+        HF_CUDA(cudaEventRecord(sd.fork, s));
+        HF_CUDA(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
+        HF_CUDA(cudaMemsetAsync(at, 0xff, sizeof(float) * size_t(g.n) * S, sd.s2));
+        const bool prefill = env_int("HF_PREFILL", 0) != 0;
+        if (!prefill) HF_CUDA(cudaMemsetAsync(rat, 0xff, sizeof(float) * size_t(g.n) * S, sd.s2));
+        HF_CUDA(cudaEventRecord(sd.join, sd.s2));
+        g.ws_wns.alloc(sizeof(int32_t) * size_t(S), s);
+        int32_t *ord = g.ws_wns.as<int32_t>();
+        k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+        if (t_arr) {
+            k_check_t<<<1, 256, 0, s>>>(t_arr, S, g.d_err());
+            HF_CHECK_LAUNCH();
+            g.launches += 1;
+        }
+        FlowParams pf{}, pb{};
+        const int V = pick_vec(S, {d, at, rat, slack});
+        pf.row_ptr = g.lo_in_ptr.as<int32_t>();
+        pf.nbr = g.lo_in_nbr.as<int32_t>();
+        pf.eid = g.lo_in_eid.as<int32_t>();
+        pf.node_of = g.lo_in_node.as<int32_t>();
+        pf.S = S;
+        pf.d = d;
+        pf.src_val = at_src;
+        pf.out = at;
+        pf.prefill = prefill ? rat : nullptr;
+        pb.row_ptr = g.lo_out_ptr.as<int32_t>();
+        pb.nbr = g.lo_out_nbr.as<int32_t>();
+        pb.eid = g.lo_out_eid.as<int32_t>();
+        pb.node_of = g.lo_out_node.as<int32_t>();
+        pb.S = S;
+        pb.d = d;
+        pb.src_val = t_arr;
+        pb.t_scalar = 0.0f;
+        pb.other = at;
+        pb.out = rat;
+        pb.slack = slack;
+        pb.wns_ord = ord;
+        PassCtx cf, cb;
+        prepare_pass<true>(g, pf, V, cf, false);
+        prepare_pass<false>(g, pb, V, cb, false);
+        HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));
+        launch_pass<true>(g, pf, check_d, V, cf, s, 0);
+        launch_pass<false>(g, pb, false, V, cb, s, 0);
+        prof_record(g, 7);
+        if (wns_f) {
+            k_ord_to_float<<<1, 256, 0, s>>>(ord, wns_f, S);
+            HF_CHECK_LAUNCH();
+            g.launches += 1;
+        }
         return;
     }
     g.ws_wns.alloc(sizeof(int32_t) * size_t(S), s);
@@ -1252,18 +1341,14 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
     const int ob = dispatch<false, false>(g, pb, V, cb.LPN, s, 0, 1);
     const int capf = std::max(1, env_int("HF_CAP_F", (of + 1) / 2));
     const int capb = std::max(1, env_int("HF_CAP_B", ob / 2));
-    if (!g.s2) {
-        HF_CUDA(cudaStreamCreateWithFlags(&g.s2, cudaStreamNonBlocking));
-        HF_CUDA(cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming));
-        HF_CUDA(cudaEventCreateWithFlags(&g.join, cudaEventDisableTiming));
-    }
+    Side &sd = side_of(g);
     prof_record(g, 6);
-    HF_CUDA(cudaEventRecord(g.fork, s));
-    HF_CUDA(cudaStreamWaitEvent(g.s2, g.fork, 0));
-    launch_pass<false>(g, pb, false, V, cb, g.s2, capb);
+    HF_CUDA(cudaEventRecord(sd.fork, s));
+    HF_CUDA(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
+    launch_pass<false>(g, pb, false, V, cb, sd.s2, capb);
     launch_pass<true>(g, pf, check_d, V, cf, s, capf);
-    HF_CUDA(cudaEventRecord(g.join, g.s2));
-    HF_CUDA(cudaStreamWaitEvent(s, g.join, 0));
+    HF_CUDA(cudaEventRecord(sd.join, sd.s2));
+    HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));
     const int lpn = S / V;
     const int grid = grid_for(int64_t(g.n) * lpn, 512, g.sms);
     const size_t sm = sizeof(int32_t) * size_t(S);

@@ -16,7 +16,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhf.so")
+# HF_LIB: an alternative in-tree build (A/B timing of kernel variants in tools/)
+LIB_PATH = os.environ.get("HF_LIB") or os.path.join(_HERE, "libhf.so")
 
 HF_OK, HF_ERR_INVALID_ARG, HF_ERR_BAD_CSR, HF_ERR_CYCLE = 0, 1, 2, 3
 HF_ERR_NOT_LEVELIZED, HF_ERR_OOM, HF_ERR_CUDA, HF_ERR_NCCL = 4, 5, 6, 7
