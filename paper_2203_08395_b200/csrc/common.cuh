@@ -124,10 +124,13 @@ struct Graph {
     TaskSched ts_f, ts_b;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
-    // single-pass scan state (primitives.cu): per-tile words + tile counter
-    DevBuf scan_state;
-    uint64_t scan_base = 0;
-    unsigned scan_epoch = 0;
+    // single-pass scan state (primitives.cu): per-tile words + tile counter; one per
+    // stream that scans concurrently (slot 0: the graph's stream, 1: the side stream)
+    struct ScanState {
+        DevBuf buf;
+        uint64_t base = 0;
+        unsigned epoch = 0;
+    } scan[2];
     // small device scalars: [0] error bits, [1..] scratch
     DevBuf d_small;
     uint32_t *d_err() const { return d_small.as<uint32_t>(); }
@@ -140,10 +143,18 @@ struct Graph {
     int64_t launches = 0;
 };
 
+// second stream + fork/join events, one set per host thread and device, created
+// once and kept for the process (propagate.cu)
+struct Side {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+Side &side_of(Graph &g);
+
 // ---- primitives (primitives.cu) --------------------------------------------
 // exclusive scan of int32 (out may alias in); writes the total to *total_d if non-null
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t count, int32_t *total_d,
-                    cudaStream_t s, Graph &g);
+                    cudaStream_t s, Graph &g, int slot = 0);
 // stable LSD radix sort of (key, value) pairs, keys in [0, 2^key_bits); vals_in
 // NULL => values are 0..count-1.  Results in keys_out / vals_out.
 void radix_sort_pairs(const int32_t *keys_in, const int32_t *vals_in, int32_t *keys_out,

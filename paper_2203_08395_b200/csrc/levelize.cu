@@ -482,8 +482,34 @@ int coop_grid(const void *func, int block, int sms, int cap = 2) {
 
 }  // namespace
 
+// HF_LEV_TIMES=1: per-stage device times of hf_levelize on stderr (tools only)
+struct LevTimes {
+    bool on = getenv("HF_LEV_TIMES") != nullptr;
+    std::vector<std::pair<const char *, cudaEvent_t>> ev;
+    void mark(const char *name, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        HF_CUDA(cudaEventCreate(&e));
+        HF_CUDA(cudaEventRecord(e, s));
+        ev.emplace_back(name, e);
+    }
+    ~LevTimes() {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        std::string line = "levelize stages (us):";
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            line += std::string(" ") + ev[i].first + "=" + std::to_string(int(ms * 1000));
+        }
+        fprintf(stderr, "%s\n", line.c_str());
+        for (auto &x : ev) cudaEventDestroy(x.second);
+    }
+};
+
 // Returns the number of never-ready nodes (0 on success); fills g.level/order/level_ptr.
 int64_t levelize_device(Graph &g) {
+    LevTimes lt;
     cudaStream_t s = g.stream;
     const int32_t n = g.n, m = g.m;
     g.levelized = false;
@@ -499,6 +525,7 @@ int64_t levelize_device(Graph &g) {
         return 0;
     }
     DevBuf pd, cnt, lev, la, lb, bar, skeys, cptr;
+    lt.mark("start", s);
     pd.alloc(sizeof(long long) * n, s);
     cnt.alloc(sizeof(int32_t) * n, s);
     lev.alloc(sizeof(int32_t) * n, s);
@@ -515,6 +542,7 @@ int64_t levelize_device(Graph &g) {
         cnt.as<int32_t>(), lev.as<int32_t>(), la.as<int32_t>(), lb.as<int32_t>(), sc);
     HF_CHECK_LAUNCH();
     g.launches += 2;
+    lt.mark("init", s);
     {
         // pointer jumping: lists la (active) / keys buffer as ping-pong partner
         DevBuf act2;
@@ -529,6 +557,7 @@ int64_t levelize_device(Graph &g) {
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_jump, grid, block, args, 0, s));
         g.launches += 1;
     }
+    lt.mark("jump", s);
     // contracted fan-out of the junctions (counting sort by root)
     DevBuf ccur, cdst, cw;
     cptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
@@ -564,6 +593,7 @@ int64_t levelize_device(Graph &g) {
         HF_CHECK_LAUNCH();
         g.launches += 1;
         HF_CUDA(cudaMemsetAsync(sc + SC_FR + 1, 0, sizeof(int32_t), s));   // round 0 appends here
+        lt.mark("contract+seed", s);
         const int block = 1024;
         int grid = coop_grid((const void *)k_lev_kahn, block, g.sms, 1);
         DevBuf wbuf;   // three 64-bit round words {arrivals | frontier size}
@@ -584,6 +614,7 @@ int64_t levelize_device(Graph &g) {
         void *args[] = {&cp, &cd, &cwp, &cn, &lv, &fa, &fb, &sc, &wp, &tr};
         HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn, grid, block, args, 0, s));
         g.launches += 1;
+        lt.mark("kahn", s);
         if (trace_env) {
             std::vector<unsigned long long> h(3 * 4096);
             HF_CUDA(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -602,6 +633,7 @@ int64_t levelize_device(Graph &g) {
     g.launches += 1;
     int32_t h_sc[16];
     HF_CUDA(cudaMemcpyAsync(h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, s));
+    lt.mark("final", s);
     HF_CUDA(cudaStreamSynchronize(s));
     int64_t unresolved = h_sc[SC_UNRES];
     if (unresolved) return unresolved;
@@ -611,6 +643,7 @@ int64_t levelize_device(Graph &g) {
     radix_sort_pairs(g.level.as<int32_t>(), nullptr, skeys.as<int32_t>(), g.order.as<int32_t>(),
                      n, bits_for(int64_t(L) - 1), s, g);
     keys_to_ptr(skeys.as<int32_t>(), n, L, g.level_ptr.as<int32_t>(), s, g);
+    lt.mark("sync+sort", s);
     // relabel (a4): level-ordered CSR for the propagation passes.
     // Inside a level the rows with degree <= LO_SPLIT come first, then the longer
     // rows (cut into part tasks by the passes); both runs keep canonical order.
@@ -626,53 +659,65 @@ int64_t levelize_device(Graph &g) {
         g.lo_in_eid.alloc(sizeof(int32_t) * mm, s);
         g.lo_out_nbr.alloc(sizeof(int32_t) * mm, s);
         g.lo_out_eid.alloc(sizeof(int32_t) * mm, s);
-        DevBuf flag, fs, deg, parts, pos, enc;
-        flag.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        fs.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        deg.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        parts.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        pos.alloc(sizeof(int32_t) * n, s);
-        enc.alloc(sizeof(int32_t) * n, s);
+        // the two directions are independent: fan-out on the side stream, fan-in here
+        DevBuf flag[2], fs[2], deg[2], parts[2], pos[2], enc[2];
+        const size_t npcap = size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1);
         for (int dir = 0; dir < 2; ++dir) {
+            flag[dir].alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+            fs[dir].alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+            deg[dir].alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+            parts[dir].alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+            pos[dir].alloc(sizeof(int32_t) * n, s);
+            enc[dir].alloc(sizeof(int32_t) * n, s);
+            // parts of every long row, indexed by its first part id (<= m/9 + m/LO_PE ids)
+            (dir == 0 ? g.lo_in_np : g.lo_out_np).alloc(sizeof(int32_t) * npcap * 2, s);
+        }
+        g.np_cap_in = g.np_cap_out = int32_t(npcap);
+        Side &sd = side_of(g);
+        HF_CUDA(cudaEventRecord(sd.fork, s));
+        HF_CUDA(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
+        for (int dir = 1; dir >= 0; --dir) {
             const bool in = dir == 0;
+            cudaStream_t ds = in ? s : sd.s2;
             const int32_t *ptr = in ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>();
             int32_t *lo_node = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
             int32_t *lo_ptr = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
             int32_t *lo_q = in ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
             DevBuf &np = in ? g.lo_in_np : g.lo_out_np;
-            k_lo_flags<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
-                g.order.as<int32_t>(), ptr, n, flag.as<int32_t>());
+            k_lo_flags<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, ds>>>(
+                g.order.as<int32_t>(), ptr, n, flag[dir].as<int32_t>());
             HF_CHECK_LAUNCH();
-            scan_exclusive(flag.as<int32_t>(), fs.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-            k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
+            scan_exclusive(flag[dir].as<int32_t>(), fs[dir].as<int32_t>(), int64_t(n) + 1, nullptr,
+                           ds, g, dir);
+            k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, ds>>>(
                 g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(),
-                fs.as<int32_t>(), flag.as<int32_t>(), ptr, n, lo_node, deg.as<int32_t>(),
-                parts.as<int32_t>(), pos.as<int32_t>());
+                fs[dir].as<int32_t>(), flag[dir].as<int32_t>(), ptr, n, lo_node,
+                deg[dir].as<int32_t>(), parts[dir].as<int32_t>(), pos[dir].as<int32_t>());
             HF_CHECK_LAUNCH();
-            scan_exclusive(deg.as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, s, g);
-            scan_exclusive(parts.as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, s, g);
-            // parts of every long row, indexed by its first part id (<= m/9 + m/LO_PE ids)
-            const size_t npcap = size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1);
-            np.alloc(sizeof(int32_t) * npcap * 2, s);   // [np | row] by first part id
-            HF_CUDA(cudaMemsetAsync(np.p, 0, sizeof(int32_t) * npcap, s));
-            (in ? g.np_cap_in : g.np_cap_out) = int32_t(npcap);
-            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lo_q, n, np.as<int32_t>(),
-                                                            np.as<int32_t>() + npcap);
+            scan_exclusive(deg[dir].as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, ds, g, dir);
+            scan_exclusive(parts[dir].as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, ds, g,
+                           dir);
+            HF_CUDA(cudaMemsetAsync(np.p, 0, sizeof(int32_t) * npcap, ds));
+            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(lo_q, n, np.as<int32_t>(),
+                                                             np.as<int32_t>() + npcap);
             HF_CHECK_LAUNCH();
-            k_lo_enc<<<grid_for(n, 256, g.sms), 256, 0, s>>>(ptr, pos.as<int32_t>(), lo_q, n,
-                                                             enc.as<int32_t>());
+            k_lo_enc<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(ptr, pos[dir].as<int32_t>(), lo_q, n,
+                                                              enc[dir].as<int32_t>());
             HF_CHECK_LAUNCH();
             if (in)
-                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-                    lo_node, n, ptr, g.in_src.as<int32_t>(), nullptr, lo_ptr, enc.as<int32_t>(),
-                    g.lo_in_nbr.as<int32_t>(), g.lo_in_eid.as<int32_t>());
+                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(
+                    lo_node, n, ptr, g.in_src.as<int32_t>(), nullptr, lo_ptr,
+                    enc[dir].as<int32_t>(), g.lo_in_nbr.as<int32_t>(), g.lo_in_eid.as<int32_t>());
             else
-                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+                k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(
                     lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
-                    enc.as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
+                    enc[dir].as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
             g.launches += 4;
         }
+        HF_CUDA(cudaEventRecord(sd.join, sd.s2));
+        HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));   // before the scratch is freed on s
+        lt.mark("relabel", s);
     }
     // no second host round trip: the passes size the part buffers by the bound
     // np_cap and read the exact part counts (sc[12], sc[13]) on the device

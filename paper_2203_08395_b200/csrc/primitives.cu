@@ -240,7 +240,7 @@ __global__ void k_row_ids(const int32_t *__restrict__ ptr, int32_t nrows,
 }  // namespace
 
 void scan_exclusive(const int32_t *in, int32_t *out, int64_t count, int32_t *total_d,
-                    cudaStream_t s, Graph &g) {
+                    cudaStream_t s, Graph &g, int slot) {
     if (count <= 0) {
         if (total_d) HF_CUDA(cudaMemsetAsync(total_d, 0, sizeof(int32_t), s));
         return;
@@ -248,24 +248,25 @@ void scan_exclusive(const int32_t *in, int32_t *out, int64_t count, int32_t *tot
     const int64_t tiles = (count + LB_TILE - 1) / LB_TILE;
     // look-back state: one word per tile + the tile counter, zeroed once on growth
     const size_t need = sizeof(unsigned long long) * size_t(tiles + 1);
-    if (g.scan_state.bytes < need || g.scan_state.s != s) {
-        g.scan_state.alloc(std::max(need, size_t(8) << 12), s);
-        HF_CUDA(cudaMemsetAsync(g.scan_state.p, 0, g.scan_state.bytes, s));
-        g.scan_base = 0;
-        g.scan_epoch = 0;
+    Graph::ScanState &ss = g.scan[slot];
+    if (ss.buf.bytes < need || ss.buf.s != s) {
+        ss.buf.alloc(std::max(need, size_t(8) << 12), s);
+        HF_CUDA(cudaMemsetAsync(ss.buf.p, 0, ss.buf.bytes, s));
+        ss.base = 0;
+        ss.epoch = 0;
     }
-    if (++g.scan_epoch >= (1u << 29)) {   // tag overflow: start over from a clean state
-        HF_CUDA(cudaMemsetAsync(g.scan_state.p, 0, g.scan_state.bytes, s));
-        g.scan_base = 0;
-        g.scan_epoch = 1;
+    if (++ss.epoch >= (1u << 29)) {   // tag overflow: start over from a clean state
+        HF_CUDA(cudaMemsetAsync(ss.buf.p, 0, ss.buf.bytes, s));
+        ss.base = 0;
+        ss.epoch = 1;
     }
-    unsigned long long *st = g.scan_state.as<unsigned long long>();
+    unsigned long long *st = ss.buf.as<unsigned long long>();
     unsigned *ctr = reinterpret_cast<unsigned *>(st);   // word 0 is the tile counter
     k_scan_lookback<<<unsigned(tiles), LB_BLOCK, 0, s>>>(in, out, count, st + 1, ctr,
-                                                         unsigned(g.scan_base), g.scan_epoch,
+                                                         unsigned(ss.base), ss.epoch,
                                                          total_d);
     HF_CHECK_LAUNCH();
-    g.scan_base += uint64_t(tiles);
+    ss.base += uint64_t(tiles);
     g.launches += 1;
 }
 

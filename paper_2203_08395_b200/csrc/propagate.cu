@@ -1215,14 +1215,8 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
 // Measured on C4 (S = 64): slower (1.48 ms vs 1.32 ms for the phase), because each
 // pass then has half the resident warps and the dataflow needs many warps to keep
 // several levels in flight; kept for the record.
-// second stream + fork/join events for the batch, one set per host thread and
-// device, created once and kept for the process (creating them per graph cost
-// ~70 us of host time per create/levelize/batch step)
-struct Side {
-    cudaStream_t s2 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-static Side &side_of(Graph &g) {
+// (creating the side stream per graph cost ~70 us of host time per step)
+Side &side_of(Graph &g) {
     thread_local Side sides[64];
     Side &x = sides[g.device & 63];
     if (!x.s2) {
