@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -112,6 +114,8 @@ struct Graph {
     // run in canonical order (per direction): node ids lo_in_node / lo_out_node.
     DevBuf lo_in_node, lo_in_ptr, lo_in_nbr, lo_in_eid, lo_in_q, lo_in_np;
     DevBuf lo_out_node, lo_out_ptr, lo_out_nbr, lo_out_eid, lo_out_q, lo_out_np;
+    // [L] first long row of every level (= level end when the level has none)
+    DevBuf lo_in_lstart, lo_out_lstart;
     // lo_*_nbr: neighbour node id, or -(first part id + 1) when the neighbour's own
     // row (same direction) is long; lo_*_q: [n+1] first part id of every row;
     // lo_*_np: parts of the long row whose first part id is the index, then that row
@@ -150,6 +154,34 @@ struct Side {
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 Side &side_of(Graph &g);
+
+// Per-stage device times on stderr when the environment variable `env` is set
+// (tools only: HF_LEV_TIMES in levelize, HF_PROP_TIMES in the batch).
+struct StageTimes {
+    const char *title;
+    bool on;
+    std::vector<std::pair<const char *, cudaEvent_t>> ev;
+    StageTimes(const char *env, const char *t) : title(t), on(getenv(env) != nullptr) {}
+    void mark(const char *name, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, s);
+        ev.emplace_back(name, e);
+    }
+    ~StageTimes() {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back().second);
+        std::string line = std::string(title) + " stages (us):";
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+            line += std::string(" ") + ev[i].first + "=" + std::to_string(int(ms * 1000));
+        }
+        fprintf(stderr, "%s\n", line.c_str());
+        for (auto &x : ev) cudaEventDestroy(x.second);
+    }
+};
 
 // ---- primitives (primitives.cu) --------------------------------------------
 // exclusive scan of int32 (out may alias in); writes the total to *total_d if non-null

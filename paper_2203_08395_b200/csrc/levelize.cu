@@ -358,6 +358,14 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
         pos_of[v] = pos;
     }
 }
+// first long row of every level: level end minus the level's long-row count
+__global__ void k_lo_lstart(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ fs,
+                            int32_t L, int32_t *__restrict__ lstart) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+        const int ls = level_ptr[k], le = level_ptr[k + 1];
+        lstart[k] = le - (fs[le] - fs[ls]);
+    }
+}
 // parts of every long row, stored at its first part id
 __global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__restrict__ np,
                         int32_t *__restrict__ prow) {
@@ -482,34 +490,9 @@ int coop_grid(const void *func, int block, int sms, int cap = 2) {
 
 }  // namespace
 
-// HF_LEV_TIMES=1: per-stage device times of hf_levelize on stderr (tools only)
-struct LevTimes {
-    bool on = getenv("HF_LEV_TIMES") != nullptr;
-    std::vector<std::pair<const char *, cudaEvent_t>> ev;
-    void mark(const char *name, cudaStream_t s) {
-        if (!on) return;
-        cudaEvent_t e;
-        HF_CUDA(cudaEventCreate(&e));
-        HF_CUDA(cudaEventRecord(e, s));
-        ev.emplace_back(name, e);
-    }
-    ~LevTimes() {
-        if (!on || ev.empty()) return;
-        cudaEventSynchronize(ev.back().second);
-        std::string line = "levelize stages (us):";
-        for (size_t i = 1; i < ev.size(); ++i) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
-            line += std::string(" ") + ev[i].first + "=" + std::to_string(int(ms * 1000));
-        }
-        fprintf(stderr, "%s\n", line.c_str());
-        for (auto &x : ev) cudaEventDestroy(x.second);
-    }
-};
-
 // Returns the number of never-ready nodes (0 on success); fills g.level/order/level_ptr.
 int64_t levelize_device(Graph &g) {
-    LevTimes lt;
+    StageTimes lt("HF_LEV_TIMES", "levelize");
     cudaStream_t s = g.stream;
     const int32_t n = g.n, m = g.m;
     g.levelized = false;
@@ -671,6 +654,7 @@ int64_t levelize_device(Graph &g) {
             enc[dir].alloc(sizeof(int32_t) * n, s);
             // parts of every long row, indexed by its first part id (<= m/9 + m/LO_PE ids)
             (dir == 0 ? g.lo_in_np : g.lo_out_np).alloc(sizeof(int32_t) * npcap * 2, s);
+            (dir == 0 ? g.lo_in_lstart : g.lo_out_lstart).alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
         }
         g.np_cap_in = g.np_cap_out = int32_t(npcap);
         Side &sd = side_of(g);
@@ -689,6 +673,11 @@ int64_t levelize_device(Graph &g) {
             HF_CHECK_LAUNCH();
             scan_exclusive(flag[dir].as<int32_t>(), fs[dir].as<int32_t>(), int64_t(n) + 1, nullptr,
                            ds, g, dir);
+            DevBuf &lst = in ? g.lo_in_lstart : g.lo_out_lstart;
+            k_lo_lstart<<<grid_for(L, 256, g.sms), 256, 0, ds>>>(g.level_ptr.as<int32_t>(),
+                                                                fs[dir].as<int32_t>(), L,
+                                                                lst.as<int32_t>());
+            HF_CHECK_LAUNCH();
             k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, ds>>>(
                 g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(),
                 fs[dir].as<int32_t>(), flag[dir].as<int32_t>(), ptr, n, lo_node,
@@ -713,7 +702,7 @@ int64_t levelize_device(Graph &g) {
                     lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
                     enc[dir].as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
-            g.launches += 4;
+            g.launches += 5;
         }
         HF_CUDA(cudaEventRecord(sd.join, sd.s2));
         HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));   // before the scratch is freed on s

@@ -776,39 +776,144 @@ __global__ void k_slack_wns(const float *__restrict__ at, const float *__restric
 // floor(prefix of its last short row / tw) + 1 normal tasks (some may be empty when
 // one row spans several multiples of tw).  Long row i becomes parts q[i]..q[i+1]-1
 // of <= LO_PE edges.
-__global__ void k_tb_count(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ Q,
-                           const int32_t *__restrict__ row_ptr, int32_t L, int32_t tw,
-                           int32_t fwd, int32_t *__restrict__ nt, int32_t *__restrict__ ntn,
-                           int32_t *__restrict__ lonorm) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
-        const int ls = level_ptr[k], le = level_ptr[k + 1];
-        int lo = ls, hi = le;   // first long row
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (row_ptr[mid + 1] - row_ptr[mid] > LO_SPLIT) hi = mid;
-            else lo = mid + 1;
+// Per-level task counts and their prefix sums in one block (L is small): pass-level
+// q = k (forward) or L-1-k (backward) has nt[q] = ntn + parts tasks per chunk,
+// ntn = ceil-ish(weight of its short rows / tw); doff = exclusive scan of nt (the
+// first descriptor of q), tb = exclusive scan of nt * nch (first global task of q).
+__global__ void __launch_bounds__(1024) k_tb_sched(
+    const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ lstart,
+    const int32_t *__restrict__ Q, const int32_t *__restrict__ row_ptr, int32_t L, int32_t tw,
+    int32_t fwd, int32_t nch, int32_t *__restrict__ nt, int32_t *__restrict__ ntn,
+    int32_t *__restrict__ doff, int32_t *__restrict__ tb) {
+    __shared__ int warp_a[32], warp_b[32];
+    __shared__ int carry_a, carry_b;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry_a = carry_b = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < L; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        int a = 0;
+        if (q < L) {
+            const int k = fwd ? q : L - 1 - q;
+            const int ls = level_ptr[k], le = level_ptr[k + 1], lo = lstart[k];
+            const int c = lo > ls ? ((row_ptr[lo - 1] - row_ptr[ls]) + (lo - 1 - ls)) / tw + 1 : 0;
+            ntn[k] = c;
+            a = c + (Q[le] - Q[ls]);
+            nt[q] = a;
         }
-        const int c = lo > ls ? ((row_ptr[lo - 1] - row_ptr[ls]) + (lo - 1 - ls)) / tw + 1 : 0;
-        ntn[k] = c;
-        lonorm[k] = lo;
-        nt[fwd ? k : L - 1 - k] = c + (Q[le] - Q[ls]);
+        int xa = a, xb = a * nch;
+        const int va = xa, vb = xb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ya = __shfl_up_sync(0xffffffffu, xa, o);
+            const int yb = __shfl_up_sync(0xffffffffu, xb, o);
+            if (lane >= o) {
+                xa += ya;
+                xb += yb;
+            }
+        }
+        if (lane == 31) {
+            warp_a[wid] = xa;
+            warp_b[wid] = xb;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            int sa = lane < nw ? warp_a[lane] : 0, sb = lane < nw ? warp_b[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ya = __shfl_up_sync(0xffffffffu, sa, o);
+                const int yb = __shfl_up_sync(0xffffffffu, sb, o);
+                if (lane >= o) {
+                    sa += ya;
+                    sb += yb;
+                }
+            }
+            if (lane < nw) {
+                warp_a[lane] = sa;
+                warp_b[lane] = sb;
+            }
+        }
+        __syncthreads();
+        const int ba = carry_a + (wid ? warp_a[wid - 1] : 0) + xa - va;
+        const int bb = carry_b + (wid ? warp_b[wid - 1] : 0) + xb - vb;
+        if (q < L) {
+            doff[q] = ba;
+            tb[q] = bb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry_a += warp_a[nw - 1];
+            carry_b += warp_b[nw - 1];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        nt[L] = 0;
+        doff[L] = carry_a;
+        tb[L] = carry_b;
     }
 }
-// row i (> level start) starts every task j with P(i-1) < j*tw <= P(i) and ends
-// task j - 1 (P = weight prefix); one thread per row, no search
-__global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ row_ptr,
+// task-base prefix only (a cached schedule used with another chunk count)
+__global__ void __launch_bounds__(1024) k_tb_bases(const int32_t *__restrict__ nt, int32_t L,
+                                                   int32_t nch, int32_t *__restrict__ tb) {
+    __shared__ int warp_b[32];
+    __shared__ int carry_b;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry_b = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < L; q0 += blockDim.x) {
+        const int q = q0 + threadIdx.x;
+        const int vb = q < L ? nt[q] * nch : 0;
+        int xb = vb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yb = __shfl_up_sync(0xffffffffu, xb, o);
+            if (lane >= o) xb += yb;
+        }
+        if (lane == 31) warp_b[wid] = xb;
+        __syncthreads();
+        if (wid == 0) {
+            int sb = lane < nw ? warp_b[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int yb = __shfl_up_sync(0xffffffffu, sb, o);
+                if (lane >= o) sb += yb;
+            }
+            if (lane < nw) warp_b[lane] = sb;
+        }
+        __syncthreads();
+        if (q < L) tb[q] = carry_b + (wid ? warp_b[wid - 1] : 0) + xb - vb;
+        __syncthreads();
+        if (threadIdx.x == 0) carry_b += warp_b[nw - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tb[L] = carry_b;
+}
+// Descriptors, one thread per row.  A short row i (> level start) starts every task
+// j with P(i-1) < j*tw <= P(i) and ends task j - 1 (P = weight prefix of the
+// level's short rows); a long row writes its part tasks after the level's ntn.
+__global__ void k_tb_rows(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ row_ptr,
                           const int32_t *__restrict__ doff, const int32_t *__restrict__ ntn,
-                          const int32_t *__restrict__ lonorm, const int32_t *__restrict__ level,
-                          const int32_t *__restrict__ node_of, int32_t n, int32_t L, int32_t tw,
-                          int32_t fwd, int4 *__restrict__ desc) {
+                          const int32_t *__restrict__ lstart, const int32_t *__restrict__ Q,
+                          const int32_t *__restrict__ level, const int32_t *__restrict__ node_of,
+                          int32_t n, int32_t L, int32_t tw, int32_t fwd, int4 *__restrict__ desc) {
     for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < n;
          ii += int64_t(gridDim.x) * blockDim.x) {
         const int i = int(ii);
         const int k = level[node_of[i]];
-        const int ls = level_ptr[k], lo = lonorm[k];
-        if (i >= lo) continue;   // long row: part tasks
-        int *d = reinterpret_cast<int *>(desc + doff[fwd ? k : L - 1 - k]);
+        const int ls = level_ptr[k], lo = lstart[k];
+        const int d0 = doff[fwd ? k : L - 1 - k];
         const int nn = ntn[k];
+        if (i >= lo) {   // long row: its part tasks
+            const int q0 = Q[i], np = Q[i + 1] - q0;
+            const int rb = row_ptr[i], re = row_ptr[i + 1];
+            const int base = d0 + nn + (q0 - Q[ls]);
+            for (int t = 0; t < np; ++t)
+                desc[base + t] = make_int4(i, -(q0 + t + 1), rb + t * LO_PE,
+                                           min(re, rb + (t + 1) * LO_PE));
+            continue;
+        }
+        int *d = reinterpret_cast<int *>(desc + d0);
         const int r0 = row_ptr[ls];
         const int rp = row_ptr[i];
         if (i == ls) {
@@ -831,75 +936,39 @@ __global__ void k_tb_fill(const int32_t *__restrict__ level_ptr, const int32_t *
         }
     }
 }
-__global__ void k_tb_parts(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
-                           const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
-                           const int32_t *__restrict__ Q, const int32_t *__restrict__ doff,
-                           const int32_t *__restrict__ ntn, int32_t n, int32_t L, int32_t fwd,
-                           int4 *__restrict__ desc) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int q0 = Q[i], np = Q[i + 1] - q0;
-        if (np == 0) continue;
-        const int rb = row_ptr[i], re = row_ptr[i + 1];
-        const int k = level[node_of[i]];
-        const int base = doff[fwd ? k : L - 1 - k] + ntn[k] + (q0 - Q[level_ptr[k]]);
-        for (int t = 0; t < np; ++t)
-            desc[base + t] = make_int4(int(i), -(q0 + t + 1), rb + t * LO_PE,
-                                       min(re, rb + (t + 1) * LO_PE));
-    }
-}
-__global__ void k_tb_base(const int32_t *__restrict__ nt, int32_t L, int32_t nch,
-                          int32_t *__restrict__ x) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x)
-        x[k] = nt[k] * nch;
-}
 
-// no host round trip: descriptors are sized by the bound (n + m)/tw + L + parts
+// no host round trip: descriptors are sized by the bound (n + m)/tw + L + parts.
+// Two launches: the per-level counts and prefixes (one block), the descriptors.
 template <bool FWD>
 void build_tasks(Graph &g, const int32_t *row_ptr, const int32_t *node_of, const int32_t *Q,
-                 int32_t nparts, int tw, TaskSched &ts) {
+                 int32_t nparts, int tw, int nch, TaskSched &ts) {
     cudaStream_t s = g.stream;
     const int32_t n = g.n, L = g.L, m = g.m;
-    DevBuf ntn, lonorm;
+    const int32_t *lst = FWD ? g.lo_in_lstart.as<int32_t>() : g.lo_out_lstart.as<int32_t>();
+    DevBuf ntn;
     ntn.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    lonorm.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     ts.nt.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
     ts.doff.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    HF_CUDA(cudaMemsetAsync(ts.nt.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_tb_count<<<grid_for(L, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), Q, row_ptr, L, tw, FWD ? 1 : 0, ts.nt.as<int32_t>(),
-        ntn.as<int32_t>(), lonorm.as<int32_t>());
+    ts.tb.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
+    k_tb_sched<<<1, 1024, 0, s>>>(g.level_ptr.as<int32_t>(), lst, Q, row_ptr, L, tw, FWD ? 1 : 0,
+                                  nch, ts.nt.as<int32_t>(), ntn.as<int32_t>(),
+                                  ts.doff.as<int32_t>(), ts.tb.as<int32_t>());
     HF_CHECK_LAUNCH();
-    scan_exclusive(ts.nt.as<int32_t>(), ts.doff.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
     const int64_t cap = (int64_t(n) + m) / tw + L + nparts + 1;
     ts.desc.alloc(sizeof(int4) * size_t(cap), s);
-    k_tb_fill<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-        g.level_ptr.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(), ntn.as<int32_t>(),
-        lonorm.as<int32_t>(), g.level.as<int32_t>(), node_of, n, L, tw, FWD ? 1 : 0,
-        ts.desc.as<int4>());
+    k_tb_rows<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
+        g.level_ptr.as<int32_t>(), row_ptr, ts.doff.as<int32_t>(), ntn.as<int32_t>(), lst, Q,
+        g.level.as<int32_t>(), node_of, n, L, tw, FWD ? 1 : 0, ts.desc.as<int4>());
     HF_CHECK_LAUNCH();
     g.launches += 2;
-    if (nparts > 0) {
-        k_tb_parts<<<grid_for(n, 256, g.sms), 256, 0, s>>>(
-            row_ptr, node_of, g.level.as<int32_t>(), g.level_ptr.as<int32_t>(), Q,
-            ts.doff.as<int32_t>(), ntn.as<int32_t>(), n, L, FWD ? 1 : 0, ts.desc.as<int4>());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
-    }
-    ts.tb_nch = -1;
+    ts.tb_nch = nch;
 }
 
 void task_bases(Graph &g, TaskSched &ts, int nch) {
     if (ts.tb_nch == nch) return;
     cudaStream_t s = g.stream;
-    const int32_t L = g.L;
-    DevBuf x;
-    x.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    ts.tb.alloc(sizeof(int32_t) * (int64_t(L) + 1), s);
-    HF_CUDA(cudaMemsetAsync(x.as<int32_t>() + L, 0, sizeof(int32_t), s));
-    k_tb_base<<<grid_for(L, 256, g.sms), 256, 0, s>>>(ts.nt.as<int32_t>(), L, nch, x.as<int32_t>());
+    k_tb_bases<<<1, 1024, 0, s>>>(ts.nt.as<int32_t>(), g.L, nch, ts.tb.as<int32_t>());
     HF_CHECK_LAUNCH();
-    scan_exclusive(x.as<int32_t>(), ts.tb.as<int32_t>(), int64_t(L) + 1, nullptr, s, g);
     g.launches += 1;
     ts.tb_nch = nch;
 }
@@ -1057,7 +1126,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     const int32_t *nparts_dev = g.nparts_d + (FWD ? 0 : 1);
     cx.Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
     if (ts.key != tw || !ts.desc.p) {
-        build_tasks<FWD>(g, p.row_ptr, p.node_of, cx.Q, cx.nparts, tw, ts);
+        build_tasks<FWD>(g, p.row_ptr, p.node_of, cx.Q, cx.nparts, tw, p.nch, ts);
         ts.key = tw;
     }
     task_bases(g, ts, p.nch);
@@ -1243,6 +1312,8 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
         // task schedules, and the forward kernel NaN-fills each rat row as it writes
         // the at row (so the backward needs no fill of its own).
         Side &sd = side_of(g);
+        StageTimes pt("HF_PROP_TIMES", "batch");
+        pt.mark("start", s);
         prof_record(g, 6);
         HF_CUDA(cudaEventRecord(sd.fork, s));
         HF_CUDA(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
@@ -1286,9 +1357,13 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
         PassCtx cf, cb;
         prepare_pass<true>(g, pf, V, cf, false);
         prepare_pass<false>(g, pb, V, cb, false);
+        pt.mark("build_tasks", s);
         HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));
+        pt.mark("fills", s);
         launch_pass<true>(g, pf, check_d, V, cf, s, 0);
+        pt.mark("forward+finalize", s);
         launch_pass<false>(g, pb, false, V, cb, s, 0);
+        pt.mark("backward+finalize", s);
         prof_record(g, 7);
         if (wns_f) {
             k_ord_to_float<<<1, 256, 0, s>>>(ord, wns_f, S);
