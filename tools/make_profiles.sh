@@ -23,4 +23,7 @@ python tools/trace_report.py $OUT/tr/c3_fwd_S1.bin $OUT/tr/c3_bwd_S1.bin $OUT/tr
     $OUT/tr/c3_bwd_S64.bin > $OUT/trace_C3.txt 2>&1
 python tools/kahn_report.py $OUT/tr/c3_kahn.bin > $OUT/kahn_C3.txt 2>&1
 rm -f $OUT/tr/*.bin
+# warm per-stage device times of the levelizer and the batch (CUDA events per stage)
+HF_LEV_TIMES=1 HF_PROP_TIMES=1 timeout 200 python bench.py --steps 5 --warmup 3 2>&1 \
+    | grep stages | tail -2 > $OUT/stages.txt
 echo done
