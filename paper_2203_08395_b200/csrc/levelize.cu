@@ -83,13 +83,36 @@ __device__ __forceinline__ void warp_append(bool pred, int item, int *list, int 
 //          [6] unresolved count, [7] max level, [8] visited junctions
 enum { SC_ACT = 0, SC_FR = 3, SC_UNRES = 6, SC_MAXLV = 7, SC_VIS = 8 };
 
+// block-aggregated append of `item` when `pred`: one global atomic per block and
+// call instead of one per warp (all threads of the block must call; s_w[33] shared)
+__device__ __forceinline__ void block_append(bool pred, int item, int *list, int *count, int *s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) s_w[wid] = __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            const int c = s_w[w];
+            s_w[w] = tot;
+            tot += c;
+        }
+        s_w[32] = tot ? atomicAdd(count, tot) : 0;
+    }
+    __syncthreads();
+    if (pred) list[s_w[32] + s_w[wid] + __popc(mask & ((1u << lane) - 1u))] = item;
+    __syncthreads();   // s_w is reused by the next call
+}
+
 __global__ void k_lev_init(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
                            int32_t n, long long *__restrict__ pd, int32_t *__restrict__ cnt,
                            int32_t *__restrict__ lev, int32_t *__restrict__ active,
                            int32_t *__restrict__ frontier, int32_t *sc) {
+    __shared__ int s_w[33];
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t nround = (int64_t(n) + 31) / 32 * 32;   // warp-uniform trip count
-    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < nround; v += stride) {
+    // block-uniform trip count (block_append synchronises the block)
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
         bool in = v < n;
         int deg = 0;
         if (in) {
@@ -99,8 +122,8 @@ __global__ void k_lev_init(const int32_t *__restrict__ in_ptr, const int32_t *__
             cnt[v] = deg;
             lev[v] = 0;
         }
-        warp_append(in && deg == 1, int(v), active, sc + SC_ACT + 0);
-        warp_append(in && deg == 0, int(v), frontier, sc + SC_FR + 1);
+        block_append(in && deg == 1, int(v), active, sc + SC_ACT + 0, s_w);
+        block_append(in && deg == 0, int(v), frontier, sc + SC_FR + 1, s_w);
     }
 }
 
@@ -114,6 +137,7 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
     // warp-granular interleave across SMs (a warp stays contiguous for coalescing)
     const int64_t tid = (int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
     int32_t *lists[2] = {act_a, act_b};
+    __shared__ int s_w[33];
     unsigned bar_target = 0;
     for (int r = 0; r < max_rounds; ++r) {
         volatile int32_t *vsc = sc;
@@ -122,8 +146,10 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
         if (tid == 0) vsc[SC_ACT + (r + 2) % 3] = 0;
         const int32_t *in = lists[r & 1];
         int32_t *out = lists[(r + 1) & 1];
-        const int64_t lim = (int64_t(size) + 31) / 32 * 32;
-        for (int64_t i = tid; i < lim; i += nthreads) {
+        // block-uniform trip count (block_append synchronises the block)
+        const int64_t iters = (int64_t(size) + nthreads - 1) / nthreads;
+        for (int64_t it = 0; it < iters; ++it) {
+            const int64_t i = tid + it * nthreads;
             bool keep = false;
             int v = 0;
             if (i < size) {
@@ -135,7 +161,7 @@ __global__ void k_lev_jump(long long *__restrict__ pd, int32_t *__restrict__ act
                     keep = true;
                 }
             }
-            warp_append(keep, v, out, sc + SC_ACT + (r + 1) % 3);
+            block_append(keep, v, out, sc + SC_ACT + (r + 1) % 3, s_w);
         }
         grid_sync(bar, bar_target);
     }
@@ -286,32 +312,33 @@ __device__ __forceinline__ int contracted_root(const int32_t *in_ptr, const long
     return r;
 }
 
+// count pass: every contracted edge takes its slot in its root's row (the atomic's
+// old value) and remembers {root, slot} and its weight, so the scatter pass is a
+// sequential read plus one store per edge
 __global__ void k_lev_ccount(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
                              const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
-                             int32_t m, int32_t *__restrict__ ccnt) {
+                             int32_t m, int32_t *__restrict__ ccnt, int2 *__restrict__ eslot,
+                             int32_t *__restrict__ ew) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
-        int w;
-        int r = contracted_root(in_ptr, pd, in_dst[e], in_src[e], w);
-        if (r >= 0) atomicAdd(ccnt + r, 1);
+        int w = 0;
+        const int r = contracted_root(in_ptr, pd, in_dst[e], in_src[e], w);
+        eslot[e] = make_int2(r, r >= 0 ? atomicAdd(ccnt + r, 1) : 0);
+        ew[e] = w;
     }
 }
 
-__global__ void k_lev_cscatter(const int32_t *__restrict__ in_ptr,
-                               const int32_t *__restrict__ in_src,
-                               const int32_t *__restrict__ in_dst, const long long *__restrict__ pd,
-                               int32_t m, const int32_t *__restrict__ cptr,
-                               int32_t *__restrict__ ccur, int32_t *__restrict__ cdst,
+__global__ void k_lev_cscatter(const int32_t *__restrict__ in_dst, const int2 *__restrict__ eslot,
+                               const int32_t *__restrict__ ew, int32_t m,
+                               const int32_t *__restrict__ cptr, int32_t *__restrict__ cdst,
                                int32_t *__restrict__ cw) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
-        int w;
-        int j = in_dst[e];
-        int r = contracted_root(in_ptr, pd, j, in_src[e], w);
-        if (r >= 0) {
-            int k = cptr[r] + atomicAdd(ccur + r, 1);
-            cdst[k] = j;
-            cw[k] = w;
+        const int2 rs = eslot[e];
+        if (rs.x >= 0) {
+            const int k = cptr[rs.x] + rs.y;
+            cdst[k] = in_dst[e];
+            cw[k] = ew[e];
         }
     }
 }
@@ -454,11 +481,23 @@ __global__ void k_lev_final(const long long *__restrict__ pd, const int32_t *__r
         if (lv < 0) ++unres;
         mx = max(mx, lv);
     }
+    // one atomic per block (per-warp atomics on one address serialise)
+    __shared__ int s_un, s_mx;
+    if (threadIdx.x == 0) {
+        s_un = 0;
+        s_mx = -1;
+    }
+    __syncthreads();
     unres = __reduce_add_sync(0xffffffffu, unres);
     mx = __reduce_max_sync(0xffffffffu, mx);
     if ((threadIdx.x & 31) == 0) {
-        if (unres) atomicAdd(sc + SC_UNRES, unres);
-        atomicMax(sc + SC_MAXLV, mx);
+        if (unres) atomicAdd(&s_un, unres);
+        atomicMax(&s_mx, mx);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_un) atomicAdd(sc + SC_UNRES, s_un);
+        atomicMax(sc + SC_MAXLV, s_mx);
     }
 }
 
@@ -548,22 +587,25 @@ int64_t levelize_device(Graph &g) {
     cdst.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
     cw.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
     HF_CUDA(cudaMemsetAsync(ccur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
-    if (m) {
-        k_lev_ccount<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
-            g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
-            pd.as<long long>(), m, ccur.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
-    }
-    scan_exclusive(ccur.as<int32_t>(), cptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-    HF_CUDA(cudaMemsetAsync(ccur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
-    if (m) {
-        k_lev_cscatter<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
-            g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
-            pd.as<long long>(), m, cptr.as<int32_t>(), ccur.as<int32_t>(), cdst.as<int32_t>(),
-            cw.as<int32_t>());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
+    {
+        DevBuf eslot, ew;
+        eslot.alloc(sizeof(int2) * int64_t(m > 0 ? m : 1), s);
+        ew.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
+        if (m) {
+            k_lev_ccount<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+                g.in_ptr.as<int32_t>(), g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(),
+                pd.as<long long>(), m, ccur.as<int32_t>(), eslot.as<int2>(), ew.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            g.launches += 1;
+        }
+        scan_exclusive(ccur.as<int32_t>(), cptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+        if (m) {
+            k_lev_cscatter<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+                g.in_dst.as<int32_t>(), eslot.as<int2>(), ew.as<int32_t>(), m, cptr.as<int32_t>(),
+                cdst.as<int32_t>(), cw.as<int32_t>());
+            HF_CHECK_LAUNCH();
+            g.launches += 1;
+        }
     }
     {
         // frontier entries {first contracted edge, node}: at most n + m/KCH per round
