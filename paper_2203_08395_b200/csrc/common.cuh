@@ -213,6 +213,27 @@ inline int grid_for(int64_t work, int block, int sms, int per_sm = 8) {
 }
 
 // ---- device helpers --------------------------------------------------------
+// block-aggregated append of `item` when `pred`: one global atomic per block and
+// call instead of one per warp (all threads of the block must call; s_w[33] shared)
+__device__ __forceinline__ void block_append(bool pred, int item, int *list, int *count, int *s_w) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) s_w[wid] = __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            const int c = s_w[w];
+            s_w[w] = tot;
+            tot += c;
+        }
+        s_w[32] = tot ? atomicAdd(count, tot) : 0;
+    }
+    __syncthreads();
+    if (pred) list[s_w[32] + s_w[wid] + __popc(mask & ((1u << lane) - 1u))] = item;
+    __syncthreads();   // s_w is reused by the next call
+}
+
 // float <-> order-preserving int32 (reading R9): signed compare of the keys
 // orders all non-NaN floats; the map is an involution.
 __device__ __forceinline__ int32_t f2ord(float f) {

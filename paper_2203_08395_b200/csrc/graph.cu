@@ -48,21 +48,22 @@ __global__ void k_check_fanout(const int32_t *__restrict__ ptr, const int32_t *_
     if (bits) atomicOr(err, bits);
 }
 
-__global__ void k_count_keys(const int32_t *__restrict__ keys, int64_t count,
-                             int32_t *__restrict__ cnt) {
+// count pass of the fan-out counting sort: every edge takes its slot in its
+// source's row (the atomic's old value), so the scatter needs no second atomic
+__global__ void k_count_slots(const int32_t *__restrict__ keys, int64_t count,
+                              int32_t *__restrict__ cnt, int32_t *__restrict__ slot) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
          i += int64_t(gridDim.x) * blockDim.x)
-        atomicAdd(cnt + keys[i], 1);
+        slot[i] = atomicAdd(cnt + keys[i], 1);
 }
 
 __global__ void k_scatter_fanout(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                                  int64_t m, const int32_t *__restrict__ out_ptr,
-                                 int32_t *__restrict__ cur, int32_t *__restrict__ out_dst,
+                                 const int32_t *__restrict__ slot, int32_t *__restrict__ out_dst,
                                  int32_t *__restrict__ out_eid) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
          e += int64_t(gridDim.x) * blockDim.x) {
-        int u = src[e];
-        int k = out_ptr[u] + atomicAdd(cur + u, 1);
+        const int k = out_ptr[src[e]] + slot[e];
         out_dst[k] = dst[e];
         out_eid[k] = int(e);
     }
@@ -150,21 +151,22 @@ void graph_build(Graph &g, const int32_t *in_ptr, const int32_t *in_src,
     // order inside a fan-out row is irrelevant: min is exact and commutative)
     csr_row_ids(g.in_ptr.as<int32_t>(), n, g.in_dst.as<int32_t>(), s, g);
     {
-        DevBuf cur;
+        DevBuf cur, slot;
         cur.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        slot.alloc(sizeof(int32_t) * int64_t(m > 0 ? m : 1), s);
         HF_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
         if (m) {
-            k_count_keys<<<grid_for(m, 256, g.sms), 256, 0, s>>>(g.in_src.as<int32_t>(), m,
-                                                               cur.as<int32_t>());
+            k_count_slots<<<grid_for(m, 256, g.sms), 256, 0, s>>>(g.in_src.as<int32_t>(), m,
+                                                                cur.as<int32_t>(),
+                                                                slot.as<int32_t>());
             HF_CHECK_LAUNCH();
             g.launches += 1;
         }
         scan_exclusive(cur.as<int32_t>(), g.out_ptr.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
-        HF_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (int64_t(n) + 1), s));
         if (m) {
             k_scatter_fanout<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
                 g.in_src.as<int32_t>(), g.in_dst.as<int32_t>(), m, g.out_ptr.as<int32_t>(),
-                cur.as<int32_t>(), g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>());
+                slot.as<int32_t>(), g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
             g.launches += 1;
         }

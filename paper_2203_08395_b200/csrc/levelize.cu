@@ -83,27 +83,6 @@ __device__ __forceinline__ void warp_append(bool pred, int item, int *list, int 
 //          [6] unresolved count, [7] max level, [8] visited junctions
 enum { SC_ACT = 0, SC_FR = 3, SC_UNRES = 6, SC_MAXLV = 7, SC_VIS = 8 };
 
-// block-aggregated append of `item` when `pred`: one global atomic per block and
-// call instead of one per warp (all threads of the block must call; s_w[33] shared)
-__device__ __forceinline__ void block_append(bool pred, int item, int *list, int *count, int *s_w) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const unsigned mask = __ballot_sync(0xffffffffu, pred);
-    if (lane == 0) s_w[wid] = __popc(mask);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            const int c = s_w[w];
-            s_w[w] = tot;
-            tot += c;
-        }
-        s_w[32] = tot ? atomicAdd(count, tot) : 0;
-    }
-    __syncthreads();
-    if (pred) list[s_w[32] + s_w[wid] + __popc(mask & ((1u << lane) - 1u))] = item;
-    __syncthreads();   // s_w is reused by the next call
-}
-
 __global__ void k_lev_init(const int32_t *__restrict__ in_ptr, const int32_t *__restrict__ in_src,
                            int32_t n, long long *__restrict__ pd, int32_t *__restrict__ cnt,
                            int32_t *__restrict__ lev, int32_t *__restrict__ active,
