@@ -309,12 +309,15 @@ def test_batch_concurrent_passes(hf, S, monkeypatch):
     assert_bits_equal(w, wo, "wns")
 
 
-@pytest.mark.parametrize("knob", ["HF_GA", "HF_POLL_ALL"])
-def test_batch_kernel_variants(hf, knob, monkeypatch):
-    # the measured-and-rejected kernel variants kept as switches:
-    # cp.async gathers into shared memory (HF_GA=1), one-lane polling (HF_POLL_ALL=0)
-    monkeypatch.setenv(knob, "1" if knob == "HF_GA" else "0")
-    S = 64
+@pytest.mark.parametrize("knob,val", [("HF_GA", "1"), ("HF_POLL_ALL", "0"), ("HF_PREFILL", "1"),
+                                      ("HF_BATCH_PLAIN", "1")])
+@pytest.mark.parametrize("S", [64, 12])
+def test_batch_kernel_variants(hf, knob, val, S, monkeypatch):
+    # the measured-and-rejected variants kept as switches: cp.async
+    # gathers into shared memory (HF_GA=1), one-lane polling (HF_POLL_ALL=0), the
+    # forward kernel NaN-filling rat (HF_PREFILL=1), the batch as two plain passes
+    # without the side stream (HF_BATCH_PLAIN=1)
+    monkeypatch.setenv(knob, val)
     g = hfgen.config("C3", 0.004)
     D = hfgen.scenario_delays(g, 0, S, "ms")
     T = np.full(S, g.t_req, F32)
@@ -324,6 +327,37 @@ def test_batch_kernel_variants(hf, knob, monkeypatch):
     assert_bits_equal(at, ato, "at")
     assert_bits_equal(rat, rato, "rat")
     assert_bits_equal(w, wo, "wns")
+
+
+def test_batch_reuses_schedule_across_scenario_counts(hf):
+    # one levelized graph, batches of S = 64, 128 (same task weight, new task bases),
+    # 32 (new task weight: schedule rebuilt), 64 again, 1 (two index slots per lane):
+    # every call bit-identical to the oracle
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.config("C3", 0.004)
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_levelize(G)
+    a = torch.from_numpy(g.at_src).to(dev)
+    for S in (64, 128, 32, 64, 1):
+        D = hfgen.scenario_delays(g, 0, S, "ms")
+        T = np.full(S, g.t_req, F32)
+        T[::5] -= 1.5
+        d = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
+        t = torch.from_numpy(T).to(dev)
+        w = torch.empty(S, dtype=torch.float32, device=dev)
+        at = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+        rat = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+        hf.hf_run_batch(G, S, d, hf.HF_LAYOUT_MS, t, a, w, at=at, rat=rat)
+        hf.hf_sync(G)
+        wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms",
+                                     threads=4, want_at_rat=True)
+        assert_bits_equal(at.cpu().numpy().reshape(g.n, S), ato, f"at S={S}")
+        assert_bits_equal(rat.cpu().numpy().reshape(g.n, S), rato, f"rat S={S}")
+        assert_bits_equal(w.cpu().numpy(), wo, f"wns S={S}")
+    G.close()
 
 
 def test_batch_host_api_both_layouts(hf):
