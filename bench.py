@@ -347,6 +347,11 @@ def main():
         h_wall = pin(np.zeros(S * world, np.float32)) if comm else None
 
         def e2e_step():
+            if comm is None:
+                # one call: create + levelize + batch, scenario upload overlapped
+                hf.hf_analyze(n, m, h_ptr, h_src, S, h_D, h_T, h_at, h_w, delay=h_delay,
+                              device=local, stream=stream)
+                return
             G = hf.hf_graph_create(n, m, h_ptr, h_src, delay=h_delay, device=local, stream=stream)
             hf.hf_levelize(G)
             hf.hf_run_batch(G, S, h_D, hf.HF_LAYOUT_MS, h_T, h_at, h_w, comm, h_wall)

@@ -176,6 +176,30 @@ hf_status hf_run_batch_d(hf_graph g, int32_t s_local, const float *delays_d, int
                          const float *t_req_d, const float *at_src_d, float *wns_local_d,
                          float *at_d, float *rat_d, void *nccl_comm, float *wns_all_d);
 
+/*
+ * hf_analyze -- the whole hot path in one call from HOST buffers: graph create
+ * (SURVEY.md §8(a) a1), levelize (a2-a4), forward + backward + worst slack for
+ * s_local delay sets (a5-a7), as hf_graph_create + hf_levelize + hf_run_batch.
+ * The scenario data (the bulk of the host->device bytes) is uploaded on a second
+ * stream while the graph is built and levelized; with pinned host buffers the
+ * upload overlaps that work.
+ *   n, m, fanin_ptr, fanin_src, delay   as hf_graph_create (fan-out derived).
+ *   s_local, delays [m*s_local] in HF_LAYOUT_MS, t_req [s_local], at_src [n] or
+ *   NULL => +0     as hf_run_batch (no NCCL gather).
+ *   wns_local  [s_local] output worst slack per scenario.
+ *   num_levels output L, or NULL.
+ *   device, cuda_stream   as hf_graph_create.
+ *   out_graph  receives the levelized graph (reusable with hf_run_batch; destroy
+ *              with hf_graph_destroy), or NULL to destroy it before returning.
+ * Synchronous: returns after wns_local is written; the host buffers may be reused
+ * on return.  Errors as the three calls it stands for (nothing is returned in
+ * out_graph on error).
+ */
+hf_status hf_analyze(int32_t n, int32_t m, const int32_t *fanin_ptr, const int32_t *fanin_src,
+                     const float *delay, int32_t s_local, const float *delays, const float *t_req,
+                     const float *at_src, float *wns_local, int32_t *num_levels, int device,
+                     void *cuda_stream, hf_graph *out_graph);
+
 /* NEXT-1: critical-path trace-back (PAPER.md:1002-1003
  * "extract graph information (critical paths, ...)"; reading R17).
  * Per scenario s: the endpoint is the sink (out-degree 0) with the smallest slack

@@ -544,6 +544,86 @@ hf_status hf_run_batch(hf_graph h, int32_t s_local, const float *delays, int lay
     });
 }
 
+// upload stream + events for hf_analyze, one set per host thread and device (its
+// own stream: the graph's side stream carries levelize work that must not queue
+// behind a multi-millisecond upload)
+struct Uploader {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+};
+static Uploader &uploader_of(int device) {
+    thread_local Uploader ups[64];
+    Uploader &u = ups[device & 63];
+    if (!u.s) {
+        HF_CUDA(cudaStreamCreateWithFlags(&u.s, cudaStreamNonBlocking));
+        HF_CUDA(cudaEventCreateWithFlags(&u.fork, cudaEventDisableTiming));
+        HF_CUDA(cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming));
+    }
+    return u;
+}
+
+hf_status hf_analyze(int32_t n, int32_t m, const int32_t *fanin_ptr, const int32_t *fanin_src,
+                     const float *delay, int32_t s_local, const float *delays, const float *t_req,
+                     const float *at_src, float *wns_local, int32_t *num_levels, int device,
+                     void *cuda_stream, hf_graph *out_graph) {
+    hf_graph h = nullptr;
+    const hf_status st = guarded([&]() -> hf_status {
+        if (out_graph) *out_graph = nullptr;
+        if (s_local < 1) fail(HF_ERR_INVALID_ARG, "s_local < 1");
+        if (!delays || !t_req || !wns_local)
+            fail(HF_ERR_INVALID_ARG, "delays, t_req or wns_local is NULL");
+        if (n < 0 || m < 0) fail(HF_ERR_INVALID_ARG, "negative n or m");
+        int ndev = 0;
+        HF_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) fail(HF_ERR_INVALID_ARG, "bad device ordinal");
+        DeviceGuard dg(device);
+        init_pool(device);
+        Uploader &up = uploader_of(device);
+        // the scenario data goes up on the upload stream while the graph is built
+        HF_CUDA(cudaEventRecord(up.fork, static_cast<cudaStream_t>(cuda_stream)));
+        HF_CUDA(cudaStreamWaitEvent(up.s, up.fork, 0));
+        struct Drain {   // host buffers stay in use until the upload stream drains
+            cudaStream_t s;
+            ~Drain() { cudaStreamSynchronize(s); }
+        } drain{up.s};
+        const size_t db = sizeof(float) * size_t(m) * size_t(s_local);
+        DevBuf d, t, a;
+        d.alloc(db > 0 ? db : 4, up.s);
+        t.alloc(sizeof(float) * size_t(s_local), up.s);
+        if (db) HF_CUDA(cudaMemcpyAsync(d.p, delays, db, cudaMemcpyHostToDevice, up.s));
+        HF_CUDA(cudaMemcpyAsync(t.p, t_req, sizeof(float) * size_t(s_local),
+                                cudaMemcpyHostToDevice, up.s));
+        if (at_src && n) {
+            a.alloc(sizeof(float) * size_t(n), up.s);
+            HF_CUDA(cudaMemcpyAsync(a.p, at_src, sizeof(float) * size_t(n),
+                                    cudaMemcpyHostToDevice, up.s));
+        }
+        HF_CUDA(cudaEventRecord(up.done, up.s));
+        hf_status cs = create_impl(false, n, m, fanin_ptr, fanin_src, nullptr, nullptr, delay,
+                                   device, cuda_stream, &h);
+        if (cs != HF_OK) return cs;
+        cs = levelize_impl(h, num_levels, nullptr, nullptr, nullptr, false);
+        if (cs != HF_OK) return cs;
+        Graph *g = G(h);
+        HF_CUDA(cudaStreamWaitEvent(g->stream, up.done, 0));
+        DevBuf w;
+        w.alloc(sizeof(float) * size_t(s_local), g->stream);
+        batch_core(g, s_local, d.as<float>(), t.as<float>(), (at_src && n) ? a.as<float>() : nullptr,
+                   w.as<float>(), nullptr, nullptr, nullptr, nullptr);
+        HF_CUDA(cudaMemcpyAsync(wns_local, w.p, sizeof(float) * size_t(s_local),
+                                cudaMemcpyDeviceToHost, g->stream));
+        // latch synchronises the graph's stream: the batch is done before d/t/a are
+        // freed (stream-ordered on the upload stream)
+        return latch(*g);
+    });
+    if (st != HF_OK || !out_graph) {
+        if (h) hf_graph_destroy(h);
+        h = nullptr;
+    }
+    if (out_graph) *out_graph = h;
+    return st;
+}
+
 hf_status hf_nccl_unique_id(void *id128) {
     return guarded([&]() -> hf_status {
         if (!id128) fail(HF_ERR_INVALID_ARG, "id is NULL");

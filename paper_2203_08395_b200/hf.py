@@ -31,7 +31,7 @@ EXPORTS = [
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
     "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d", "hf_graph_set_mode",
-    "hf_mis", "hf_mis_d",
+    "hf_mis", "hf_mis_d", "hf_analyze",
 ]
 
 
@@ -77,6 +77,7 @@ def _load() -> ctypes.CDLL:
         "hf_profile_read_batch": (c_int, [P, P]),
         "hf_critical_path_d": (c_int, [P, i32, P, P, P, f32, i32, P, P]),
         "hf_critical_path": (c_int, [P, P, f32, i32, P, P]),
+        "hf_analyze": (c_int, [i32, i32, P, P, P, i32, P, P, P, P, P, c_int, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -285,6 +286,22 @@ def hf_run_batch(g: Graph, s_local: int, delays, layout: int, t_req, at_src, wns
         a = _np(at_src, np.float32)
         _check(_lib.hf_run_batch(g.handle, s_local, _ptr(d), layout, _ptr(t), _ptr(a),
                                  _ptr(wns_local), nccl_comm, _ptr(wns_all)))
+
+
+def hf_analyze(n, m, fanin_ptr, fanin_src, s_local: int, delays, t_req, at_src, wns_local,
+               delay=None, device: int = 0, stream=None, keep_graph: bool = False):
+    """Create + levelize + batch in one call from host arrays (scenario data uploaded
+    while the graph is built).  Returns (num_levels, Graph or None)."""
+    a = [_np(fanin_ptr, np.int32), _np(fanin_src, np.int32), _np(delay, np.float32)]
+    d = _np(delays, np.float32)
+    t = _np(t_req, np.float32)
+    at = _np(at_src, np.float32)
+    L = ctypes.c_int32()
+    out = ctypes.c_void_p()
+    _check(_lib.hf_analyze(n, m, _ptr(a[0]), _ptr(a[1]), _ptr(a[2]), s_local, _ptr(d), _ptr(t),
+                           _ptr(at), _ptr(wns_local), ctypes.byref(L), device, _stream_of(stream),
+                           ctypes.byref(out) if keep_graph else None))
+    return L.value, (Graph(out, n, m, device) if keep_graph else None)
 
 
 def hf_nccl_unique_id() -> bytes:

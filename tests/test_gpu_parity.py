@@ -360,6 +360,36 @@ def test_batch_reuses_schedule_across_scenario_counts(hf):
     G.close()
 
 
+def test_analyze_one_call_host_api(hf):
+    # hf_analyze = create + levelize + batch from host buffers (pinned and pageable),
+    # same bits as the oracle; the kept graph is reusable; errors leave no graph
+    import torch
+    g = hfgen.config("C3", 0.004)
+    S = 16
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[::3] += 0.75
+    wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    for conv in (lambda a: a, pin):
+        w = conv(np.zeros(S, F32))
+        L, G = hf.hf_analyze(g.n, g.m, conv(g.in_ptr), conv(g.in_src), S, conv(D), conv(T),
+                             conv(g.at_src), w, delay=conv(g.delay), keep_graph=True)
+        assert_bits_equal(np.asarray(w), wo, "wns analyze")
+        assert L == hf.hf_graph_info(G)[2]
+        w2 = np.zeros(S, F32)
+        hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, g.at_src, w2)
+        assert_bits_equal(w2, wo, "wns reuse")
+        G.close()
+    # a 2-cycle: HF_ERR_CYCLE, nothing kept
+    ptr = np.array([0, 1, 2], np.int32)
+    src = np.array([1, 0], np.int32)
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_analyze(2, 2, ptr, src, 1, np.zeros(2, F32), np.zeros(1, F32), None,
+                      np.zeros(1, F32), keep_graph=True)
+    assert ei.value.status == hf.HF_ERR_CYCLE
+
+
 def test_batch_host_api_both_layouts(hf):
     g = hfgen.config("C1")
     S = 6
