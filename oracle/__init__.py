@@ -67,8 +67,9 @@ def _load():
         lib.oracle_critical_path.argtypes = [i32, i32, P, P, P, ctypes.c_int64, P,
                                              ctypes.c_float, P, i32, P]
         lib.oracle_critical_paths.argtypes = [i32, i32, P, P, i32, P, P, P, P, i32, P]
+        lib.oracle_critical_paths_k.argtypes = [i32, i32, P, P, i32, P, P, P, i32, P, P, i32, P]
         lib.oracle_mis.argtypes = [i32, i32, P, P, P, P]
-        for f in (lib.oracle_mis, lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
+        for f in (lib.oracle_critical_paths_k, lib.oracle_mis, lib.oracle_check_csr, lib.oracle_check_fanout, lib.oracle_levelize,
                   lib.oracle_forward, lib.oracle_backward, lib.oracle_batch,
                   lib.oracle_critical_path, lib.oracle_critical_paths, lib.oracle_forward_mode,
                   lib.oracle_backward_mode, lib.oracle_batch_mode):
@@ -238,6 +239,27 @@ def critical_paths(n, m, in_ptr, in_src, delays_ms, at_all, t_req, max_len=None)
     if rc:
         raise OracleError(rc)
     return [paths[s, :lens[s]].copy() for s in range(S)]
+
+
+def critical_paths_k(n, m, in_ptr, in_src, delays_ms, at_all, t_req, K, max_len=None):
+    """Top-K endpoints per scenario (NEXT-1, reading R17): delays [m][S], at [n][S],
+    t_req[S] -> (endpoints [S][K], list over s of K paths); endpoint -1 / empty path
+    past the number of sinks."""
+    lib = _load()
+    in_ptr, in_src = _i32(in_ptr), _i32(in_src)
+    delays_ms = _f32(delays_ms)
+    S = delays_ms.shape[1]
+    at_all = _f32(at_all)
+    t = _f32(np.broadcast_to(np.asarray(t_req, np.float32), (S,)))
+    max_len = max(1, n if max_len is None else max_len)
+    ends = np.zeros((S, K), np.int32)
+    paths = np.zeros((S, K, max_len), np.int32)
+    lens = np.zeros((S, K), np.int32)
+    rc = lib.oracle_critical_paths_k(n, m, _p(in_ptr), _p(in_src), S, _p(delays_ms), _p(at_all),
+                                     _p(t), K, _p(ends), _p(paths), max_len, _p(lens))
+    if rc:
+        raise OracleError(rc)
+    return ends, [[paths[s, r, :lens[s, r]].copy() for r in range(K)] for s in range(S)]
 
 
 def mis(n, m, in_ptr, in_src, prio):

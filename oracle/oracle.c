@@ -22,6 +22,7 @@
  *   - slack = fl(rat - at), wns = min slack                  BASELINE.json:5; reading R4
  *   - batched what-if scenarios = independent delay sets     PAPER.md:969-980; BASELINE.json:10
  *   - critical path of the worst endpoint (argmax trace-back) PAPER.md:1002-1003; reading R17
+ *     (and of the top-K endpoints by (slack, id))
  *   - greedy MIS by priority (Blelloch's lexicographically-first MIS)
  *                                                           PAPER.md:1141-1150; reading R19
  *   - early (hold) mode: min-plus forward, max-plus backward, slack = at - rat
@@ -378,6 +379,83 @@ int oracle_critical_path(int32_t n, int32_t m, const int32_t *in_ptr, const int3
         if (best < 0) return OR_INVALID;
         v = in_src[best];
     }
+}
+
+/* Top-K endpoints (SURVEY.md §8(f) NEXT-1 "with optional top-k endpoints"; reading
+ * R17): the K sinks with the smallest (slack fl(T - at), node id), in that order,
+ * and for each the same argmax trace-back as oracle_critical_path.  endpoints[K]
+ * (-1 past the number of sinks), paths[K][max_len], lens[K] (0 past the number of
+ * sinks). */
+typedef struct {
+    float slack;
+    int32_t v;
+} sink_key;
+static int cmp_sink_key(const void *a, const void *b) {
+    const sink_key *x = (const sink_key *)a, *y = (const sink_key *)b;
+    if (x->slack < y->slack) return -1;
+    if (x->slack > y->slack) return 1;
+    return (x->v > y->v) - (x->v < y->v);
+}
+int oracle_critical_path_k(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                           const float *d, int64_t dstride, const float *at, float T, int32_t K,
+                           int32_t *endpoints, int32_t *paths, int32_t max_len, int32_t *lens) {
+    for (int32_t r = 0; r < K; ++r) {
+        endpoints[r] = -1;
+        lens[r] = 0;
+    }
+    if (n == 0) return OR_OK;
+    int32_t *outdeg = (int32_t *)calloc((size_t)n, sizeof(int32_t));
+    sink_key *keys = (sink_key *)malloc(sizeof(sink_key) * (size_t)n);
+    for (int32_t e = 0; e < m; ++e) outdeg[in_src[e]] += 1;
+    T = canon(T);
+    int32_t ns = 0;
+    for (int32_t u = 0; u < n; ++u)
+        if (outdeg[u] == 0) {
+            keys[ns].slack = T - at[u];
+            keys[ns].v = u;
+            ++ns;
+        }
+    free(outdeg);
+    qsort(keys, (size_t)ns, sizeof(sink_key), cmp_sink_key);
+    int rc = OR_OK;
+    for (int32_t r = 0; r < K && r < ns && rc == OR_OK; ++r) {
+        int32_t v = keys[r].v, len = 0;
+        int32_t *path = paths + (int64_t)r * max_len;
+        endpoints[r] = v;
+        for (;;) {
+            if (len >= max_len) { rc = OR_INVALID; break; }
+            path[len++] = v;
+            if (in_ptr[v + 1] == in_ptr[v]) break;   /* source */
+            int32_t best = -1;
+            for (int32_t e = in_ptr[v]; e < in_ptr[v + 1] && best < 0; ++e) {
+                float x = at[in_src[e]] + canon(d[(int64_t)e * dstride]);
+                if (x == at[v]) best = e;
+            }
+            if (best < 0) { rc = OR_INVALID; break; }
+            v = in_src[best];
+        }
+        lens[r] = len;
+    }
+    free(keys);
+    return rc;
+}
+
+/* S scenarios x top-K: endpoints [S][K], paths [S][K][max_len], lens [S][K]. */
+int oracle_critical_paths_k(int32_t n, int32_t m, const int32_t *in_ptr, const int32_t *in_src,
+                            int32_t S, const float *delays, const float *at_all,
+                            const float *t_req, int32_t K, int32_t *endpoints, int32_t *paths,
+                            int32_t max_len, int32_t *lens) {
+    float *at = (float *)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    int rc = OR_OK;
+    for (int32_t s = 0; s < S && rc == OR_OK; ++s) {
+        for (int32_t v = 0; v < n; ++v) at[v] = at_all[(int64_t)v * S + s];
+        rc = oracle_critical_path_k(n, m, in_ptr, in_src, delays + s, S, at, t_req[s], K,
+                                    endpoints + (int64_t)s * K,
+                                    paths + (int64_t)s * K * max_len, max_len,
+                                    lens + (int64_t)s * K);
+    }
+    free(at);
+    return rc;
 }
 
 /* S scenarios: delays [m][S] (scenario-minor), at_all [n][S], t_req[S];

@@ -426,6 +426,52 @@ def test_p11_critical_path_chain():
     assert path.tolist() == walk[::-1]     # the whole chain, endpoint first
 
 
+def test_p11_critical_paths_top_k_integer():
+    # top-K endpoints: the K sinks in (T - at, id) order computed in exact integers,
+    # each traced with the integer greedy; -1 / empty past the number of sinks
+    rng = np.random.default_rng(1103)
+    for trial in range(300):
+        n, edges = random_tiny_dag(rng, nmax=10, p=0.5)
+        m = len(edges)
+        in_ptr, in_src, perm = csr_from_edges(n, edges)
+        dst = np.repeat(np.arange(n), np.diff(in_ptr)).astype(np.int64)
+        S = 3
+        d_int = rng.integers(1, 5, size=(m, S))
+        a_int = rng.integers(0, 3, size=n)
+        T = rng.integers(20, 30, size=S)
+        at = np.stack([oracle.forward(n, m, in_ptr, in_src, d_int[:, s].astype(F32),
+                                      a_int.astype(F32)) for s in range(S)], axis=1)
+        K = int(rng.integers(1, 6))
+        ends, paths = oracle.critical_paths_k(n, m, in_ptr, in_src, d_int.astype(F32), at,
+                                              T.astype(F32), K)
+        src_l, dst_l = in_src.tolist(), dst.tolist()
+        outdeg = np.bincount(in_src, minlength=n) if m else np.zeros(n, np.int64)
+        for s in range(S):
+            at_i = dfs_int_at(n, src_l, dst_l, d_int[:, s].tolist(), a_int.tolist())
+            sinks = sorted((v for v in range(n) if outdeg[v] == 0),
+                           key=lambda v: (int(T[s]) - at_i[v], v))
+            for r in range(K):
+                if r >= len(sinks):
+                    assert ends[s, r] == -1 and len(paths[s][r]) == 0, (trial, s, r)
+                    continue
+                v = sinks[r]
+                assert ends[s, r] == v, (trial, s, r)
+                ins = [[] for _ in range(n)]
+                for e in range(m):
+                    ins[dst_l[e]].append(e)
+                path = [v]
+                while ins[v]:
+                    e = min(e for e in ins[v] if at_i[src_l[e]] + d_int[e, s] == at_i[v])
+                    v = src_l[e]
+                    path.append(v)
+                assert paths[s][r].tolist() == path, (trial, s, r)
+        # K = 1 is the single worst path
+        one = oracle.critical_paths(n, m, in_ptr, in_src, d_int.astype(F32), at, T.astype(F32))
+        e1, p1 = oracle.critical_paths_k(n, m, in_ptr, in_src, d_int.astype(F32), at,
+                                         T.astype(F32), 1)
+        assert all(p1[s][0].tolist() == one[s].tolist() for s in range(S)), trial
+
+
 # ---- P12: early (hold) mode -- min-plus forward, max-plus backward (NEXT-2, R18) ----
 def test_p12_early_mode_bruteforce_tiny_dags():
     rng = np.random.default_rng(1203)
