@@ -222,6 +222,16 @@ hf_status hf_critical_path_d(hf_graph g, int32_t S, const float *delays, const f
                              int32_t *path, int32_t *path_len);
 hf_status hf_critical_path(hf_graph g, const float *at, float t_req, int32_t max_len,
                            int32_t *path, int32_t *path_len);
+/* hf_critical_paths_d: top-K endpoints per scenario (SURVEY.md §8(f) NEXT-1
+ *   "with optional top-k endpoints").  The K sinks with the smallest (slack, node
+ *   id), in that order, each traced as above.  endpoints [S][K] (or NULL) receives
+ *   the sink ids, -1 past the number of sinks; path [S][K][max_len]; path_len
+ *   [S][K] as for hf_critical_path_d, 0 past the number of sinks.  K = 1 gives
+ *   hf_critical_path_d.  Device pointers, stream-ordered; K + 1 launches. */
+hf_status hf_critical_paths_d(hf_graph g, int32_t S, const float *delays, const float *at,
+                              const float *t_req, float t_scalar, int32_t K, int32_t max_len,
+                              int32_t *endpoints, int32_t *path, int32_t *path_len);
+
 
 /* NEXT-4: greedy maximal independent set (PAPER.md:1141-1150
  * "a parallel maximal independent set finding step using Blelloch's Algorithm";

@@ -28,8 +28,8 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
 void profile_mark(Graph &g, int idx);
 void mis_device(Graph &g, const int32_t *prio, uint8_t *in_set);
 void critical_path_device(Graph &g, int32_t S, const float *d, const float *at,
-                          const float *t_arr, float t_scalar, int32_t max_len, int32_t *path,
-                          int32_t *len);
+                          const float *t_arr, float t_scalar, int32_t K, int32_t max_len,
+                          int32_t *endpoints, int32_t *path, int32_t *len);
 
 // ---- NCCL through dlopen (no link-time dependency) -------------------------
 namespace nccl {
@@ -701,7 +701,25 @@ hf_status hf_critical_path_d(hf_graph h, int32_t S, const float *delays_d, const
         if (g->early) fail(HF_ERR_INVALID_ARG, "the critical path is defined in late mode only");
         if (!delays_d && S != 1) fail(HF_ERR_INVALID_ARG, "graph delays need S == 1");
         critical_path_device(*g, S, delays_d ? delays_d : g->delay.as<float>(), at_d, t_req_d,
-                             t_scalar, max_len, path_d, path_len_d);
+                             t_scalar, 1, max_len, nullptr, path_d, path_len_d);
+        return HF_OK;
+    });
+}
+
+hf_status hf_critical_paths_d(hf_graph h, int32_t S, const float *delays_d, const float *at_d,
+                              const float *t_req_d, float t_scalar, int32_t K, int32_t max_len,
+                              int32_t *endpoints_d, int32_t *path_d, int32_t *path_len_d) {
+    return guarded([&]() -> hf_status {
+        if (!h || !at_d || !path_d || !path_len_d)
+            fail(HF_ERR_INVALID_ARG, "graph, at, path or path_len is NULL");
+        if (S < 1 || K < 1 || max_len < 1)
+            fail(HF_ERR_INVALID_ARG, "S, K and max_len must be >= 1");
+        Graph *g = G(h);
+        DeviceGuard dg(g->device);
+        if (g->early) fail(HF_ERR_INVALID_ARG, "the critical path is defined in late mode only");
+        if (!delays_d && S != 1) fail(HF_ERR_INVALID_ARG, "graph delays need S == 1");
+        critical_path_device(*g, S, delays_d ? delays_d : g->delay.as<float>(), at_d, t_req_d,
+                             t_scalar, K, max_len, endpoints_d, path_d, path_len_d);
         return HF_OK;
     });
 }
@@ -723,8 +741,8 @@ hf_status hf_critical_path(hf_graph h, const float *at, float t_req, int32_t max
         l.alloc(sizeof(int32_t), s);
         if (g->n)
             HF_CUDA(cudaMemcpyAsync(a.p, at, sizeof(float) * g->n, cudaMemcpyHostToDevice, s));
-        critical_path_device(*g, 1, g->delay.as<float>(), a.as<float>(), nullptr, t_req, max_len,
-                             p.as<int32_t>(), l.as<int32_t>());
+        critical_path_device(*g, 1, g->delay.as<float>(), a.as<float>(), nullptr, t_req, 1,
+                             max_len, nullptr, p.as<int32_t>(), l.as<int32_t>());
         int32_t ln = 0;
         HF_CUDA(cudaMemcpyAsync(&ln, l.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         HF_CUDA(cudaStreamSynchronize(s));

@@ -31,7 +31,7 @@ EXPORTS = [
     "hf_propagate_backward_d", "hf_run_batch", "hf_run_batch_d", "hf_nccl_unique_id",
     "hf_nccl_comm_init", "hf_nccl_comm_destroy", "hf_profile_enable", "hf_profile_read",
     "hf_profile_read_batch", "hf_critical_path", "hf_critical_path_d", "hf_graph_set_mode",
-    "hf_mis", "hf_mis_d", "hf_analyze",
+    "hf_mis", "hf_mis_d", "hf_analyze", "hf_critical_paths_d",
 ]
 
 
@@ -78,6 +78,7 @@ def _load() -> ctypes.CDLL:
         "hf_critical_path_d": (c_int, [P, i32, P, P, P, f32, i32, P, P]),
         "hf_critical_path": (c_int, [P, P, f32, i32, P, P]),
         "hf_analyze": (c_int, [i32, i32, P, P, P, i32, P, P, P, P, P, c_int, P, P]),
+        "hf_critical_paths_d": (c_int, [P, i32, P, P, P, f32, i32, i32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -257,6 +258,18 @@ def hf_critical_path(g: Graph, at, t_req, max_len: int, path=None, path_len=None
     _check(_lib.hf_critical_path(g.handle, _ptr(a), ctypes.c_float(t_req), max_len, _ptr(out),
                                  ctypes.byref(ln)))
     return out[:ln.value].copy()
+
+
+def hf_critical_paths(g: Graph, s: int, delays, at, t_req, k: int, max_len: int, endpoints,
+                      path, path_len):
+    """NEXT-1 top-K endpoints per scenario (device tensors, stream-ordered): endpoints
+    [S][K] int32 (or None), path [S][K][max_len] int32, path_len [S][K] int32."""
+    tr = t_req if _is_torch(t_req) else None
+    ts = 0.0 if _is_torch(t_req) else float(t_req)
+    _check(_lib.hf_critical_paths_d(g.handle, s, _ptr(delays), _ptr(at), _ptr(tr),
+                                    ctypes.c_float(ts), k, max_len, _ptr(endpoints), _ptr(path),
+                                    _ptr(path_len)))
+    return endpoints, path, path_len
 
 
 def hf_mis(g: Graph, prio, in_set=None):

@@ -536,6 +536,43 @@ def test_critical_path_batch_device(hf, name, scale, S):
     G.close()
 
 
+@pytest.mark.parametrize("name,scale,S,K", [("C3", 0.004, 8, 5), ("C3", 1.0, 4, 8),
+                                           ("C1", 1.0, 3, 40), ("chain", 0, 2, 3)])
+def test_critical_paths_top_k_device(hf, name, scale, S, K):
+    # top-K endpoints per scenario (NEXT-1): endpoints, paths and lengths identical to
+    # the oracle's; the chain has one sink (endpoint -1, length 0 past it)
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.chain(300, seed=3, relabel=True) if name == "chain" else hfgen.config(name, scale)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[1::2] -= 3.5
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    L = hf.hf_levelize(G)
+    d = torch.from_numpy(np.ascontiguousarray(D)).to(dev)
+    t = torch.from_numpy(T).to(dev)
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    at = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    rat = torch.empty(g.n * S, dtype=torch.float32, device=dev)
+    hf.hf_run_batch(G, S, d, hf.HF_LAYOUT_MS, t, torch.from_numpy(g.at_src).to(dev), w, at=at, rat=rat)
+    ends = torch.full((S, K), -7, dtype=torch.int32, device=dev)
+    path = torch.full((S, K, L), -7, dtype=torch.int32, device=dev)
+    plen = torch.full((S, K), -7, dtype=torch.int32, device=dev)
+    hf.hf_critical_paths(G, S, d, at, t, K, L, ends, path, plen)
+    hf.hf_sync(G)
+    at_h = at.cpu().numpy().reshape(g.n, S)
+    e_o, p_o = oracle.critical_paths_k(g.n, g.m, g.in_ptr, g.in_src, D, at_h, T, K, max_len=L)
+    got_e, got_p, got_l = ends.cpu().numpy(), path.cpu().numpy(), plen.cpu().numpy()
+    assert np.array_equal(got_e, e_o)
+    for s in range(S):
+        for r in range(K):
+            assert got_l[s, r] == len(p_o[s][r]), (s, r)
+            assert got_p[s, r, :got_l[s, r]].tolist() == p_o[s][r].tolist(), (s, r)
+    G.close()
+
+
 # ---- NEXT-2: early (hold) mode (reading R18) --------------------------------------------
 def _single_mode(hf, g, early, T):
     G = hf.hf_graph_create(g.n, g.m, g.in_ptr, g.in_src, delay=g.delay)
