@@ -1098,6 +1098,31 @@ struct PassCtx {
     DevBuf part_buf;
 };
 
+// all-ones (NaN sentinel) fill, 16-byte grid-stride stores: faster than
+// cudaMemsetAsync of the same bytes
+__global__ void k_fill_nan4(uint4 *__restrict__ p4, size_t n4, uint32_t *__restrict__ p,
+                            size_t n) {
+    const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
+         i += size_t(gridDim.x) * blockDim.x)
+        p4[i] = v;
+    for (size_t i = n4 * 4 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        p[i] = ~0u;
+}
+
+void fill_nan(Graph &g, float *buf, size_t cnt, cudaStream_t st) {
+    const int ctas = env_int("HF_FILL_CTAS", 8 * g.sms);   // 0: cudaMemsetAsync
+    if (ctas > 0 && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
+        k_fill_nan4<<<ctas, 256, 0, st>>>(reinterpret_cast<uint4 *>(buf), cnt / 4,
+                                          reinterpret_cast<uint32_t *>(buf), cnt);
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    } else {
+        HF_CUDA(cudaMemsetAsync(buf, 0xff, sizeof(float) * cnt, st));
+    }
+}
+
 // task schedule, bases, partial buffer and the sentinel fill of the output (on the
 // graph's stream)
 template <bool FWD>
@@ -1147,7 +1172,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
         g.launches += 1;
     }
     // the NaN sentinel (all-ones bit pattern): "not yet computed"
-    if (fill_out) HF_CUDA(cudaMemsetAsync(p.out, 0xff, sizeof(float) * size_t(g.n) * p.S, s));
+    if (fill_out) fill_nan(g, p.out, size_t(g.n) * p.S, s);
 }
 
 // the dataflow kernel and the long-row finalisation, on stream st
@@ -1284,18 +1309,6 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
 // Measured on C4 (S = 64): slower (1.48 ms vs 1.32 ms for the phase), because each
 // pass then has half the resident warps and the dataflow needs many warps to keep
 // several levels in flight; kept for the record.
-// all-ones fill with a small grid (HF_FILL_CTAS blocks): leaves SM slots free
-__global__ void k_fill_nan4(uint4 *__restrict__ p4, size_t n4, uint32_t *__restrict__ p,
-                            size_t n) {
-    const uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n4;
-         i += size_t(gridDim.x) * blockDim.x)
-        p4[i] = v;
-    for (size_t i = n4 * 4 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-         i += size_t(gridDim.x) * blockDim.x)
-        p[i] = ~0u;
-}
-
 // (creating the side stream per graph cost ~70 us of host time per step)
 Side &side_of(Graph &g) {
     thread_local Side sides[64];
@@ -1335,19 +1348,8 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
         HF_CUDA(cudaEventRecord(sd.fork, s));
         HF_CUDA(cudaStreamWaitEvent(sd.s2, sd.fork, 0));
         const bool prefill = env_int("HF_PREFILL", 0) != 0;
-        const int fill_ctas = env_int("HF_FILL_CTAS", 8 * g.sms);   // 0: cudaMemsetAsync
-        for (float *buf : {at, prefill ? nullptr : rat}) {
-            if (!buf) continue;
-            const size_t cnt = size_t(g.n) * S;
-            if (fill_ctas > 0 && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
-                k_fill_nan4<<<fill_ctas, 256, 0, sd.s2>>>(reinterpret_cast<uint4 *>(buf), cnt / 4,
-                                                         reinterpret_cast<uint32_t *>(buf), cnt);
-                HF_CHECK_LAUNCH();
-                g.launches += 1;
-            } else {
-                HF_CUDA(cudaMemsetAsync(buf, 0xff, sizeof(float) * cnt, sd.s2));
-            }
-        }
+        fill_nan(g, at, size_t(g.n) * S, sd.s2);
+        if (!prefill) fill_nan(g, rat, size_t(g.n) * S, sd.s2);
         HF_CUDA(cudaEventRecord(sd.join, sd.s2));
         g.ws_wns.alloc(sizeof(int32_t) * size_t(S), s);
         int32_t *ord = g.ws_wns.as<int32_t>();
