@@ -1140,7 +1140,8 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     // (at the end of their level, levelize.cu) are cut into parts of LO_PE edges;
     // scratch capacity ecap = tw + LO_SPLIT edges (>= LO_PE), ncap = tw rows
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
-    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? 12 : 16));
+    // measured per direction (tools/tune.py, C3 S=64): forward 12, backward 14
+    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? (FWD ? 12 : 14) : 16));
     tw = std::max(LO_PE - LO_SPLIT, std::min(tw, 32 * slots - LO_SPLIT));
     p.ecap = tw + LO_SPLIT;
     p.ncap = tw;
