@@ -625,21 +625,25 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 
 // After a pass: every long row gets its value (combine of its partials), its
 // optional slack and its worst-slack contribution.  One thread per (first part id,
-// V-wide column vector): all long rows and columns in parallel, the partials of a
-// row loaded four at a time; worst slack folded per block (ordered-int atomicMin).
+// V-wide column vector) up to the exact part count read on the device: all long
+// rows and columns in parallel, the partials of a row loaded eight at a time; worst
+// slack folded per block (ordered-int atomicMin).
 template <bool FWD, bool EARLY, int V>
 __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32_t *__restrict__ prow,
-                                 int32_t nparts, const int32_t *__restrict__ node_of, int32_t S,
+                                 const int32_t *__restrict__ nparts_dev,
+                                 const int32_t *__restrict__ node_of, int32_t S,
                                  const float *__restrict__ part_buf, float *__restrict__ out,
                                  const float *__restrict__ other, float *__restrict__ slack,
                                  int32_t *__restrict__ wns_ord, float *__restrict__ prefill) {
     constexpr bool MX = FWD != EARLY;
+    constexpr int FB = 8;   // partials in flight per thread
     extern __shared__ int32_t s_wmin[];
     const bool do_slack = !FWD && other;
     if (do_slack) {
         for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
         __syncthreads();
     }
+    const int64_t nparts = *nparts_dev;   // exact part count (the grid is sized by a bound)
     const int lpn = S / V;
     const int apb = blockDim.x / lpn * lpn;            // active threads per block
     const int64_t step = int64_t(gridDim.x) * apb;     // a multiple of lpn: lane fixed
@@ -649,29 +653,30 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
 #pragma unroll
     for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
     if (int(threadIdx.x) < apb) {
-        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < int64_t(nparts) * lpn;
-             t += step) {
+        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < nparts * lpn; t += step) {
             const int64_t p = t / lpn;
             const int np = np_arr[p];
             if (np == 0) continue;   // not the first part of a row
-            const int64_t node = node_of[prow[p]];
+            const int row = prow[p];
             const float *base = part_buf + p * S + col;
-            Vec<V> acc = ld_relaxed<V>(base);
-            for (int k = 1; k < np; k += 4) {
-                Vec<V> v[4];
+            Vec<V> acc;
+            for (int k = 0; k < np; k += FB) {
+                Vec<V> v[FB];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < FB; ++u)
                     if (k + u < np) v[u] = ld_relaxed<V>(base + int64_t(k + u) * S);
+                if (k == 0) acc = v[0];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (k + u < np)
+                for (int u = 0; u < FB; ++u)
+                    if (k + u < np && k + u > 0)
 #pragma unroll
                         for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v[u].x[j]);
             }
+            const int64_t node = node_of[row];
             st_plain<V>(out + node * S + col, acc);
             if (FWD && prefill) st_plain<V>(prefill + node * S + col, nan_vec<V>());
             if (do_slack) {
-                const Vec<V> a = ld_relaxed<V>(other + node * S + col);
+                const Vec<V> a = ld_relaxed<V>(other + node * S + col);   // final: after the pass
                 Vec<V> sl;
 #pragma unroll
                 for (int j = 0; j < V; ++j) {
@@ -1185,11 +1190,12 @@ void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cuda
     if (cx.nparts > 0) {
         const int32_t *npa = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
         const int32_t *prow = npa + (FWD ? g.np_cap_in : g.np_cap_out);
+        const int32_t *nparts_dev = g.nparts_d + (FWD ? 0 : 1);
         const int lpn = p.S / V;
         const int grid = grid_for(int64_t(cx.nparts) * lpn, 256, g.sms);
         const size_t sm = sizeof(int32_t) * size_t(p.S);
 #define HF_FIN(EE, VV)                                                                    \
-    k_finalize_split<FWD, EE, VV><<<grid, 256, sm, st>>>(npa, prow, cx.nparts, p.node_of, p.S, \
+    k_finalize_split<FWD, EE, VV><<<grid, 256, sm, st>>>(npa, prow, nparts_dev, p.node_of, p.S, \
                                                           p.part_buf, p.out, p.other, p.slack, \
                                                           p.wns_ord, p.prefill)
         if (g.early) {
