@@ -549,7 +549,7 @@ int64_t levelize_device(Graph &g) {
         DevBuf act2;
         act2.alloc(sizeof(int32_t) * n, s);
         int max_rounds = bits_for(n) + 2;
-        const int block = 1024;
+        const int block = std::max(64, std::min(1024, getenv("HF_JUMP_BLOCK") ? atoi(getenv("HF_JUMP_BLOCK")) : 1024));
         int grid = coop_grid((const void *)k_lev_jump, block, g.sms, 1);
         long long *pdp = pd.as<long long>();
         int32_t *a = la.as<int32_t>(), *b = act2.as<int32_t>();
@@ -598,7 +598,7 @@ int64_t levelize_device(Graph &g) {
         g.launches += 1;
         HF_CUDA(cudaMemsetAsync(sc + SC_FR + 1, 0, sizeof(int32_t), s));   // round 0 appends here
         lt.mark("contract+seed", s);
-        const int block = 1024;
+        const int block = std::max(64, std::min(1024, getenv("HF_KAHN_BLOCK") ? atoi(getenv("HF_KAHN_BLOCK")) : 1024));
         int grid = coop_grid((const void *)k_lev_kahn, block, g.sms, 1);
         DevBuf wbuf;   // three 64-bit round words {arrivals | frontier size}
         wbuf.alloc(sizeof(unsigned long long) * 3, s);
