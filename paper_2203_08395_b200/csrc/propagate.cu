@@ -221,8 +221,11 @@ template <int NSL> struct Idx {
 };
 template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 
+#ifndef FLOW_MINB_BWD
+#define FLOW_MINB_BWD 1   // minimum resident CTAs per SM asked of ptxas for the backward
+#endif
 template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
-__global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
+__global__ void __launch_bounds__(FLOW_THREADS, FWD ? 1 : FLOW_MINB_BWD) k_flow(FlowParams p) {
     // MX: the pass combines with max (late forward, early backward), else min
     constexpr bool MX = FWD != EARLY;
     constexpr int SC = V * LPN;   // columns per chunk
