@@ -373,26 +373,24 @@ __global__ void k_lo_lstart(const int32_t *__restrict__ level_ptr, const int32_t
     }
 }
 // parts of every long row, stored at its first part id
-__global__ void k_lo_np(const int32_t *__restrict__ lo_q, int32_t n, int32_t *__restrict__ np,
-                        int32_t *__restrict__ prow) {
+// Per row i: the part count of a long row at its first part id (0 at its other
+// part ids, so no fill of the array is needed: ids past the exact part count are
+// never read) and the row of that part; per node u: its neighbour encoding, its id
+// or -(first part id + 1) when its own row (this direction) is long, so the relabel
+// reads one value per edge.
+__global__ void k_lo_np_enc(const int32_t *__restrict__ lo_q, const int32_t *__restrict__ ptr,
+                            const int32_t *__restrict__ pos, int32_t n, int32_t *__restrict__ np,
+                            int32_t *__restrict__ prow, int32_t *__restrict__ enc) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x)
-        if (lo_q[i + 1] != lo_q[i]) {
-            np[lo_q[i]] = lo_q[i + 1] - lo_q[i];
-            prow[lo_q[i]] = int32_t(i);
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int q0 = lo_q[i], q1 = lo_q[i + 1];
+        if (q1 != q0) {
+            np[q0] = q1 - q0;
+            prow[q0] = int32_t(i);
+            for (int q = q0 + 1; q < q1; ++q) np[q] = 0;
         }
-}
-
-// copy row order[i] of (ptr, a) to row i of (nptr, na) and its edge ids to neid
-// (eid_map == null -> the edge id is the source position itself); a neighbour u
-// whose own row in this direction is long is written as -(first part id + 1)
-// neighbour encoding of every node, once per node: its id, or -(first part id + 1)
-// when its own row (this direction) is long; the relabel then reads one value per edge
-__global__ void k_lo_enc(const int32_t *__restrict__ ptr, const int32_t *__restrict__ pos,
-                         const int32_t *__restrict__ q, int32_t n, int32_t *__restrict__ enc) {
-    for (int64_t u = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; u < n;
-         u += int64_t(gridDim.x) * blockDim.x)
-        enc[u] = ptr[u + 1] - ptr[u] > LO_SPLIT ? -(q[pos[u]] + 1) : int32_t(u);
+        enc[i] = ptr[i + 1] - ptr[i] > LO_SPLIT ? -(lo_q[pos[i]] + 1) : int32_t(i);
+    }
 }
 // A warp copies the rows of 32 consecutive output positions as one flattened edge
 // range: every output store is coalesced and every lane does one edge per step (a
@@ -707,12 +705,9 @@ int64_t levelize_device(Graph &g) {
             scan_exclusive(deg[dir].as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, ds, g, dir);
             scan_exclusive(parts[dir].as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, ds, g,
                            dir);
-            HF_CUDA(cudaMemsetAsync(np.p, 0, sizeof(int32_t) * npcap, ds));
-            k_lo_np<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(lo_q, n, np.as<int32_t>(),
-                                                             np.as<int32_t>() + npcap);
-            HF_CHECK_LAUNCH();
-            k_lo_enc<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(ptr, pos[dir].as<int32_t>(), lo_q, n,
-                                                              enc[dir].as<int32_t>());
+            k_lo_np_enc<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(
+                lo_q, ptr, pos[dir].as<int32_t>(), n, np.as<int32_t>(), np.as<int32_t>() + npcap,
+                enc[dir].as<int32_t>());
             HF_CHECK_LAUNCH();
             if (in)
                 k_relabel_rows<<<grid_for(n, 256, g.sms), 256, 0, ds>>>(
@@ -723,7 +718,7 @@ int64_t levelize_device(Graph &g) {
                     lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
                     enc[dir].as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
-            g.launches += 5;
+            g.launches += 5;   // flags, lstart, place, np_enc, relabel (scans count themselves)
         }
         HF_CUDA(cudaEventRecord(sd.join, sd.s2));
         HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));   // before the scratch is freed on s
