@@ -107,14 +107,16 @@ class ClockSampler:
             getr = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                 nv.nvmlDeviceGetCurrentClocksThrottleReasons
             mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            mmx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM)
             while not self._stop.is_set():
-                # two cheap queries per sample, 100 ms apart: NVML calls take driver
+                # three cheap queries per sample, 100 ms apart: NVML calls take driver
                 # locks that the timed CUDA calls also need
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mem = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)
                 r = int(getr(h))
                 act = lambda bit: "Active" if r & bit else "Not Active"
                 self.rows.append([str(sm), str(mx), "", hex(r), act(0x8), act(0x40), act(0x20),
-                                  act(0x4)])
+                                  act(0x4), str(mem), str(mmx)])
                 self._stop.wait(0.1)
             return
         except Exception:
@@ -147,9 +149,38 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 4 + i and r[4 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        mem = [float(r[8]) for r in self.rows if len(r) > 9 and r[8].isdigit()]
+        mmx = [float(r[9]) for r in self.rows if len(r) > 9 and r[9].isdigit()]
+        out = {"sm_mhz": float(np.median(sm)) if sm else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+               "samples": len(self.rows)}
+        if mem:   # HBM clock (box-to-box differences in memory bandwidth show here)
+            out["mem_mhz"] = float(np.median(mem))
+            out["mem_max_mhz"] = max(mmx) if mmx else None
+        return out
+
+
+def copy_probe(dev):
+    """This box's device copy bandwidth (read + write bytes of a 2 GiB copy, best of 5,
+    CUDA events), measured after the timed region: context for roofline.peak, which
+    is the pool's MEASURED_PEAKS.json figure (boxes differ by up to ~30% in HBM rate)."""
+    import torch
+    try:
+        a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+        b = torch.empty_like(a)
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        return round(2 * (2 << 30) / (best * 1e-3) / 1e9, 1)
+    except Exception:
+        return None
 
 
 def cpu_baseline(g, D_host, T, at_src, sample_note):
@@ -329,6 +360,7 @@ def main():
     prop_ms = (fwd_ms + bwd_ms) / K
     achieved = (b_fwd + b_bwd) / (prop_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
+    box_gbs = copy_probe(dev)
     traffic = None   # measured dram bytes of the same two kernels (profiles/traffic.json)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and S == 64:
@@ -400,7 +432,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "forward + backward dataflow propagation kernels (k_flow)",
-                         "algorithmic_bytes": b_fwd + b_bwd, "peak_source": peak_src},
+                         "algorithmic_bytes": b_fwd + b_bwd, "peak_source": peak_src,
+                         "copy_gbs_this_box": box_gbs},
             "e2e": e2e,
             "gpu_launches": stats["launches"],
             "clocks": clk.summary(),

@@ -24,6 +24,6 @@ python tools/trace_report.py $OUT/tr/c3_fwd_S1.bin $OUT/tr/c3_bwd_S1.bin $OUT/tr
 python tools/kahn_report.py $OUT/tr/c3_kahn.bin > $OUT/kahn_C3.txt 2>&1
 rm -f $OUT/tr/*.bin
 # warm per-stage device times of the levelizer and the batch (CUDA events per stage)
-HF_LEV_TIMES=1 HF_PROP_TIMES=1 timeout 200 python bench.py --steps 5 --warmup 3 2>&1 \
+HF_LEV_TIMES=1 HF_PROP_TIMES=1 timeout 200 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 \
     | grep stages | tail -2 > $OUT/stages.txt
 echo done
