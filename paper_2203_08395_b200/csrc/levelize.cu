@@ -342,7 +342,8 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
                            const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ fs,
                            const int32_t *__restrict__ flag, const int32_t *__restrict__ ptr,
                            int32_t n, int32_t *__restrict__ lo_node, int32_t *__restrict__ deg,
-                           int32_t *__restrict__ parts, int32_t *__restrict__ pos_of) {
+                           int32_t *__restrict__ parts, int32_t *__restrict__ pos_of,
+                           int32_t *__restrict__ lstart) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
          i += int64_t(gridDim.x) * blockDim.x) {
         if (i == n) {
@@ -356,6 +357,7 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
         const int sl = fs[i] - fs[ls];
         const int nlong = fs[le] - fs[ls];
         const bool lng = flag[i] != 0;
+        if (int(i) == ls) lstart[k] = le - nlong;   // first long row of the level
         const int pos = lng ? le - nlong + sl : ls + (int(i) - ls) - sl;
         const int d = ptr[v + 1] - ptr[v];
         lo_node[pos] = v;
@@ -364,15 +366,6 @@ __global__ void k_lo_place(const int32_t *__restrict__ order, const int32_t *__r
         pos_of[v] = pos;
     }
 }
-// first long row of every level: level end minus the level's long-row count
-__global__ void k_lo_lstart(const int32_t *__restrict__ level_ptr, const int32_t *__restrict__ fs,
-                            int32_t L, int32_t *__restrict__ lstart) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
-        const int ls = level_ptr[k], le = level_ptr[k + 1];
-        lstart[k] = le - (fs[le] - fs[ls]);
-    }
-}
-// parts of every long row, stored at its first part id
 // Per row i: the part count of a long row at its first part id (0 at its other
 // part ids, so no fill of the array is needed: ids past the exact part count are
 // never read) and the row of that part; per node u: its neighbour encoding, its id
@@ -693,14 +686,11 @@ int64_t levelize_device(Graph &g) {
             scan_exclusive(flag[dir].as<int32_t>(), fs[dir].as<int32_t>(), int64_t(n) + 1, nullptr,
                            ds, g, dir);
             DevBuf &lst = in ? g.lo_in_lstart : g.lo_out_lstart;
-            k_lo_lstart<<<grid_for(L, 256, g.sms), 256, 0, ds>>>(g.level_ptr.as<int32_t>(),
-                                                                fs[dir].as<int32_t>(), L,
-                                                                lst.as<int32_t>());
-            HF_CHECK_LAUNCH();
             k_lo_place<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, ds>>>(
                 g.order.as<int32_t>(), g.level.as<int32_t>(), g.level_ptr.as<int32_t>(),
                 fs[dir].as<int32_t>(), flag[dir].as<int32_t>(), ptr, n, lo_node,
-                deg[dir].as<int32_t>(), parts[dir].as<int32_t>(), pos[dir].as<int32_t>());
+                deg[dir].as<int32_t>(), parts[dir].as<int32_t>(), pos[dir].as<int32_t>(),
+                lst.as<int32_t>());
             HF_CHECK_LAUNCH();
             scan_exclusive(deg[dir].as<int32_t>(), lo_ptr, int64_t(n) + 1, nullptr, ds, g, dir);
             scan_exclusive(parts[dir].as<int32_t>(), lo_q, int64_t(n) + 1, sc + 12 + dir, ds, g,
@@ -718,7 +708,7 @@ int64_t levelize_device(Graph &g) {
                     lo_node, n, ptr, g.out_dst.as<int32_t>(), g.out_eid.as<int32_t>(), lo_ptr,
                     enc[dir].as<int32_t>(), g.lo_out_nbr.as<int32_t>(), g.lo_out_eid.as<int32_t>());
             HF_CHECK_LAUNCH();
-            g.launches += 5;   // flags, lstart, place, np_enc, relabel (scans count themselves)
+            g.launches += 4;   // flags, place, np_enc, relabel (scans count themselves)
         }
         HF_CUDA(cudaEventRecord(sd.join, sd.s2));
         HF_CUDA(cudaStreamWaitEvent(s, sd.join, 0));   // before the scratch is freed on s
