@@ -221,11 +221,15 @@ template <int NSL> struct Idx {
 };
 template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 
-#ifndef FLOW_MINB_BWD
-#define FLOW_MINB_BWD 1   // minimum resident CTAs per SM asked of ptxas for the backward
-#endif
+// Only the thread bound: an explicit minimum of 1 block per SM lets ptxas spend
+// 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured); the
+// backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
 template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
+#ifdef FLOW_MINB_BWD
 __global__ void __launch_bounds__(FLOW_THREADS, FWD ? 1 : FLOW_MINB_BWD) k_flow(FlowParams p) {
+#else
+__global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
+#endif
     // MX: the pass combines with max (late forward, early backward), else min
     constexpr bool MX = FWD != EARLY;
     constexpr int SC = V * LPN;   // columns per chunk
