@@ -163,7 +163,7 @@ class ClockSampler:
 def copy_probe(dev):
     """This box's device copy bandwidth (read + write bytes of a 2 GiB copy, best of 5,
     CUDA events), measured after the timed region: context for roofline.peak, which
-    is the pool's MEASURED_PEAKS.json figure (boxes differ by up to ~30% in HBM rate)."""
+    is the pool's MEASURED_PEAKS.json figure."""
     import torch
     try:
         a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
