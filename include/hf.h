@@ -35,7 +35,11 @@
 extern "C" {
 #endif
 
-#define HF_VERSION 100
+#define HF_VERSION 101
+
+/* Largest scenario count of one batch call (s_local); larger -> HF_ERR_INVALID_ARG.
+ * (The per-CTA worst-slack table of the kernels holds 4 bytes per scenario.) */
+#define HF_MAX_SCENARIOS 8192
 
 typedef struct hf_graph_s *hf_graph; /* opaque; owns device copies of the graph */
 
@@ -158,7 +162,9 @@ hf_status hf_propagate_backward_d(hf_graph g, float t_req, const float *at_d, fl
  * views; BASELINE.json:10), forward + backward + worst slack
  * per scenario, then (optionally) an NCCL all-gather of the per-rank worst
  * slacks (BASELINE.json:5 "NCCL over NVLink used only to gather worst slack").
- *   s_local    number of scenarios on this rank (>= 1).
+ *   s_local    number of scenarios on this rank, 1 <= s_local <= HF_MAX_SCENARIOS;
+ *              HF_ERR_INVALID_ARG also when the pass would exceed 2^31 - 1 warp
+ *              tasks (odd s_local on a graph of tens of millions of nodes).
  *   delays     [m*s_local] scenario delays in `layout` (HF_LAYOUT_MS preferred).
  *   t_req      [s_local] required time per scenario.
  *   at_src     [n] source arrival times shared by all scenarios, or NULL => +0.

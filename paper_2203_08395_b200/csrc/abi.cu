@@ -109,7 +109,8 @@ static hf_status latch(Graph &g) {
     if (e) {
         HF_CUDA(cudaMemsetAsync(g.d_err(), 0, sizeof(uint32_t), g.stream));
         HF_CUDA(cudaStreamSynchronize(g.stream));
-        set_error("device-side validation: NaN or inf in scenario delays / required times");
+        set_error("device-side validation: NaN or inf in delays, source arrival times or required "
+                  "times");
         return HF_ERR_INVALID_ARG;
     }
     return HF_OK;
@@ -369,8 +370,7 @@ hf_status hf_propagate_forward(hf_graph h, const float *at_src, float *at) {
         if (g->n)
             HF_CUDA(cudaMemcpyAsync(at, o.p, sizeof(float) * g->n, cudaMemcpyDeviceToHost,
                                     g->stream));
-        HF_CUDA(cudaStreamSynchronize(g->stream));
-        return HF_OK;
+        return latch(*g);
     });
 }
 
@@ -409,9 +409,9 @@ hf_status hf_propagate_backward(hf_graph h, float t_req, const float *at, float 
             HF_CUDA(cudaMemcpyAsync(slack, sl.p, nb, cudaMemcpyDeviceToHost, g->stream));
         float wv = 0;
         HF_CUDA(cudaMemcpyAsync(&wv, w.p, sizeof(float), cudaMemcpyDeviceToHost, g->stream));
-        HF_CUDA(cudaStreamSynchronize(g->stream));
+        const hf_status st = latch(*g);
         if (wns) *wns = wv;
-        return HF_OK;
+        return st;
     });
 }
 
@@ -464,7 +464,8 @@ hf_status hf_run_batch_d(hf_graph h, int32_t s_local, const float *delays_d, int
     return guarded([&]() -> hf_status {
         if (!h || !delays_d || !t_req_d || !wns_local_d)
             fail(HF_ERR_INVALID_ARG, "graph, delays, t_req or wns_local is NULL");
-        if (s_local < 1) fail(HF_ERR_INVALID_ARG, "s_local < 1");
+        if (s_local < 1 || s_local > HF_MAX_SCENARIOS)
+            fail(HF_ERR_INVALID_ARG, "s_local outside [1, HF_MAX_SCENARIOS]");
         if (layout != HF_LAYOUT_SM && layout != HF_LAYOUT_MS) fail(HF_ERR_INVALID_ARG, "layout");
         if (comm && !wns_all_d) fail(HF_ERR_INVALID_ARG, "wns_all is NULL with a communicator");
         Graph *g = G(h);
@@ -491,7 +492,8 @@ hf_status hf_run_batch(hf_graph h, int32_t s_local, const float *delays, int lay
     return guarded([&]() -> hf_status {
         if (!h || !delays || !t_req || !wns_local)
             fail(HF_ERR_INVALID_ARG, "graph, delays, t_req or wns_local is NULL");
-        if (s_local < 1) fail(HF_ERR_INVALID_ARG, "s_local < 1");
+        if (s_local < 1 || s_local > HF_MAX_SCENARIOS)
+            fail(HF_ERR_INVALID_ARG, "s_local outside [1, HF_MAX_SCENARIOS]");
         if (layout != HF_LAYOUT_SM && layout != HF_LAYOUT_MS) fail(HF_ERR_INVALID_ARG, "layout");
         if (comm && !wns_all) fail(HF_ERR_INVALID_ARG, "wns_all is NULL with a communicator");
         Graph *g = G(h);
@@ -569,7 +571,8 @@ hf_status hf_analyze(int32_t n, int32_t m, const int32_t *fanin_ptr, const int32
     hf_graph h = nullptr;
     const hf_status st = guarded([&]() -> hf_status {
         if (out_graph) *out_graph = nullptr;
-        if (s_local < 1) fail(HF_ERR_INVALID_ARG, "s_local < 1");
+        if (s_local < 1 || s_local > HF_MAX_SCENARIOS)
+            fail(HF_ERR_INVALID_ARG, "s_local outside [1, HF_MAX_SCENARIOS]");
         if (!delays || !t_req || !wns_local)
             fail(HF_ERR_INVALID_ARG, "delays, t_req or wns_local is NULL");
         if (n < 0 || m < 0) fail(HF_ERR_INVALID_ARG, "negative n or m");

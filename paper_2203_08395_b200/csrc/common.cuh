@@ -244,5 +244,14 @@ __device__ __forceinline__ float ord2f(int32_t k) {
     return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF));
 }
 __device__ __forceinline__ float canon0(float x) { return __fadd_rn(x, 0.0f); }  // -0 -> +0
+// An input value (delay, source arrival, required time) as the propagation kernels
+// use it: -0 -> +0; NaN / +-inf (rejected, reading R9) set `bad` (latched as
+// HF_ERR_INVALID_ARG) and are replaced by +0, so no output row can become NaN -- the
+// "not yet computed" sentinel of the dataflow kernels -- and every pass terminates.
+__device__ __forceinline__ float sane(float x, bool &bad) {
+    const bool ok = fabsf(x) <= 3.40282346638528859812e+38f;   // false for NaN and +-inf
+    bad |= !ok;
+    return ok ? canon0(x) : 0.0f;
+}
 
 }  // namespace hf

@@ -224,7 +224,7 @@ template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 // Only the thread bound: an explicit minimum of 1 block per SM lets ptxas spend
 // 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured); the
 // backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
+template <int V, int LPN, bool FWD, bool GA, bool EARLY>
 #ifdef FLOW_MINB_BWD
 __global__ void __launch_bounds__(FLOW_THREADS, FWD ? 1 : FLOW_MINB_BWD) k_flow(FlowParams p) {
 #else
@@ -428,12 +428,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 Vec<V> x;
 #pragma unroll
                 for (int j = 0; j < V; ++j) {
-                    float d1 = dv.x[j];
-                    if (CHECK_D) {
-                        bad |= !isfinite(d1);
-                        d1 = canon0(d1);
-                    }
-                    x.x[j] = relax<FWD>(av.x[j], d1);
+                    x.x[j] = relax<FWD>(av.x[j], sane(dv.x[j], bad));
                 }
                 st_s<V>(dp, x);
             }
@@ -535,12 +530,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     Vec<V> x;
 #pragma unroll
                     for (int j = 0; j < V; ++j) {
-                        float d1 = dv.x[j];
-                        if (CHECK_D) {
-                            bad |= !isfinite(d1);
-                            d1 = canon0(d1);
-                        }
-                        x.x[j] = relax<FWD>(a[r].x[j], d1);
+                        x.x[j] = relax<FWD>(a[r].x[j], sane(dv.x[j], bad));
                     }
                     st_s<V>(dp, x);
                 }
@@ -575,13 +565,13 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 Vec<V> best;
                 if (ee == eb) {
                     if (FWD) {
-                        const float a0 = p.src_val ? canon0(__ldg(p.src_val + node)) : 0.0f;
+                        const float a0 = p.src_val ? sane(__ldg(p.src_val + node), bad) : 0.0f;
 #pragma unroll
                         for (int j = 0; j < V; ++j) best.x[j] = a0;
                     } else {
 #pragma unroll
                         for (int j = 0; j < V; ++j)
-                            best.x[j] = canon0(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar);
+                            best.x[j] = sane(p.src_val ? __ldg(p.src_val + col + j) : p.t_scalar, bad);
                     }
                 } else {
                     best = ld_s<V>(s_d + eb * SC + gl * V);
@@ -621,7 +611,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         X0 = X1;
     }
 
-    if (CHECK_D && bad) atomicOr(p.err, ERR_NONFINITE);
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
     if (!FWD) {
         flush_run();
         __syncthreads();
@@ -651,55 +641,81 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
         __syncthreads();
     }
     const int64_t nparts = *nparts_dev;   // exact part count (the grid is sized by a bound)
-    const int lpn = S / V;
-    const int apb = blockDim.x / lpn * lpn;            // active threads per block
-    const int64_t step = int64_t(gridDim.x) * apb;     // a multiple of lpn: lane fixed
-    const int lane = int(threadIdx.x % lpn);
-    const int64_t col = int64_t(lane) * V;
-    float mn[V];
+    const int lpn = S / V;   // column vectors per row
+    // long row p (first part id), column vector at col: combine the partials, store,
+    // slack; the row minimum of the slack goes to mn
+    auto row_vec = [&](int64_t p, int np, int64_t col, float *mn) {
+        const int row = prow[p];
+        const float *base = part_buf + p * S + col;
+        Vec<V> acc;
+        for (int k = 0; k < np; k += FB) {
+            Vec<V> v[FB];
 #pragma unroll
-    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
-    if (int(threadIdx.x) < apb) {
-        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < nparts * lpn; t += step) {
-            const int64_t p = t / lpn;
-            const int np = np_arr[p];
-            if (np == 0) continue;   // not the first part of a row
-            const int row = prow[p];
-            const float *base = part_buf + p * S + col;
-            Vec<V> acc;
-            for (int k = 0; k < np; k += FB) {
-                Vec<V> v[FB];
+            for (int u = 0; u < FB; ++u)
+                if (k + u < np) v[u] = ld_relaxed<V>(base + int64_t(k + u) * S);
+            if (k == 0) acc = v[0];
 #pragma unroll
-                for (int u = 0; u < FB; ++u)
-                    if (k + u < np) v[u] = ld_relaxed<V>(base + int64_t(k + u) * S);
-                if (k == 0) acc = v[0];
+            for (int u = 0; u < FB; ++u)
+                if (k + u < np && k + u > 0)
 #pragma unroll
-                for (int u = 0; u < FB; ++u)
-                    if (k + u < np && k + u > 0)
+                    for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v[u].x[j]);
+        }
+        const int64_t node = node_of[row];
+        st_plain<V>(out + node * S + col, acc);
+        if (FWD && prefill) st_plain<V>(prefill + node * S + col, nan_vec<V>());
+        if (do_slack) {
+            const Vec<V> a = ld_relaxed<V>(other + node * S + col);   // final: after the pass
+            Vec<V> sl;
 #pragma unroll
-                        for (int j = 0; j < V; ++j) acc.x[j] = combine<MX>(acc.x[j], v[u].x[j]);
+            for (int j = 0; j < V; ++j) {
+                sl.x[j] = EARLY ? __fsub_rn(a.x[j], acc.x[j]) : __fsub_rn(acc.x[j], a.x[j]);
+                mn[j] = fminf(mn[j], sl.x[j]);
             }
-            const int64_t node = node_of[row];
-            st_plain<V>(out + node * S + col, acc);
-            if (FWD && prefill) st_plain<V>(prefill + node * S + col, nan_vec<V>());
-            if (do_slack) {
-                const Vec<V> a = ld_relaxed<V>(other + node * S + col);   // final: after the pass
-                Vec<V> sl;
+            if (slack) st_plain<V>(slack + node * S + col, sl);
+        }
+    };
+    if (lpn <= int(blockDim.x)) {
+        // a thread keeps one column vector (lane) for all its rows: minima in registers
+        const int apb = blockDim.x / lpn * lpn;            // active threads per block
+        const int64_t step = int64_t(gridDim.x) * apb;     // a multiple of lpn: lane fixed
+        const int lane = int(threadIdx.x % lpn);
+        const int64_t col = int64_t(lane) * V;
+        float mn[V];
 #pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    sl.x[j] = EARLY ? __fsub_rn(a.x[j], acc.x[j]) : __fsub_rn(acc.x[j], a.x[j]);
-                    mn[j] = fminf(mn[j], sl.x[j]);
-                }
-                if (slack) st_plain<V>(slack + node * S + col, sl);
+        for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+        if (int(threadIdx.x) < apb) {
+            for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < nparts * lpn; t += step) {
+                const int64_t p = t / lpn;
+                const int np = np_arr[p];
+                if (np == 0) continue;   // not the first part of a row
+                row_vec(p, np, col, mn);
+            }
+            if (do_slack)
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    if (mn[j] != __int_as_float(0x7f800000))
+                        atomicMin(s_wmin + col + j, f2ord(mn[j]));
+        }
+    } else {
+        // rows wider than the block (S / V > blockDim): a block per row, the column
+        // vectors strided over its threads, minima folded per row
+        for (int64_t p = blockIdx.x; p < nparts; p += gridDim.x) {
+            const int np = np_arr[p];
+            if (np == 0) continue;
+            for (int cv = threadIdx.x; cv < lpn; cv += blockDim.x) {
+                float mn[V];
+#pragma unroll
+                for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+                row_vec(p, np, int64_t(cv) * V, mn);
+                if (do_slack)
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        if (mn[j] != __int_as_float(0x7f800000))
+                            atomicMin(s_wmin + cv * V + j, f2ord(mn[j]));
             }
         }
     }
     if (do_slack) {
-        if (int(threadIdx.x) < apb)
-#pragma unroll
-            for (int j = 0; j < V; ++j)
-                if (mn[j] != __int_as_float(0x7f800000))
-                    atomicMin(s_wmin + col + j, f2ord(mn[j]));
         __syncthreads();
         for (int s = threadIdx.x; s < S; s += blockDim.x)
             if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
@@ -725,11 +741,6 @@ __global__ void k_ord_to_float(const int32_t *__restrict__ k, float *__restrict_
         f[i] = ord2f(k[i]);
 }
 
-__global__ void k_check_t(const float *__restrict__ t, int32_t S, uint32_t *err) {
-    for (int i = threadIdx.x; i < S; i += blockDim.x)
-        if (!isfinite(t[i])) atomicOr(err, ERR_NONFINITE);
-}
-
 // slack = fl(rat - at) for every node and scenario, the worst slack per scenario
 // (ordered-int atomicMin), optional slack store: the epilogue of the concurrent
 // batch, where the backward kernel runs next to the forward one and never sees at.
@@ -740,39 +751,56 @@ __global__ void k_slack_wns(const float *__restrict__ at, const float *__restric
     extern __shared__ int32_t s_wmin[];
     for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
     __syncthreads();
-    const int lpn = S / V;
-    const int apb = blockDim.x / lpn * lpn;             // active threads per block
-    const int64_t step = int64_t(gridDim.x) * apb;      // a multiple of lpn: lane fixed
-    const int lane = int(threadIdx.x % lpn);
-    float mn[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
-    if (int(threadIdx.x) < apb) {
-        for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < int64_t(n) * lpn; t += step) {
-            const int64_t o = (t / lpn) * S + int64_t(lane) * V;
-            Vec<V> a, r, sl;
-            if constexpr (V == 4) {
-                const float4 x = __ldcs(reinterpret_cast<const float4 *>(at + o));
-                const float4 y = __ldcs(reinterpret_cast<const float4 *>(rat + o));
-                a.x[0] = x.x; a.x[1] = x.y; a.x[2] = x.z; a.x[3] = x.w;
-                r.x[0] = y.x; r.x[1] = y.y; r.x[2] = y.z; r.x[3] = y.w;
-            } else {
-#pragma unroll
-                for (int j = 0; j < V; ++j) {
-                    a.x[j] = __ldcs(at + o + j);
-                    r.x[j] = __ldcs(rat + o + j);
-                }
-            }
+    const int lpn = S / V;   // column vectors per row
+    // one (row, column vector): slack, its optional store, the minimum into mn
+    auto one = [&](int64_t row, int64_t col, float *mn) {
+        const int64_t o = row * S + col;
+        Vec<V> a, r, sl;
+        if constexpr (V == 4) {
+            const float4 x = __ldcs(reinterpret_cast<const float4 *>(at + o));
+            const float4 y = __ldcs(reinterpret_cast<const float4 *>(rat + o));
+            a.x[0] = x.x; a.x[1] = x.y; a.x[2] = x.z; a.x[3] = x.w;
+            r.x[0] = y.x; r.x[1] = y.y; r.x[2] = y.z; r.x[3] = y.w;
+        } else {
 #pragma unroll
             for (int j = 0; j < V; ++j) {
-                sl.x[j] = EARLY ? __fsub_rn(a.x[j], r.x[j]) : __fsub_rn(r.x[j], a.x[j]);
-                mn[j] = fminf(mn[j], sl.x[j]);
+                a.x[j] = __ldcs(at + o + j);
+                r.x[j] = __ldcs(rat + o + j);
             }
-            if (slack) st_plain<V>(slack + o, sl);
         }
 #pragma unroll
-        for (int j = 0; j < V; ++j)
-            if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + lane * V + j, f2ord(mn[j]));
+        for (int j = 0; j < V; ++j) {
+            sl.x[j] = EARLY ? __fsub_rn(a.x[j], r.x[j]) : __fsub_rn(r.x[j], a.x[j]);
+            mn[j] = fminf(mn[j], sl.x[j]);
+        }
+        if (slack) st_plain<V>(slack + o, sl);
+    };
+    if (lpn <= int(blockDim.x)) {
+        const int apb = blockDim.x / lpn * lpn;             // active threads per block
+        const int64_t step = int64_t(gridDim.x) * apb;      // a multiple of lpn: lane fixed
+        const int lane = int(threadIdx.x % lpn);
+        float mn[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+        if (int(threadIdx.x) < apb) {
+            for (int64_t t = blockIdx.x * int64_t(apb) + threadIdx.x; t < int64_t(n) * lpn; t += step)
+                one(t / lpn, int64_t(lane) * V, mn);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + lane * V + j, f2ord(mn[j]));
+        }
+    } else {
+        // rows wider than the block: column vectors strided over the threads, minima
+        // per thread and column vector over the block's rows
+        for (int cv = threadIdx.x; cv < lpn; cv += blockDim.x) {
+            float mn[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) mn[j] = __int_as_float(0x7f800000);
+            for (int64_t row = blockIdx.x; row < n; row += gridDim.x) one(row, int64_t(cv) * V, mn);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (mn[j] != __int_as_float(0x7f800000)) atomicMin(s_wmin + cv * V + j, f2ord(mn[j]));
+        }
     }
     __syncthreads();
     for (int s = threadIdx.x; s < S; s += blockDim.x)
@@ -1005,9 +1033,9 @@ int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
+template <int V, int LPN, bool FWD, bool GA, bool EARLY>
 void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
-    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA, EARLY>;
+    auto kern = k_flow<V, LPN, FWD, GA, EARLY>;
     constexpr int SC = V * LPN;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
@@ -1043,9 +1071,9 @@ void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
 }
 
 // blocks per SM a kernel can keep resident alone (cached occupancy query)
-template <int V, int LPN, bool FWD, bool CHECK_D, bool GA, bool EARLY>
+template <int V, int LPN, bool FWD, bool GA, bool EARLY>
 int occupancy_of(FlowParams &p) {
-    auto kern = k_flow<V, LPN, FWD, CHECK_D, GA, EARLY>;
+    auto kern = k_flow<V, LPN, FWD, GA, EARLY>;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, V * LPN, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
     static std::map<size_t, int> cache;
@@ -1061,12 +1089,12 @@ int occupancy_of(FlowParams &p) {
 }
 
 // op = 0: launch, op = 1: return the solo occupancy (blocks per SM)
-template <bool FWD, bool CHECK_D, bool GA, bool EARLY>
+template <bool FWD, bool GA, bool EARLY>
 int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int op) {
 #define HF_CASE(L)                                                               \
     case L:                                                                      \
-        if (op) return occupancy_of<4, L, FWD, CHECK_D, GA, EARLY>(p);           \
-        launch_flow<4, L, FWD, CHECK_D, GA, EARLY>(g, p, st, cap);               \
+        if (op) return occupancy_of<4, L, FWD, GA, EARLY>(p);           \
+        launch_flow<4, L, FWD, GA, EARLY>(g, p, st, cap);               \
         return 0;
     switch (LPN) {
         HF_CASE(16)
@@ -1078,28 +1106,28 @@ int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int 
     }
 #undef HF_CASE
 }
-template <bool FWD, bool CHECK_D, bool EARLY>
+template <bool FWD, bool EARLY>
 int dispatch_mode(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st, int cap, int op) {
     if (V == 4) {
         // the cp.async-gather variant (HF_GA=1, measured slower) exists for late mode only
         if (!EARLY && env_int("HF_GA", 0))
-            return dispatch_ga<FWD, CHECK_D, true, false>(g, p, LPN, st, cap, op);
-        return dispatch_ga<FWD, CHECK_D, false, EARLY>(g, p, LPN, st, cap, op);
+            return dispatch_ga<FWD, true, false>(g, p, LPN, st, cap, op);
+        return dispatch_ga<FWD, false, EARLY>(g, p, LPN, st, cap, op);
     } else if (V == 2) {
-        if (op) return occupancy_of<2, 1, FWD, CHECK_D, false, EARLY>(p);
-        launch_flow<2, 1, FWD, CHECK_D, false, EARLY>(g, p, st, cap);
+        if (op) return occupancy_of<2, 1, FWD, false, EARLY>(p);
+        launch_flow<2, 1, FWD, false, EARLY>(g, p, st, cap);
     } else {
-        if (op) return occupancy_of<1, 1, FWD, CHECK_D, false, EARLY>(p);
-        launch_flow<1, 1, FWD, CHECK_D, false, EARLY>(g, p, st, cap);
+        if (op) return occupancy_of<1, 1, FWD, false, EARLY>(p);
+        launch_flow<1, 1, FWD, false, EARLY>(g, p, st, cap);
     }
     return 0;
 }
-template <bool FWD, bool CHECK_D>
+template <bool FWD>
 int dispatch(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st = nullptr, int cap = 0,
              int op = 0) {
     if (!st) st = g.stream;
-    if (g.early) return dispatch_mode<FWD, CHECK_D, true>(g, p, V, LPN, st, cap, op);
-    return dispatch_mode<FWD, CHECK_D, false>(g, p, V, LPN, st, cap, op);
+    if (g.early) return dispatch_mode<FWD, true>(g, p, V, LPN, st, cap, op);
+    return dispatch_mode<FWD, false>(g, p, V, LPN, st, cap, op);
 }
 
 // host-side state of a prepared pass
@@ -1163,6 +1191,10 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     cx.nparts = FWD ? g.np_cap_in : g.np_cap_out;   // bound; exact count on the device
     const int32_t *nparts_dev = g.nparts_d + (FWD ? 0 : 1);
     cx.Q = FWD ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
+    // task ids and bases are int32: bound the pass's task count (the descriptor bound
+    // of build_tasks times the chunk count)
+    if (((int64_t(g.n) + g.m) / tw + g.L + cx.nparts + 1) * p.nch > INT32_MAX)
+        fail(HF_ERR_INVALID_ARG, "too many warp tasks for one pass (scenario count x graph size)");
     if (ts.key != tw || !ts.desc.p) {
         build_tasks<FWD>(g, p.row_ptr, p.node_of, cx.Q, cx.nparts, tw, p.nch, ts);
         ts.key = tw;
@@ -1192,8 +1224,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
 template <bool FWD>
 void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cudaStream_t st,
                  int cap) {
-    if (check_d) dispatch<FWD, true>(g, p, V, cx.LPN, st, cap);
-    else dispatch<FWD, false>(g, p, V, cx.LPN, st, cap);
+    dispatch<FWD>(g, p, V, cx.LPN, st, cap);
     if (cx.nparts > 0) {
         const int32_t *npa = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
         const int32_t *prow = npa + (FWD ? g.np_cap_in : g.np_cap_out);
@@ -1286,11 +1317,6 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
     k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
     HF_CHECK_LAUNCH();
     g.launches += 1;
-    if (t_arr) {
-        k_check_t<<<1, 256, 0, s>>>(t_arr, S, g.d_err());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
-    }
     if (g.n > 0) {
         FlowParams p{};
         const int V = pick_vec(S, {d, at, rat, slack});
@@ -1370,11 +1396,6 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
         k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
         HF_CHECK_LAUNCH();
         g.launches += 1;
-        if (t_arr) {
-            k_check_t<<<1, 256, 0, s>>>(t_arr, S, g.d_err());
-            HF_CHECK_LAUNCH();
-            g.launches += 1;
-        }
         FlowParams pf{}, pb{};
         const int V = pick_vec(S, {d, at, rat, slack});
         pf.row_ptr = g.lo_in_ptr.as<int32_t>();
@@ -1421,11 +1442,6 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
     k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
     HF_CHECK_LAUNCH();
     g.launches += 1;
-    if (t_arr) {
-        k_check_t<<<1, 256, 0, s>>>(t_arr, S, g.d_err());
-        HF_CHECK_LAUNCH();
-        g.launches += 1;
-    }
     FlowParams pf{}, pb{};
     const int V = pick_vec(S, {d, at, rat, slack});
     pf.row_ptr = g.lo_in_ptr.as<int32_t>();
@@ -1449,9 +1465,8 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
     prepare_pass<true>(g, pf, V, cf);
     prepare_pass<false>(g, pb, V, cb);
     // blocks per SM for each kernel when both are resident
-    const int of = check_d ? dispatch<true, true>(g, pf, V, cf.LPN, s, 0, 1)
-                           : dispatch<true, false>(g, pf, V, cf.LPN, s, 0, 1);
-    const int ob = dispatch<false, false>(g, pb, V, cb.LPN, s, 0, 1);
+    const int of = dispatch<true>(g, pf, V, cf.LPN, s, 0, 1);
+    const int ob = dispatch<false>(g, pb, V, cb.LPN, s, 0, 1);
     const int capf = std::max(1, env_int("HF_CAP_F", (of + 1) / 2));
     const int capb = std::max(1, env_int("HF_CAP_B", ob / 2));
     Side &sd = side_of(g);

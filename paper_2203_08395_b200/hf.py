@@ -116,6 +116,21 @@ def _ptr(x):
     return x.ctypes.data_as(ctypes.c_void_p)
 
 
+def _out(x, count: int, dtype, what: str):
+    """A host output array: must be a C-contiguous `dtype` array of >= count elements
+    (the library writes through its pointer; a wrong dtype or a short array would be
+    garbled or overrun).  None passes through (optional outputs)."""
+    if x is None or _is_torch(x):
+        return x
+    if not isinstance(x, np.ndarray) or x.dtype != np.dtype(dtype):
+        raise TypeError(f"{what}: expected a numpy {np.dtype(dtype).name} array")
+    if not x.flags["C_CONTIGUOUS"] or not x.flags["WRITEABLE"]:
+        raise ValueError(f"{what}: array must be C-contiguous and writeable")
+    if x.size < count:
+        raise ValueError(f"{what}: needs >= {count} elements, has {x.size}")
+    return x
+
+
 def _np(x, dtype):
     return None if x is None else np.ascontiguousarray(x, dtype=dtype)
 
@@ -193,6 +208,11 @@ def hf_levelize(g: Graph, level=None, level_ptr=None, order=None) -> int:
     """Levelize; optional outputs are filled in place (numpy => host variant,
     torch CUDA => device variant).  Returns L."""
     L = ctypes.c_int32()
+    for x, what in ((level, "level"), (order, "order")):
+        _out(x, g.n, np.int32, what)
+    _out(level_ptr, 1, np.int32, "level_ptr")
+    if level_ptr is not None and not _is_torch(level_ptr) and level_ptr.size < g.n + 1:
+        raise ValueError("level_ptr: needs n + 1 elements")
     if any(_is_torch(x) for x in (level, level_ptr, order)):
         _check(_lib.hf_levelize_d(g.handle, ctypes.byref(L), _ptr(level), _ptr(level_ptr),
                                   _ptr(order)))
@@ -215,6 +235,7 @@ def hf_propagate_forward(g: Graph, at_src, at):
     if _is_torch(at):
         _check(_lib.hf_propagate_forward_d(g.handle, _ptr(at_src), _ptr(at)))
     else:
+        _out(at, g.n, np.float32, "at")
         a = _np(at_src, np.float32)
         _check(_lib.hf_propagate_forward(g.handle, _ptr(a), _ptr(at)))
 
@@ -225,6 +246,9 @@ def hf_propagate_backward(g: Graph, t_req: float, at, rat, slack=None, wns=None)
         _check(_lib.hf_propagate_backward_d(g.handle, ctypes.c_float(t_req), _ptr(at), _ptr(rat),
                                             _ptr(slack), _ptr(wns)))
     else:
+        _out(rat, g.n, np.float32, "rat")
+        _out(slack, g.n, np.float32, "slack")
+        _out(wns, 1, np.float32, "wns")
         a = _np(at, np.float32)
         _check(_lib.hf_propagate_backward(g.handle, ctypes.c_float(t_req), _ptr(a), _ptr(rat),
                                           _ptr(slack), _ptr(wns)))
@@ -294,6 +318,8 @@ def hf_run_batch(g: Graph, s_local: int, delays, layout: int, t_req, at_src, wns
     else:
         if at is not None or rat is not None:
             raise ValueError("at/rat outputs are only available with device tensors")
+        _out(wns_local, s_local, np.float32, "wns_local")
+        _out(wns_all, s_local, np.float32, "wns_all")
         d = _np(delays, np.float32)
         t = _np(t_req, np.float32)
         a = _np(at_src, np.float32)
@@ -305,6 +331,7 @@ def hf_analyze(n, m, fanin_ptr, fanin_src, s_local: int, delays, t_req, at_src, 
                delay=None, device: int = 0, stream=None, keep_graph: bool = False):
     """Create + levelize + batch in one call from host arrays (scenario data uploaded
     while the graph is built).  Returns (num_levels, Graph or None)."""
+    _out(wns_local, s_local, np.float32, "wns_local")
     a = [_np(fanin_ptr, np.int32), _np(fanin_src, np.int32), _np(delay, np.float32)]
     d = _np(delays, np.float32)
     t = _np(t_req, np.float32)

@@ -51,7 +51,7 @@ def test_library_is_sm100a(hf):
 
 
 def test_status_strings_and_version(hf):
-    assert hf.hf_version() == 100
+    assert hf.hf_version() == 101
     assert hf._status_name(3) == "HF_ERR_CYCLE"
     assert hf._status_name(0) == "HF_OK"
 
