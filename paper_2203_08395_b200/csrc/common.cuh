@@ -90,6 +90,9 @@ constexpr int LO_SPLIT = 8;
 // a long row is cut into parts of LO_PE edges (part ids: exclusive scan over the
 // level-ordered rows of ceil(degree / LO_PE) for long rows, 0 otherwise)
 constexpr int LO_PE = 20;
+// the level-synchronous passes cut a long row into slices of WIDE_SL edges (one
+// thread each, all loads of a slice in flight at once)
+constexpr int WIDE_SL = 8;
 
 // ---- the graph -------------------------------------------------------------
 struct Graph {
@@ -126,6 +129,18 @@ struct Graph {
     const int32_t *nparts_d = nullptr;
     // task schedules of the dataflow propagation kernels (per direction)
     TaskSched ts_f, ts_b;
+    // level-synchronous ("wide") passes (wide.cu), built on first use after each
+    // hf_levelize: per direction the long rows cut into slices of WIDE_SL edges --
+    // wide_*_sfirst[n+1] first slice of every level-ordered row (0 slices for short
+    // rows), wide_*_slice[] {row, first edge} -- and the graph's own delays
+    // permuted into level order per direction (lo_*_d[m], single-delay-set calls)
+    DevBuf wide_in_sfirst, wide_in_slice, wide_out_sfirst, wide_out_slice;
+    // S = 1 (k_wide1): the long rows of a level as one edge range cut into chunks of
+    // 32 edges; wide_*_coff[L+1] first chunk of each level, wide_*_crow[] the row
+    // holding each chunk's first edge
+    DevBuf wide_in_coff, wide_in_crow, wide_out_coff, wide_out_crow;
+    DevBuf lo_in_d, lo_out_d;
+    bool wide_ready = false, lo_d_ready = false;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // single-pass scan state (primitives.cu): per-tile words + tile counter; one per

@@ -1291,10 +1291,28 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
 
 }  // namespace
 
+// level-synchronous passes for wide graphs (wide.cu)
+bool wide_choice(const Graph &g);
+void lo_delays_prepare(Graph &g);
+template <bool FWD>
+void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float *src_val,
+               float t_scalar, const float *other, float *out, float *slack, int32_t *wns_ord,
+               cudaStream_t st);
+
 // Forward over all levels (device pointers).  d: [m][S].
 void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                     float *at) {
     if (g.n == 0) return;
+    if (wide_choice(g)) {
+        // the graph's own delays: pre-permuted into level order (contiguous rows)
+        const bool lo = S == 1 && d == g.delay.as<float>();
+        if (lo) lo_delays_prepare(g);
+        prof_record(g, 2);
+        wide_pass<true>(g, lo ? g.lo_in_d.as<float>() : d, lo, S, at_src, 0.0f, nullptr, at,
+                        nullptr, nullptr, g.stream);
+        prof_record(g, 3);
+        return;
+    }
     FlowParams p{};
     const int V = pick_vec(S, {d, at});
     p.row_ptr = g.lo_in_ptr.as<int32_t>();
@@ -1317,7 +1335,14 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
     k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
     HF_CHECK_LAUNCH();
     g.launches += 1;
-    if (g.n > 0) {
+    if (g.n > 0 && wide_choice(g)) {
+        const bool lo = S == 1 && d == g.delay.as<float>();
+        if (lo) lo_delays_prepare(g);
+        prof_record(g, 5);
+        wide_pass<false>(g, lo ? g.lo_out_d.as<float>() : d, lo, S, t_arr, t_scalar, at, rat,
+                         slack, ord, s);
+        prof_record(g, 4);
+    } else if (g.n > 0) {
         FlowParams p{};
         const int V = pick_vec(S, {d, at, rat, slack});
         p.row_ptr = g.lo_out_ptr.as<int32_t>();
@@ -1369,7 +1394,8 @@ Side &side_of(Graph &g) {
 void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                   const float *t_arr, float *at, float *rat, float *slack, float *wns_f) {
     cudaStream_t s = g.stream;
-    if (g.n == 0 || getenv("HF_TRACE") || env_int("HF_BATCH_PLAIN", 0)) {
+    if (g.n == 0 || getenv("HF_TRACE") || env_int("HF_BATCH_PLAIN", 0) || wide_choice(g)) {
+        // (wide graphs: two level-synchronous passes, no sentinel fills to overlap)
         prof_record(g, 6);
         forward_device(g, d, S, check_d, at_src, at);
         backward_device(g, d, S, t_arr, 0.0f, at, rat, slack, wns_f);

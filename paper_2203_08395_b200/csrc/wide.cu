@@ -1,0 +1,881 @@
+// wide.cu -- level-synchronous propagation passes for WIDE graphs (many nodes per
+// level: C5, 10M nodes in ~30 levels).  SURVEY.md §8(a) a5-a7 (same recurrences as
+// propagate.cu: at[v] = max over fan-in of fl(at[u] + d), rat[u] = min over fan-out
+// of fl(rat[v] - d), slack / worst slack fused; BASELINE.json:5).
+//
+// Why a second kernel.  The dataflow kernel (propagate.cu) walks warp tasks one at a
+// time per warp: right for deep graphs, where the level-to-level hop is the critical
+// path, but on a wide level (330k rows, 640k edges at C5) a warp's ~30 loads in
+// flight per task leave the memory system idle (C5 ran at 5% of the HBM roofline).
+// Here one persistent cooperative launch sweeps the levels with a grid barrier
+// between them (~1.2 us, negligible against a wide level), and every thread owns
+// whole units of work with all their loads in flight at once:
+//   * a SHORT row (<= LO_SPLIT edges) of the level-ordered CSR x one column vector
+//     (V scenarios): up to 8 neighbour gathers + 8 delay loads issued together,
+//     combined in registers, stored once;
+//   * a SLICE of WIDE_SL edges of a long row (fan-in up to 10^4 at C5): combined in
+//     registers, then folded into the row's slot with an ordered-int atomicMax /
+//     atomicMin (exact: max / min of floats is order-independent, reading R10).
+//     Consumers of a long row read its slot (neighbour id -(first part id + 1),
+//     levelize.cu); the slots become the row's value after the pass.
+// No NaN sentinel, no task schedule, no fill of the outputs: readiness is the
+// barrier.  Reads of values written during the pass bypass L1 (ld.global.cg); the
+// barrier is release / acquire at gpu scope.
+// Single delay set with the graph's own delays: the delays are pre-permuted into
+// level order per direction (lo_*_d), so a row's delays are one contiguous run.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace hf {
+
+namespace {
+
+constexpr int WIDE_THREADS = 512;
+constexpr int32_t ORD_NEG_INF = int32_t(0x807fffff);   // f2ord(-inf)
+constexpr int32_t ORD_POS_INF = int32_t(0x7f800000);   // f2ord(+inf)
+
+template <int V> struct VecW {
+    float x[V];
+};
+
+// read-only data: through the non-coherent path
+template <int V> __device__ __forceinline__ VecW<V> ldg_v(const float *p) {
+    VecW<V> r;
+    if constexpr (V == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+    } else {
+        r.x[0] = __ldg(p);
+    }
+    return r;
+}
+// values written earlier in this pass (other SMs): L2, never a stale L1 line
+template <int V> __device__ __forceinline__ VecW<V> ldcg_v(const float *p) {
+    VecW<V> r;
+    if constexpr (V == 4) {
+        const float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
+        r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+    } else {
+        r.x[0] = __ldcg(p);
+    }
+    return r;
+}
+template <int V> __device__ __forceinline__ VecW<V> ldcg_ord(const int32_t *p) {
+    VecW<V> r;
+    if constexpr (V == 4) {
+        const int4 t = __ldcg(reinterpret_cast<const int4 *>(p));
+        r.x[0] = ord2f(t.x); r.x[1] = ord2f(t.y); r.x[2] = ord2f(t.z); r.x[3] = ord2f(t.w);
+    } else {
+        r.x[0] = ord2f(__ldcg(p));
+    }
+    return r;
+}
+template <int V> __device__ __forceinline__ void st_v(float *p, const VecW<V> &v) {
+    if constexpr (V == 4) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
+    } else {
+        *p = v.x[0];
+    }
+}
+
+template <bool MX> __device__ __forceinline__ float comb(float a, float b) {
+    return MX ? fmaxf(a, b) : fminf(a, b);
+}
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// grid barrier of a cooperative launch (monotonic counter, target grows per call)
+__device__ __forceinline__ void grid_bar(unsigned *ctr, unsigned &target) {
+    target += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        while (ld_acq(ctr) < target) __nanosleep(32);
+    }
+    __syncthreads();
+}
+
+struct WideParams {
+    const int32_t *level_ptr;   // [L+1]
+    const int32_t *lstart;      // [L] first long row of each level
+    const int32_t *row_ptr;     // [n+1] level-ordered CSR of this direction
+    const int32_t *nbr;         // [m] neighbour id, or -(first part id + 1) if long
+    const int32_t *eid;         // [m] delay row of each position, or null: d is level-ordered
+    const int32_t *node_of;     // [n]
+    const int32_t *q;           // [n+1] first part id of each row (slot index of long rows)
+    const int32_t *sfirst;      // [n+1] first slice of each row
+    const int2 *slice;          // {row, first edge}
+    const int32_t *part_np;     // [np_cap] parts of the long row at its first part id
+    const int32_t *part_row;    // [np_cap] that row
+    const int32_t *nparts_d;    // exact part-id count
+    int32_t L, S;
+    const float *d;             // [m][S] by eid (or by position when eid is null)
+    const float *src_val;       // forward: at_src [n] or null; backward: t_req [S] or null
+    float t_scalar;             // backward: T when t_req is null
+    const float *other;         // backward: at (slack), or null
+    float *out;                 // at (forward) / rat (backward) [n][S]
+    float *slack;               // [n][S] or null
+    int32_t *slot;              // [parts][S] ordered ints
+    int32_t *wns_ord;           // [S] (backward with other)
+    uint32_t *err;
+    unsigned *bar;              // zeroed grid-barrier counter
+};
+
+template <int V, bool FWD, bool EARLY>
+__global__ void __launch_bounds__(WIDE_THREADS) k_wide(WideParams p) {
+    constexpr bool MX = FWD != EARLY;   // combine with max (late forward / early backward)
+    constexpr int EB = V == 1 ? 8 : 4;  // edges in flight per batch
+    extern __shared__ int32_t s_wmin[];
+    const int S = p.S;
+    const bool do_slack = !FWD && p.other;
+    if (do_slack) {
+        for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = ORD_POS_INF;
+    }
+    const int T = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned target = 0;
+    // slots of the long rows start at the combine's identity
+    const int64_t nslot = int64_t(*p.nparts_d) * S;
+    for (int64_t i = tid; i < nslot; i += T) p.slot[i] = MX ? ORD_NEG_INF : ORD_POS_INF;
+    grid_bar(p.bar, target);
+
+    const int lpn = S / V;               // column vectors per row
+    const int upt = T / lpn;             // units per sweep of the grid
+    const bool active = tid < upt * lpn;
+    const int cv = tid % lpn, u0 = tid / lpn;
+    const int64_t col = int64_t(cv) * V;
+    bool bad = false;
+    float mn[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) mn[j] = __int_as_float(ORD_POS_INF);
+    const int L = p.L;
+    for (int qq = 0; qq < L; ++qq) {
+        const int k = FWD ? qq : L - 1 - qq;
+        const int ls = __ldg(p.level_ptr + k), le = __ldg(p.level_ptr + k + 1);
+        const int lo = __ldg(p.lstart + k);
+        const int nshort = lo - ls;
+        const int s0 = __ldg(p.sfirst + lo);
+        const int nunits = nshort + (__ldg(p.sfirst + le) - s0);
+        for (int u = u0; active && u < nunits; u += upt) {
+            const bool lng = u >= nshort;
+            int row, eb, ee;
+            if (!lng) {
+                row = ls + u;
+                eb = __ldg(p.row_ptr + row);
+                ee = __ldg(p.row_ptr + row + 1);
+            } else {
+                const int2 sd = __ldg(p.slice + s0 + (u - nshort));
+                row = sd.x;
+                eb = sd.y;
+                ee = min(__ldg(p.row_ptr + row + 1), eb + WIDE_SL);
+            }
+            VecW<V> best;
+#pragma unroll
+            for (int j = 0; j < V; ++j) best.x[j] = __int_as_float(MX ? 0xff800000 : 0x7f800000);
+            for (int e0 = eb; e0 < ee; e0 += EB) {
+                int nb[EB];
+                int64_t dr[EB];
+#pragma unroll
+                for (int j = 0; j < EB; ++j) {
+                    const int e = e0 + j;
+                    nb[j] = 0;
+                    dr[j] = 0;
+                    if (e < ee) {
+                        nb[j] = __ldg(p.nbr + e);
+                        dr[j] = p.eid ? __ldg(p.eid + e) : e;
+                    }
+                }
+                VecW<V> a[EB], dv[EB];
+#pragma unroll
+                for (int j = 0; j < EB; ++j) {
+                    if (e0 + j < ee) {
+                        dv[j] = ldg_v<V>(p.d + dr[j] * S + col);
+                        if (nb[j] >= 0) a[j] = ldcg_v<V>(p.out + int64_t(nb[j]) * S + col);
+                        else a[j] = ldcg_ord<V>(p.slot + int64_t(-nb[j] - 1) * S + col);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < EB; ++j) {
+                    if (e0 + j < ee) {
+#pragma unroll
+                        for (int c = 0; c < V; ++c) {
+                            const float dd = sane(dv[j].x[c], bad);
+                            const float x = FWD ? __fadd_rn(a[j].x[c], dd) : __fsub_rn(a[j].x[c], dd);
+                            best.x[c] = comb<MX>(best.x[c], x);
+                        }
+                    }
+                }
+            }
+            if (!lng) {
+                const int node = __ldg(p.node_of + row);
+                if (ee == eb) {   // source (forward) / sink (backward)
+#pragma unroll
+                    for (int c = 0; c < V; ++c)
+                        best.x[c] = FWD ? (p.src_val ? sane(__ldg(p.src_val + node), bad) : 0.0f)
+                                        : sane(p.src_val ? __ldg(p.src_val + col + c) : p.t_scalar, bad);
+                }
+                st_v<V>(p.out + int64_t(node) * S + col, best);
+                if (do_slack) {
+                    const VecW<V> av = ldg_v<V>(p.other + int64_t(node) * S + col);
+                    VecW<V> sl;
+#pragma unroll
+                    for (int c = 0; c < V; ++c) {
+                        sl.x[c] = EARLY ? __fsub_rn(av.x[c], best.x[c]) : __fsub_rn(best.x[c], av.x[c]);
+                        mn[c] = fminf(mn[c], sl.x[c]);
+                    }
+                    if (p.slack) st_v<V>(p.slack + int64_t(node) * S + col, sl);
+                }
+            } else {
+                int32_t *sp = p.slot + int64_t(__ldg(p.q + row)) * S + col;
+#pragma unroll
+                for (int c = 0; c < V; ++c) {
+                    if (MX) atomicMax(sp + c, f2ord(best.x[c]));
+                    else atomicMin(sp + c, f2ord(best.x[c]));
+                }
+            }
+        }
+        grid_bar(p.bar, target);
+    }
+    // long rows: the slot is the row's value; slack and worst slack
+    const int64_t nparts = *p.nparts_d;
+    for (int64_t pp = u0; active && pp < nparts; pp += upt) {
+        if (__ldg(p.part_np + pp) == 0) continue;   // not a first part id
+        const int node = __ldg(p.node_of + __ldg(p.part_row + pp));
+        const VecW<V> v = ldcg_ord<V>(p.slot + pp * S + col);
+        st_v<V>(p.out + int64_t(node) * S + col, v);
+        if (do_slack) {
+            const VecW<V> av = ldg_v<V>(p.other + int64_t(node) * S + col);
+            VecW<V> sl;
+#pragma unroll
+            for (int c = 0; c < V; ++c) {
+                sl.x[c] = EARLY ? __fsub_rn(av.x[c], v.x[c]) : __fsub_rn(v.x[c], av.x[c]);
+                mn[c] = fminf(mn[c], sl.x[c]);
+            }
+            if (p.slack) st_v<V>(p.slack + int64_t(node) * S + col, sl);
+        }
+    }
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
+    if (do_slack) {
+        if (active)
+#pragma unroll
+            for (int c = 0; c < V; ++c)
+                if (mn[c] != __int_as_float(ORD_POS_INF)) atomicMin(s_wmin + col + c, f2ord(mn[c]));
+        __syncthreads();
+        for (int s = threadIdx.x; s < S; s += blockDim.x)
+            if (s_wmin[s] != ORD_POS_INF) atomicMin(p.wns_ord + s, s_wmin[s]);
+    }
+}
+
+// ---- S = 1: warp-cooperative level-synchronous pass (k_wide1) -------------------
+// A warp unit is either 32 consecutive short rows of the level (their edges are one
+// contiguous run of the level-ordered CSR) or a chunk of 32 consecutive edges of the
+// level's long rows (one contiguous run as well: long rows sit at the end of their
+// level).  Edges are processed 32 at a time, one per lane, all loads coalesced; a
+// lane finds its row by a shuffle binary search over the row ends held by the
+// lanes, and a segmented max / min scan over the lanes combines each row's edges.
+// Short rows: the segment ends combine into a per-warp shared row buffer, then lane
+// j stores row j.  Long rows: the segment ends fold into the row's slot (ordered-int
+// atomic).  The barrier between levels is split: a block arrives as soon as its
+// stores are issued, loads the structure of its first unit of the next level (row
+// offsets, neighbours, delays: nothing written in the pass) and only then waits,
+// so after the barrier a unit is one gather round trip from its result.
+constexpr int W1_THREADS = 256;
+constexpr int W1_NU = 4;   // units of a warp per level whose structure is held in registers
+constexpr int W1_CH = 2;   // edge chunks (32 edges) of a unit held in registers
+
+struct Wide1Params {
+    const int32_t *level_ptr, *lstart, *row_ptr, *nbr, *eid, *node_of, *q;
+    const int32_t *coff, *crow;
+    const int32_t *part_np, *part_row, *nparts_d;
+    int32_t L;
+    const float *d;        // [m] by eid, or level-ordered when eid is null
+    const float *src_val;  // forward: at_src [n] / null; backward: t_req [1] / null
+    float t_scalar;
+    const float *other;    // backward: at (slack) or null
+    float *out, *slack;
+    int32_t *slot, *wns_ord;
+    uint32_t *err;
+    unsigned *bar;
+};
+
+struct LevelInfo {
+    int ls, lo, le, lbase, lend, c0, us, nu;
+};
+
+__device__ __forceinline__ LevelInfo level_info(const Wide1Params &p, int k) {
+    LevelInfo li;
+    li.ls = __ldg(p.level_ptr + k);
+    li.le = __ldg(p.level_ptr + k + 1);
+    li.lo = __ldg(p.lstart + k);
+    li.lbase = __ldg(p.row_ptr + li.lo);
+    li.lend = __ldg(p.row_ptr + li.le);
+    li.c0 = __ldg(p.coff + k);
+    li.us = (li.lo - li.ls + 31) >> 5;
+    li.nu = li.us + (__ldg(p.coff + k + 1) - li.c0);
+    return li;
+}
+
+// The structure of W1_NU units (nothing written during the pass): row offsets and
+// nodes (short units) or the chunk's first row, row ends and slot ids (long chunks),
+// neighbours and delays / delay ids of the first W1_CH chunks.  Two dependent load
+// rounds, every unit's loads of a round in flight together.
+struct Units {
+    int kind[W1_NU];   // 0: none, 1: short rows, 2: long-row chunk
+    int r0[W1_NU], base[W1_NU], ne[W1_NU];
+    int pj[W1_NU], qj[W1_NU], node[W1_NU];   // lane j: short: start / end / node of row r0+j;
+                                             // long: slot / end of row r0+j
+    int nb[W1_NU][W1_CH], dx[W1_CH][W1_NU];
+};
+
+__device__ __forceinline__ void load_units(const Wide1Params &p, const LevelInfo &li, int u0,
+                                           int ustep, Units &U) {
+    const int lane = threadIdx.x & 31;
+    // round 1: row offsets / nodes of short units; chunk row + edges of long units
+#pragma unroll
+    for (int i = 0; i < W1_NU; ++i) {
+        const int u = u0 + i * ustep;
+        U.kind[i] = u >= li.nu ? 0 : (u < li.us ? 1 : 2);
+        U.pj[i] = U.qj[i] = INT32_MAX;
+        U.node[i] = 0;
+        U.ne[i] = 0;
+#pragma unroll
+        for (int c = 0; c < W1_CH; ++c) U.nb[i][c] = U.dx[c][i] = 0;
+        if (U.kind[i] == 1) {
+            U.r0[i] = li.ls + (u << 5);
+            const int r = U.r0[i] + lane;
+            if (r < li.lo) {
+                U.pj[i] = __ldg(p.row_ptr + r);
+                U.qj[i] = __ldg(p.row_ptr + r + 1);
+                U.node[i] = __ldg(p.node_of + r);
+            }
+        } else if (U.kind[i] == 2) {
+            const int c = u - li.us;
+            U.base[i] = li.lbase + (c << 5);
+            U.ne[i] = min(32, li.lend - U.base[i]);
+            U.r0[i] = __ldg(p.crow + li.c0 + c);
+            if (lane < U.ne[i]) {
+                const int e = U.base[i] + lane;
+                U.nb[i][0] = __ldg(p.nbr + e);
+                U.dx[0][i] = p.eid ? __ldg(p.eid + e) : __float_as_int(__ldg(p.d + e));
+            }
+        }
+    }
+    // round 2: edges of short units; row ends and slots of long chunks
+#pragma unroll
+    for (int i = 0; i < W1_NU; ++i) {
+        if (U.kind[i] == 1) {
+            const int nrows = min(32, li.lo - U.r0[i]);
+            U.base[i] = __shfl_sync(0xffffffffu, U.pj[i], 0);
+            U.ne[i] = __shfl_sync(0xffffffffu, U.qj[i], nrows - 1) - U.base[i];
+#pragma unroll
+            for (int c = 0; c < W1_CH; ++c) {
+                if ((c << 5) + lane < U.ne[i]) {
+                    const int e = U.base[i] + (c << 5) + lane;
+                    U.nb[i][c] = __ldg(p.nbr + e);
+                    U.dx[c][i] = p.eid ? __ldg(p.eid + e) : __float_as_int(__ldg(p.d + e));
+                }
+            }
+        } else if (U.kind[i] == 2) {
+            const int r = U.r0[i] + lane;
+            if (r < li.le) {
+                U.qj[i] = __ldg(p.row_ptr + r + 1);
+                U.pj[i] = __ldg(p.q + r);
+            }
+        }
+    }
+}
+
+// one chunk of 32 edges of a unit: x = fl(a[u] +/- d) per lane, rows by a shuffle
+// binary search over the lanes' row ends, a segmented scan combines each row's
+// edges; the segment ends go to the warp's row buffer (short) or the row's slot
+template <bool FWD, bool EARLY>
+__device__ __forceinline__ void chunk_combine(const Wide1Params &p, int kind, int e, bool valid,
+                                              float x, int qj, int pj, float *s_val) {
+    constexpr bool MX = FWD != EARLY;
+    const int lane = threadIdx.x & 31;
+    int r = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+        const int t = __shfl_sync(0xffffffffu, qj, r + step - 1);
+        if (t <= e) r += step;
+    }
+    const int rr = valid ? r : 32 + lane;
+    const int prv = __shfl_up_sync(0xffffffffu, rr, 1);
+    const int nxt = __shfl_down_sync(0xffffffffu, rr, 1);
+    const unsigned smask = __ballot_sync(0xffffffffu, lane == 0 || prv != rr);
+    const int sstart = 31 - __clz(smask & ((2u << lane) - 1u));
+    float v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane - o >= sstart) v = comb<MX>(v, y);
+    }
+    const bool seg_end = valid && (lane == 31 || nxt != rr);
+    const int slot_id = __shfl_sync(0xffffffffu, pj, r & 31);
+    if (seg_end) {
+        if (kind == 1) {
+            s_val[r] = comb<MX>(s_val[r], v);
+        } else {
+            if (MX) atomicMax(p.slot + slot_id, f2ord(v));
+            else atomicMin(p.slot + slot_id, f2ord(v));
+        }
+    }
+}
+
+template <bool FWD>
+__device__ __forceinline__ float relax1(float a, float d) {
+    return FWD ? __fadd_rn(a, d) : __fsub_rn(a, d);
+}
+
+// gathers of every unit at once (one round trip), then per unit: combine, store
+template <bool FWD, bool EARLY>
+__device__ __forceinline__ void finish_units(const Wide1Params &p, const Units &U, float *s_val,
+                                             bool &bad, float &mn) {
+    constexpr bool MX = FWD != EARLY;
+    const int lane = threadIdx.x & 31;
+    const float ident = __int_as_float(MX ? 0xff800000 : 0x7f800000);
+    const bool do_slack = !FWD && p.other;
+    float a[W1_NU][W1_CH], dd[W1_NU][W1_CH], at_node[W1_NU];
+#pragma unroll
+    for (int i = 0; i < W1_NU; ++i) {
+        at_node[i] = 0.0f;
+        if (do_slack && U.kind[i] == 1 && U.qj[i] != INT32_MAX) at_node[i] = __ldg(p.other + U.node[i]);
+#pragma unroll
+        for (int c = 0; c < W1_CH; ++c) {
+            a[i][c] = ident;
+            dd[i][c] = 0.0f;
+            if (U.kind[i] && (c << 5) + lane < U.ne[i]) {
+                const int nb = U.nb[i][c];
+                a[i][c] = nb >= 0 ? __ldcg(p.out + nb) : ord2f(__ldcg(p.slot + (-nb - 1)));
+                dd[i][c] = p.eid ? __ldg(p.d + U.dx[c][i]) : __int_as_float(U.dx[c][i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < W1_NU; ++i) {
+        if (!U.kind[i]) continue;
+        if (U.kind[i] == 1) s_val[lane] = ident;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < W1_CH; ++c) {
+            if ((c << 5) < U.ne[i]) {
+                const int k = (c << 5) + lane;
+                const bool valid = k < U.ne[i];
+                const float x = valid ? relax1<FWD>(a[i][c], sane(dd[i][c], bad)) : ident;
+                chunk_combine<FWD, EARLY>(p, U.kind[i], U.base[i] + k, valid, x, U.qj[i], U.pj[i],
+                                          s_val);
+                __syncwarp();
+            }
+        }
+        // short units with more than W1_CH chunks (rows of up to 8 edges): the rest
+        for (int c = W1_CH; (c << 5) < U.ne[i]; ++c) {
+            const int k = (c << 5) + lane;
+            const bool valid = k < U.ne[i];
+            float x = ident;
+            if (valid) {
+                const int e = U.base[i] + k;
+                const int nb = __ldg(p.nbr + e);
+                const float av = nb >= 0 ? __ldcg(p.out + nb) : ord2f(__ldcg(p.slot + (-nb - 1)));
+                const float dv = p.eid ? __ldg(p.d + __ldg(p.eid + e)) : __ldg(p.d + e);
+                x = relax1<FWD>(av, sane(dv, bad));
+            }
+            chunk_combine<FWD, EARLY>(p, U.kind[i], U.base[i] + k, valid, x, U.qj[i], U.pj[i],
+                                      s_val);
+            __syncwarp();
+        }
+        if (U.kind[i] == 1 && U.qj[i] != INT32_MAX) {
+            float best;
+            if (U.qj[i] > U.pj[i]) {
+                best = s_val[lane];
+            } else {   // source (forward) / sink (backward)
+                best = FWD ? (p.src_val ? sane(__ldg(p.src_val + U.node[i]), bad) : 0.0f)
+                           : sane(p.src_val ? __ldg(p.src_val) : p.t_scalar, bad);
+            }
+            p.out[U.node[i]] = best;
+            if (do_slack) {
+                const float sl = EARLY ? __fsub_rn(at_node[i], best) : __fsub_rn(best, at_node[i]);
+                mn = fminf(mn, sl);
+                if (p.slack) p.slack[U.node[i]] = sl;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <bool FWD, bool EARLY>
+__global__ void __launch_bounds__(W1_THREADS) k_wide1(Wide1Params p) {
+    constexpr bool MX = FWD != EARLY;
+    __shared__ float s_rows[W1_THREADS / 32][32];
+    __shared__ int32_t s_wmin;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float *s_val = s_rows[wib];
+    if (threadIdx.x == 0) s_wmin = ORD_POS_INF;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = gridDim.x * blockDim.x;
+    const int W = T >> 5;
+    const int w = wib * gridDim.x + blockIdx.x;   // consecutive units on different SMs
+    unsigned target = 0;
+    const int64_t nslot = *p.nparts_d;
+    for (int64_t i = tid; i < nslot; i += T) p.slot[i] = MX ? ORD_NEG_INF : ORD_POS_INF;
+    const int L = p.L;
+    LevelInfo li = level_info(p, FWD ? 0 : L - 1);
+    Units U;
+    load_units(p, li, w, W, U);
+    grid_bar(p.bar, target);
+    bool bad = false;
+    float mn = __int_as_float(ORD_POS_INF);
+    for (int qq = 0; qq < L; ++qq) {
+        // round 0 was loaded before the barrier; a warp with more than W1_NU units in
+        // this level loads the further rounds here
+        for (int r0 = 0; w + r0 * W1_NU * W < li.nu; ++r0) {
+            if (r0) load_units(p, li, w + r0 * W1_NU * W, W, U);
+            finish_units<FWD, EARLY>(p, U, s_val, bad, mn);
+        }
+        if (qq + 1 == L) break;
+        // split barrier: arrive, load the next level's first round, wait
+        target += gridDim.x;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+        li = level_info(p, FWD ? qq + 1 : L - 2 - qq);
+        load_units(p, li, w, W, U);
+        if (threadIdx.x == 0)
+            while (ld_acq(p.bar) < target) __nanosleep(32);
+        __syncthreads();
+    }
+    grid_bar(p.bar, target);
+    // long rows: the slot is the row's value; slack and worst slack
+    const bool do_slack = !FWD && p.other;
+    const int64_t nparts = *p.nparts_d;
+    for (int64_t pp = tid; pp < nparts; pp += T) {
+        if (__ldg(p.part_np + pp) == 0) continue;   // not a first part id
+        const int node = __ldg(p.node_of + __ldg(p.part_row + pp));
+        const float v = ord2f(__ldcg(p.slot + pp));
+        p.out[node] = v;
+        if (do_slack) {
+            const float a = __ldg(p.other + node);
+            const float sl = EARLY ? __fsub_rn(a, v) : __fsub_rn(v, a);
+            mn = fminf(mn, sl);
+            if (p.slack) p.slack[node] = sl;
+        }
+    }
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
+    if (do_slack) {
+        // warp minimum, then one shared and one global atomic per block
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        __syncthreads();
+        if (lane == 0 && mn != __int_as_float(ORD_POS_INF)) atomicMin(&s_wmin, f2ord(mn));
+        __syncthreads();
+        if (threadIdx.x == 0 && s_wmin != ORD_POS_INF) atomicMin(p.wns_ord, s_wmin);
+    }
+}
+
+// chunk tables of the long rows (k_wide1): per level the number of 32-edge chunks
+// of its long-row run, exclusive scan in one block (levels ascending)
+__global__ void __launch_bounds__(1024) k_w1_coff(const int32_t *__restrict__ level_ptr,
+                                                  const int32_t *__restrict__ lstart,
+                                                  const int32_t *__restrict__ row_ptr, int32_t L,
+                                                  int32_t *__restrict__ coff) {
+    __shared__ int warp_s[32];
+    __shared__ int carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int k0 = 0; k0 < L; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        int v = 0;
+        if (k < L) v = (row_ptr[level_ptr[k + 1]] - row_ptr[lstart[k]] + 31) >> 5;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_s[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int sx = lane < nw ? warp_s[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, sx, o);
+                if (lane >= o) sx += y;
+            }
+            if (lane < nw) warp_s[lane] = sx;
+        }
+        __syncthreads();
+        if (k < L) coff[k] = carry + (wid ? warp_s[wid - 1] : 0) + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_s[nw - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) coff[L] = carry;
+}
+// crow[coff[k] + c] = the long row of level k holding the level's long-run edge 32c
+__global__ void k_w1_crow(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                          const int32_t *__restrict__ level, const int32_t *__restrict__ lstart,
+                          const int32_t *__restrict__ coff, int32_t n, int32_t *__restrict__ crow) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int k = __ldg(level + __ldg(node_of + i));
+        const int lo = __ldg(lstart + k);
+        if (i < lo) continue;
+        const int base = row_ptr[lo];
+        const int b = row_ptr[i] - base, e = row_ptr[i + 1] - base;
+        for (int c = (b + 31) >> 5; (c << 5) < e; ++c) crow[coff[k] + c] = int(i);
+    }
+}
+
+// slices of the long rows: count per row, then {row, first edge} per slice
+__global__ void k_wide_count(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                             const int32_t *__restrict__ level, const int32_t *__restrict__ lstart,
+                             int32_t n, int32_t *__restrict__ cnt) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int c = 0;
+        if (i < n && i >= __ldg(lstart + __ldg(level + __ldg(node_of + i))))
+            c = (row_ptr[i + 1] - row_ptr[i] + WIDE_SL - 1) / WIDE_SL;
+        cnt[i] = c;
+    }
+}
+__global__ void k_wide_slices(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ sfirst,
+                              int32_t n, int2 *__restrict__ slice) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int f = sfirst[i], c = sfirst[i + 1] - f;
+        const int rb = row_ptr[i];
+        for (int t = 0; t < c; ++t) slice[f + t] = make_int2(int(i), rb + t * WIDE_SL);
+    }
+}
+// the graph's delays in level order of one direction
+__global__ void k_gather_delay(const float *__restrict__ delay, const int32_t *__restrict__ eid,
+                               int32_t m, float *__restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x)
+        out[e] = delay[eid[e]];
+}
+
+int env_int_w(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <int V, bool FWD, bool EARLY>
+void launch_wide(Graph &g, WideParams &p, cudaStream_t st) {
+    auto kern = k_wide<V, FWD, EARLY>;
+    const size_t smem = sizeof(int32_t) * size_t(p.S);
+    static std::map<std::tuple<const void *, size_t, int>, int> cache;
+    static std::mutex mu;
+    int per_sm = 0;
+    const auto key = std::make_tuple((const void *)kern, smem, g.device);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WIDE_THREADS, smem));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = per_sm;
+    }
+    if (per_sm < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
+    const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    void *args[] = {&p};
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms * per_sm, WIDE_THREADS, args, smem,
+                                        st));
+    g.launches += 1;
+}
+
+template <bool FWD, bool EARLY>
+void launch_w1(Graph &g, Wide1Params &p, cudaStream_t st) {
+    auto kern = k_wide1<FWD, EARLY>;
+    static std::map<std::pair<const void *, int>, int> cache;
+    static std::mutex mu;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({(const void *)kern, g.device});
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W1_THREADS, 0));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[{(const void *)kern, g.device}] = per_sm;
+    }
+    if (per_sm < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
+    const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    void *args[] = {&p};
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms * per_sm, W1_THREADS, args, 0, st));
+    g.launches += 1;
+}
+
+}  // namespace
+
+// Build (once per levelization) the slices of both directions.
+void wide_prepare(Graph &g) {
+    if (g.wide_ready) return;
+    cudaStream_t s = g.stream;
+    const int32_t n = g.n, m = g.m;
+    const int64_t scap = int64_t(m) / WIDE_SL + int64_t(m) / (LO_SPLIT + 1) + 1;
+    DevBuf cnt;
+    cnt.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool in = dir == 0;
+        const int32_t *rp = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+        const int32_t *no = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+        const int32_t *ls = in ? g.lo_in_lstart.as<int32_t>() : g.lo_out_lstart.as<int32_t>();
+        DevBuf &sf = in ? g.wide_in_sfirst : g.wide_out_sfirst;
+        DevBuf &sl = in ? g.wide_in_slice : g.wide_out_slice;
+        sf.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
+        sl.alloc(sizeof(int2) * size_t(scap), s);
+        k_wide_count<<<grid_for(int64_t(n) + 1, 256, g.sms), 256, 0, s>>>(
+            rp, no, g.level.as<int32_t>(), ls, n, cnt.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        scan_exclusive(cnt.as<int32_t>(), sf.as<int32_t>(), int64_t(n) + 1, nullptr, s, g);
+        k_wide_slices<<<grid_for(n, 256, g.sms), 256, 0, s>>>(rp, sf.as<int32_t>(), n,
+                                                             sl.as<int2>());
+        HF_CHECK_LAUNCH();
+        g.launches += 2;
+        DevBuf &co = in ? g.wide_in_coff : g.wide_out_coff;
+        DevBuf &cr = in ? g.wide_in_crow : g.wide_out_crow;
+        co.alloc(sizeof(int32_t) * (int64_t(g.L) + 1), s);
+        cr.alloc(sizeof(int32_t) * size_t(int64_t(m) / 32 + g.L + 1), s);
+        k_w1_coff<<<1, 1024, 0, s>>>(g.level_ptr.as<int32_t>(), ls, rp, g.L, co.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        k_w1_crow<<<grid_for(n, 256, g.sms), 256, 0, s>>>(rp, no, g.level.as<int32_t>(), ls,
+                                                         co.as<int32_t>(), n, cr.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 2;
+    }
+    g.wide_ready = true;
+}
+
+// The graph's own delays in level order of both directions (single-set calls).
+void lo_delays_prepare(Graph &g) {
+    if (g.lo_d_ready) return;
+    cudaStream_t s = g.stream;
+    const int64_t mm = g.m > 0 ? g.m : 1;
+    g.lo_in_d.alloc(sizeof(float) * mm, s);
+    g.lo_out_d.alloc(sizeof(float) * mm, s);
+    if (g.m) {
+        k_gather_delay<<<grid_for(g.m, 256, g.sms), 256, 0, s>>>(
+            g.delay.as<float>(), g.lo_in_eid.as<int32_t>(), g.m, g.lo_in_d.as<float>());
+        HF_CHECK_LAUNCH();
+        k_gather_delay<<<grid_for(g.m, 256, g.sms), 256, 0, s>>>(
+            g.delay.as<float>(), g.lo_out_eid.as<int32_t>(), g.m, g.lo_out_d.as<float>());
+        HF_CHECK_LAUNCH();
+        g.launches += 2;
+    }
+    g.lo_d_ready = true;
+}
+
+// Should the passes of this graph run level-synchronously?  HF_WIDE=1 / 0 forces
+// the choice; by default when the mean level holds >= 32768 nodes (C5: ~333k; the
+// deep C3/C4 graph: 7500, where the dataflow kernel's overlap of levels wins).
+bool wide_choice(const Graph &g) {
+    const int f = env_int_w("HF_WIDE", -1);
+    if (f >= 0) return f != 0;
+    return g.L > 0 && int64_t(g.n) >= int64_t(g.L) * 32768;
+}
+
+// One level-synchronous pass.  d: [m][S] by edge id, or level-ordered [m] when
+// lo_delays (S == 1, the graph's own delays).  wns_ord [S] must hold +inf ords.
+template <bool FWD>
+void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float *src_val,
+               float t_scalar, const float *other, float *out, float *slack, int32_t *wns_ord,
+               cudaStream_t st) {
+    wide_prepare(g);
+    WideParams p{};
+    const bool in = FWD;
+    p.level_ptr = g.level_ptr.as<int32_t>();
+    p.lstart = in ? g.lo_in_lstart.as<int32_t>() : g.lo_out_lstart.as<int32_t>();
+    p.row_ptr = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+    p.nbr = in ? g.lo_in_nbr.as<int32_t>() : g.lo_out_nbr.as<int32_t>();
+    p.eid = lo_delays ? nullptr : (in ? g.lo_in_eid.as<int32_t>() : g.lo_out_eid.as<int32_t>());
+    p.node_of = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+    p.q = in ? g.lo_in_q.as<int32_t>() : g.lo_out_q.as<int32_t>();
+    p.sfirst = in ? g.wide_in_sfirst.as<int32_t>() : g.wide_out_sfirst.as<int32_t>();
+    p.slice = in ? g.wide_in_slice.as<int2>() : g.wide_out_slice.as<int2>();
+    const int32_t npcap = in ? g.np_cap_in : g.np_cap_out;
+    p.part_np = in ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
+    p.part_row = p.part_np + npcap;
+    p.nparts_d = g.nparts_d + (in ? 0 : 1);
+    p.L = g.L;
+    p.S = S;
+    p.d = d;
+    p.src_val = src_val;
+    p.t_scalar = t_scalar;
+    p.other = other;
+    p.out = out;
+    p.slack = slack;
+    p.wns_ord = wns_ord;
+    p.err = g.d_err();
+    if (S == 1 && env_int_w("HF_WIDE1", 1)) {
+        Wide1Params w{};
+        w.level_ptr = p.level_ptr;
+        w.lstart = p.lstart;
+        w.row_ptr = p.row_ptr;
+        w.nbr = p.nbr;
+        w.eid = p.eid;
+        w.node_of = p.node_of;
+        w.q = p.q;
+        w.coff = in ? g.wide_in_coff.as<int32_t>() : g.wide_out_coff.as<int32_t>();
+        w.crow = in ? g.wide_in_crow.as<int32_t>() : g.wide_out_crow.as<int32_t>();
+        w.part_np = p.part_np;
+        w.part_row = p.part_row;
+        w.nparts_d = p.nparts_d;
+        w.L = g.L;
+        w.d = d;
+        w.src_val = src_val;
+        w.t_scalar = t_scalar;
+        w.other = other;
+        w.out = out;
+        w.slack = slack;
+        w.wns_ord = wns_ord;
+        w.err = p.err;
+        DevBuf slots1, bar1;
+        slots1.alloc(sizeof(int32_t) * std::max<size_t>(size_t(npcap), 1), st);
+        bar1.alloc(sizeof(unsigned) * 2, st);
+        HF_CUDA(cudaMemsetAsync(bar1.p, 0, sizeof(unsigned) * 2, st));
+        w.slot = slots1.as<int32_t>();
+        w.bar = bar1.as<unsigned>();
+        if (g.early) launch_w1<FWD, true>(g, w, st);
+        else launch_w1<FWD, false>(g, w, st);
+        return;
+    }
+    DevBuf slots, bar;
+    slots.alloc(sizeof(int32_t) * std::max<size_t>(size_t(npcap) * size_t(S), 1), st);
+    bar.alloc(sizeof(unsigned) * 2, st);
+    HF_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned) * 2, st));
+    p.slot = slots.as<int32_t>();
+    p.bar = bar.as<unsigned>();
+    const bool v4 = S % 4 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                    (!other || (reinterpret_cast<uintptr_t>(other) & 15) == 0) &&
+                    (!slack || (reinterpret_cast<uintptr_t>(slack) & 15) == 0);
+    if (g.early) {
+        if (v4) launch_wide<4, FWD, true>(g, p, st);
+        else launch_wide<1, FWD, true>(g, p, st);
+    } else {
+        if (v4) launch_wide<4, FWD, false>(g, p, st);
+        else launch_wide<1, FWD, false>(g, p, st);
+    }
+}
+
+template void wide_pass<true>(Graph &, const float *, bool, int32_t, const float *, float,
+                              const float *, float *, float *, int32_t *, cudaStream_t);
+template void wide_pass<false>(Graph &, const float *, bool, int32_t, const float *, float,
+                               const float *, float *, float *, int32_t *, cudaStream_t);
+
+}  // namespace hf
