@@ -93,6 +93,8 @@ constexpr int LO_PE = 20;
 // the level-synchronous passes cut a long row into slices of WIDE_SL edges (one
 // thread each, all loads of a slice in flight at once)
 constexpr int WIDE_SL = 8;
+// padding (elements) after the level-ordered arrays (bulk-copy overrun, wide.cu)
+constexpr int LO_PAD = 4;
 
 // ---- the graph -------------------------------------------------------------
 struct Graph {

@@ -644,16 +644,18 @@ int64_t levelize_device(Graph &g) {
     // rows (cut into part tasks by the passes); both runs keep canonical order.
     {
         const int64_t mm = m > 0 ? m : 1;
-        g.lo_in_node.alloc(sizeof(int32_t) * n, s);
-        g.lo_out_node.alloc(sizeof(int32_t) * n, s);
-        g.lo_in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        g.lo_out_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        g.lo_in_q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        g.lo_out_q.alloc(sizeof(int32_t) * (int64_t(n) + 1), s);
-        g.lo_in_nbr.alloc(sizeof(int32_t) * mm, s);
-        g.lo_in_eid.alloc(sizeof(int32_t) * mm, s);
-        g.lo_out_nbr.alloc(sizeof(int32_t) * mm, s);
-        g.lo_out_eid.alloc(sizeof(int32_t) * mm, s);
+        // +LO_PAD elements: the level-synchronous passes stage 16-byte-aligned runs of
+        // these arrays with bulk copies that may read up to 3 elements past the end
+        g.lo_in_node.alloc(sizeof(int32_t) * (int64_t(n) + LO_PAD), s);
+        g.lo_out_node.alloc(sizeof(int32_t) * (int64_t(n) + LO_PAD), s);
+        g.lo_in_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1 + LO_PAD), s);
+        g.lo_out_ptr.alloc(sizeof(int32_t) * (int64_t(n) + 1 + LO_PAD), s);
+        g.lo_in_q.alloc(sizeof(int32_t) * (int64_t(n) + 1 + LO_PAD), s);
+        g.lo_out_q.alloc(sizeof(int32_t) * (int64_t(n) + 1 + LO_PAD), s);
+        g.lo_in_nbr.alloc(sizeof(int32_t) * (mm + LO_PAD), s);
+        g.lo_in_eid.alloc(sizeof(int32_t) * (mm + LO_PAD), s);
+        g.lo_out_nbr.alloc(sizeof(int32_t) * (mm + LO_PAD), s);
+        g.lo_out_eid.alloc(sizeof(int32_t) * (mm + LO_PAD), s);
         // the two directions are independent: fan-out on the side stream, fan-in here
         DevBuf flag[2], fs[2], deg[2], parts[2], pos[2], enc[2];
         const size_t npcap = size_t(m / (LO_SPLIT + 1) + m / LO_PE + 1);

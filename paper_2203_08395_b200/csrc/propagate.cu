@@ -1292,7 +1292,7 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
 }  // namespace
 
 // level-synchronous passes for wide graphs (wide.cu)
-bool wide_choice(const Graph &g);
+bool wide_choice(const Graph &g, int32_t S);
 void lo_delays_prepare(Graph &g);
 template <bool FWD>
 void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float *src_val,
@@ -1303,7 +1303,7 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
 void forward_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                     float *at) {
     if (g.n == 0) return;
-    if (wide_choice(g)) {
+    if (wide_choice(g, S)) {
         // the graph's own delays: pre-permuted into level order (contiguous rows)
         const bool lo = S == 1 && d == g.delay.as<float>();
         if (lo) lo_delays_prepare(g);
@@ -1335,7 +1335,7 @@ void backward_device(Graph &g, const float *d, int32_t S, const float *t_arr, fl
     k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
     HF_CHECK_LAUNCH();
     g.launches += 1;
-    if (g.n > 0 && wide_choice(g)) {
+    if (g.n > 0 && wide_choice(g, S)) {
         const bool lo = S == 1 && d == g.delay.as<float>();
         if (lo) lo_delays_prepare(g);
         prof_record(g, 5);
@@ -1394,7 +1394,7 @@ Side &side_of(Graph &g) {
 void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float *at_src,
                   const float *t_arr, float *at, float *rat, float *slack, float *wns_f) {
     cudaStream_t s = g.stream;
-    if (g.n == 0 || getenv("HF_TRACE") || env_int("HF_BATCH_PLAIN", 0) || wide_choice(g)) {
+    if (g.n == 0 || getenv("HF_TRACE") || env_int("HF_BATCH_PLAIN", 0) || wide_choice(g, S)) {
         // (wide graphs: two level-synchronous passes, no sentinel fills to overlap)
         prof_record(g, 6);
         forward_device(g, d, S, check_d, at_src, at);

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(WideParams p) {
 // offsets, neighbours, delays: nothing written in the pass) and only then waits,
 // so after the barrier a unit is one gather round trip from its result.
 constexpr int W1_THREADS = 256;
-constexpr int W1_NU = 4;   // units of a warp per level whose structure is held in registers
+constexpr int W1_NU = 2;   // units of a warp per level whose structure is held in registers
 constexpr int W1_CH = 2;   // edge chunks (32 edges) of a unit held in registers
 
 struct Wide1Params {
@@ -765,7 +765,7 @@ void wide_prepare(Graph &g) {
 void lo_delays_prepare(Graph &g) {
     if (g.lo_d_ready) return;
     cudaStream_t s = g.stream;
-    const int64_t mm = g.m > 0 ? g.m : 1;
+    const int64_t mm = (g.m > 0 ? g.m : 1) + LO_PAD;
     g.lo_in_d.alloc(sizeof(float) * mm, s);
     g.lo_out_d.alloc(sizeof(float) * mm, s);
     if (g.m) {
@@ -781,12 +781,14 @@ void lo_delays_prepare(Graph &g) {
 }
 
 // Should the passes of this graph run level-synchronously?  HF_WIDE=1 / 0 forces
-// the choice; by default when the mean level holds >= 32768 nodes (C5: ~333k; the
-// deep C3/C4 graph: 7500, where the dataflow kernel's overlap of levels wins).
-bool wide_choice(const Graph &g) {
+// the choice; by default for a single delay set (S = 1) when the mean level holds
+// >= 32768 nodes (C5: ~333k; the deep C3/C4 graph: 7500, where the dataflow kernel's
+// overlap of levels wins).  With S >= 4 columns per row the dataflow kernel's
+// vectorised rows do as well or better on C5 (profiles/round2_*), so it keeps them.
+bool wide_choice(const Graph &g, int32_t S) {
     const int f = env_int_w("HF_WIDE", -1);
     if (f >= 0) return f != 0;
-    return g.L > 0 && int64_t(g.n) >= int64_t(g.L) * 32768;
+    return S == 1 && g.L > 0 && int64_t(g.n) >= int64_t(g.L) * 32768;
 }
 
 // One level-synchronous pass.  d: [m][S] by edge id, or level-ordered [m] when
