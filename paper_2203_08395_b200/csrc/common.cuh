@@ -269,6 +269,4 @@ __device__ __forceinline__ float sane(float x, bool &bad) {
     const bool ok = fabsf(x) <= 3.40282346638528859812e+38f;   // false for NaN and +-inf
     bad |= !ok;
     return ok ? canon0(x) : 0.0f;
-}
-
-}  // namespace hf
+}}  // namespace hf

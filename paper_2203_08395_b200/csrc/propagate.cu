@@ -253,6 +253,12 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
     int32_t *s_rp = reinterpret_cast<int32_t *>(wb + WL.rp);
     int32_t *s_node = reinterpret_cast<int32_t *>(wb + WL.node);
 
+    // Rejected input already flagged (by the forward pass of this batch, or by the
+    // pre-check of the concurrent batch): the results are void and the call reports
+    // HF_ERR_INVALID_ARG, so the backward pass does nothing -- which is what lets it
+    // use the delays unchecked (the forward pass checked the same delays; the graph's
+    // own delays were checked by hf_graph_create).
+    if (!FWD && (*reinterpret_cast<volatile uint32_t *>(p.err) & ERR_NONFINITE)) return;
     if (!FWD) {
         for (int s = threadIdx.x; s < S; s += blockDim.x) s_wmin[s] = 0x7f800000;
         __syncthreads();
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 Vec<V> x;
 #pragma unroll
                 for (int j = 0; j < V; ++j) {
-                    x.x[j] = relax<FWD>(av.x[j], sane(dv.x[j], bad));
+                    x.x[j] = relax<FWD>(av.x[j], FWD ? sane(dv.x[j], bad) : dv.x[j]);
                 }
                 st_s<V>(dp, x);
             }
@@ -530,7 +536,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                     Vec<V> x;
 #pragma unroll
                     for (int j = 0; j < V; ++j) {
-                        x.x[j] = relax<FWD>(a[r].x[j], sane(dv.x[j], bad));
+                        x.x[j] = relax<FWD>(a[r].x[j], FWD ? sane(dv.x[j], bad) : dv.x[j]);
                     }
                     st_s<V>(dp, x);
                 }
@@ -727,6 +733,15 @@ __global__ void k_fill_parts(uint32_t *buf, const int32_t *count, int32_t S) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
          i += int64_t(gridDim.x) * blockDim.x)
         buf[i] = 0xffffffffu;
+}
+
+// flags a NaN / inf among count floats (the concurrent batch's pre-check)
+__global__ void k_check_finite(const float *__restrict__ x, int64_t count, uint32_t *err) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+         i += int64_t(gridDim.x) * blockDim.x)
+        bad |= !(fabsf(__ldcs(x + i)) <= 3.40282346638528859812e+38f);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, ERR_NONFINITE);
 }
 
 __global__ void k_fill_i32(int32_t *p, int32_t v, int64_t count) {
@@ -1466,6 +1481,13 @@ void batch_device(Graph &g, const float *d, int32_t S, bool check_d, const float
     g.ws_wns.alloc(sizeof(int32_t) * size_t(S), s);
     int32_t *ord = g.ws_wns.as<int32_t>();
     k_fill_i32<<<1, 256, 0, s>>>(ord, 0x7f800000, S);
+    HF_CHECK_LAUNCH();
+    g.launches += 1;
+    // the two passes run side by side: the backward one cannot rely on the forward's
+    // check of the delays, so they are checked first (both kernels skip their work
+    // when the check flags a non-finite value)
+    k_check_finite<<<grid_for(int64_t(g.m) * S / 4 + 1, 256, g.sms), 256, 0, s>>>(
+        d, int64_t(g.m) * S, g.d_err());
     HF_CHECK_LAUNCH();
     g.launches += 1;
     FlowParams pf{}, pb{};

@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C5")
     ap.add_argument("--S", type=int, default=1)
+    ap.add_argument("--graph", default=None, help="graph of another config (e.g. C3 for C4)")
     ap.add_argument("--single", action="store_true", help="single-graph calls (graph delays, S=1)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--var", action="append", default=[])
@@ -46,7 +47,7 @@ def main():
     nb_f = 4 * (g.n + 1) + 8 * g.m + S * (4 * g.m + 8 * g.n)
     nb_b = 4 * (g.n + 1) + 12 * g.m + S * (4 * g.m + 12 * g.n) + 4 * S
     variants = a.var or [""]
-    res = {v: ([], []) for v in variants}
+    res = {v: ([], [], []) for v in variants}
     base_env = dict(os.environ)
     print(f"{a.config}: n={g.n} m={g.m} L={L} S={S} {'single' if a.single else 'batch'}")
     for r in range(a.reps + 1):
@@ -63,15 +64,19 @@ def main():
             else:
                 hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, at_src, w, at=at, rat=rat)
             _, fm, bm, _ = hf.hf_profile_read(G)
+            ph = hf.hf_profile_read_batch(G) if not a.single else fm + bm
             if r:
                 res[v][0].append(fm)
                 res[v][1].append(bm)
+                res[v][2].append(ph)
     os.environ.clear()
     os.environ.update(base_env)
     for v in variants:
         fm, bm = float(np.median(res[v][0])), float(np.median(res[v][1]))
+        ph = float(np.median(res[v][2]))
         print(f"{v or '(default)':40s} fwd {fm:7.3f} ms  bwd {bm:7.3f} ms  f+b {fm + bm:7.3f} ms "
-              f"{(nb_f + nb_b) / (fm + bm) / 1e6:7.1f} GB/s")
+              f"{(nb_f + nb_b) / (fm + bm) / 1e6:7.1f} GB/s  phase {ph:7.3f} ms "
+              f"({(nb_f + nb_b) / ph / 1e6:7.1f} GB/s)")
 
 
 if __name__ == "__main__":
