@@ -24,6 +24,8 @@ from __future__ import annotations
 import dataclasses
 from typing import Optional
 
+import os
+
 import numpy as np
 
 __all__ = [
@@ -295,8 +297,20 @@ def scenario_delays(g: Graph, s_begin: int, s_end: int, layout: str = "ms") -> n
     out = np.empty((S, g.m), dtype=np.float32)
     d64 = g.delay.astype(np.float64)
     idx = np.arange(g.m)
-    for i, s in enumerate(range(s_begin, s_end)):
+
+    def one(i):
+        s = s_begin + i
         out[i] = (d64 * (0.9 + 0.2 * uniform(g.seed, S_SCEN + s, idx))).astype(np.float32)
+
+    # rows are independent (keyed by global scenario id): numpy releases the GIL in
+    # its ufuncs, so large sweeps (NEXT-3, S up to 1024) generate on all host cores
+    if S * g.m >= (1 << 24):
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+            list(ex.map(one, range(S)))
+    else:
+        for i in range(S):
+            one(i)
     if layout == "sm":
         return out
     if layout == "ms":

@@ -233,7 +233,10 @@ hf_status hf_critical_path(hf_graph g, const float *at, float t_req, int32_t max
  *   id), in that order, each traced as above.  endpoints [S][K] (or NULL) receives
  *   the sink ids, -1 past the number of sinks; path [S][K][max_len]; path_len
  *   [S][K] as for hf_critical_path_d, 0 past the number of sinks.  K = 1 gives
- *   hf_critical_path_d.  Device pointers, stream-ordered; K + 1 launches. */
+ *   hf_critical_path_d.  Device pointers, stream-ordered.  2 <= K <= 32: one
+ *   selection for all K ranks (per-block sorted lists merged per scenario: 2
+ *   launches, one pass over the n x S slacks) + 1 trace launch; K > 32: one
+ *   selection pass per rank (K + 1 launches). */
 hf_status hf_critical_paths_d(hf_graph g, int32_t S, const float *delays, const float *at,
                               const float *t_req, float t_scalar, int32_t K, int32_t max_len,
                               int32_t *endpoints, int32_t *path, int32_t *path_len);

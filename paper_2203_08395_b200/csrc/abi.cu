@@ -8,6 +8,8 @@
 #include <cmath>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace hf {
@@ -116,7 +118,16 @@ static hf_status latch(Graph &g) {
     return HF_OK;
 }
 
-template <class F> static hf_status guarded(F &&f) {
+// Every hf_* entry point is one NVTX range named after the call (SURVEY.md §5
+// tracing; nvtx3 is header-only: without an attached tool a push / pop is one
+// indirect call that returns at once), and a status instead of an exception.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
+template <class F> static hf_status guarded_named(const char *name, F &&f) {
+    NvtxRange r(name);
     try {
         return f();
     } catch (const Fail &x) {
@@ -129,6 +140,8 @@ template <class F> static hf_status guarded(F &&f) {
         return HF_ERR_CUDA;
     }
 }
+
+#define guarded(...) guarded_named(__func__, __VA_ARGS__)
 
 static Graph *G(hf_graph g) { return reinterpret_cast<Graph *>(g); }
 

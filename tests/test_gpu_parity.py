@@ -405,21 +405,19 @@ def test_batch_host_api_both_layouts(hf):
 
 
 def test_batch_full_c4_and_shard_invariance(hf):
-    """C4 at full size: all 64 worst slacks exact; at/rat exact for every scenario
-    of two sampled columns; sharding into G = 2, 4, 8 blocks is bit-identical."""
+    """C4 at full size: all 64 worst slacks and the full at / rat matrices (every
+    node, every scenario) exact; sharding into G = 2, 4, 8 blocks is bit-identical."""
     g = hfgen.config("C4")
     S = 64
     D = hfgen.scenario_delays(g, 0, S, "ms")
     T = np.full(S, g.t_req, F32)
     w, at, rat = gpu_batch_device(hf, g, D, T, S)
-    wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms",
-                      threads=os.cpu_count() or 1)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms",
+                                 threads=os.cpu_count() or 1, want_at_rat=True)
     assert_bits_equal(w, wo, "wns")
-    for s in (0, 37):
-        _, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, np.ascontiguousarray(D[:, s:s + 1]),
-                                    T[s:s + 1], g.at_src, "ms", want_at_rat=True)
-        assert_bits_equal(at[:, s], ato[:, 0], f"at[:, {s}]")
-        assert_bits_equal(rat[:, s], rato[:, 0], f"rat[:, {s}]")
+    assert_bits_equal(at, ato, "at (all 64 columns)")
+    assert_bits_equal(rat, rato, "rat (all 64 columns)")
+    del ato, rato
     for G_ in (2, 4, 8):
         parts = []
         for r in range(G_):
@@ -537,10 +535,12 @@ def test_critical_path_batch_device(hf, name, scale, S):
 
 
 @pytest.mark.parametrize("name,scale,S,K", [("C3", 0.004, 8, 5), ("C3", 1.0, 4, 8),
+                                           ("C3", 0.02, 2, 32), ("C1", 1.0, 130, 2),
                                            ("C1", 1.0, 3, 40), ("chain", 0, 2, 3)])
 def test_critical_paths_top_k_device(hf, name, scale, S, K):
     # top-K endpoints per scenario (NEXT-1): endpoints, paths and lengths identical to
-    # the oracle's; the chain has one sink (endpoint -1, length 0 past it)
+    # the oracle's; the chain has one sink (endpoint -1, length 0 past it).  K <= 32
+    # takes the single selection (per-block lists + merge), K = 40 the per-rank passes
     import torch
     dev = torch.device("cuda:0")
     g = hfgen.chain(300, seed=3, relabel=True) if name == "chain" else hfgen.config(name, scale)
@@ -698,3 +698,47 @@ def test_mis_ties_tiny_and_device_api(hf):
     hf.hf_sync(G)
     assert np.array_equal(out.cpu().numpy(), oracle.mis(g.n, g.m, g.in_ptr, g.in_src, prio))
     G.close()
+
+
+@pytest.mark.parametrize("S", [256, 1024])
+def test_view_sweep_full_c3(hf, S):
+    """NEXT-3, the paper's view axis ("1024 timing reports",
+    1113-1115): S DISTINCT delay sets (hfgen keys every scenario by its global id) on
+    the full C3 graph in one batch.  Every scenario's worst slack is exact; at / rat
+    are exact for every node of the last 64-column chunk (the chunk the kernels
+    process last at the highest column offset)."""
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.config("C3")
+    B = 64
+    T = np.full(S, g.t_req, F32)
+    T[1::3] -= 2.5
+    T[2::7] += 11.0
+    d = torch.empty((g.m, S), dtype=torch.float32, device=dev)
+    wo = np.empty(S, F32)
+    chunk = S // B - 1
+    for b in range(S // B):
+        Db = hfgen.scenario_delays(g, b * B, (b + 1) * B, "ms")
+        d[:, b * B:(b + 1) * B].copy_(torch.from_numpy(Db))
+        res = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, Db, T[b * B:(b + 1) * B], g.at_src, "ms",
+                           threads=os.cpu_count() or 1, want_at_rat=(b == chunk))
+        if b == chunk:
+            wo[b * B:(b + 1) * B], ato, rato = res
+        else:
+            wo[b * B:(b + 1) * B] = res
+        del Db
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_levelize(G)
+    at = torch.empty((g.n, S), dtype=torch.float32, device=dev)
+    rat = torch.empty((g.n, S), dtype=torch.float32, device=dev)
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    hf.hf_run_batch(G, S, d, hf.HF_LAYOUT_MS, torch.from_numpy(T).to(dev),
+                    torch.from_numpy(g.at_src).to(dev), w, at=at, rat=rat)
+    hf.hf_sync(G)
+    G.close()
+    assert_bits_equal(w.cpu().numpy(), wo, f"wns S={S}")
+    c0 = chunk * B
+    assert_bits_equal(at[:, c0:c0 + B].cpu().numpy(), ato, f"at[:, {c0}:{c0 + B}]")
+    assert_bits_equal(rat[:, c0:c0 + B].cpu().numpy(), rato, f"rat[:, {c0}:{c0 + B}]")

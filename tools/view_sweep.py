@@ -4,8 +4,10 @@
 One C3 graph (1.5M pins / 2.5M arcs), levelized once; for every view count S the
 batch (forward + backward + slack + worst slack over S delay sets) is timed with
 CUDA events (median of --reps after one warm-up, L2 flushed before each rep).
-Delay sets: hfgen's 64 what-if scenarios, tiled on the device for S > 64 (the
-kernels' work and traffic do not depend on the values).
+Delay sets: S DISTINCT what-if sets (hfgen keys each scenario by its global id),
+generated on the host in blocks of 64 and uploaded into the columns of one
+[m][S] device array; the same S-view batches are parity-tested against the oracle
+at S = 256 and 1024 (tests/test_gpu_parity.py::test_view_sweep_full_c3).
 
     python tools/view_sweep.py [--S 32,64,128,256,512,1024] [--reps 3]
 """
@@ -35,7 +37,6 @@ def main():
                            delay=torch.from_numpy(g.delay).to(dev), stream=st)
     hf.hf_profile_enable(G, True)
     L = hf.hf_levelize(G)
-    base = torch.from_numpy(hfgen.scenario_delays(g, 0, 64, "ms")).to(dev)   # [m][64]
     at_src = torch.from_numpy(g.at_src).to(dev)
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
@@ -50,8 +51,10 @@ def main():
     print(f"{'S':>5} {'fwd ms':>8} {'bwd ms':>8} {'phase ms':>9} {'GB/s (kern)':>12} {'frac':>6} "
           f"{'edges/s (kern)':>15} {'GB resident':>12}")
     for S in [int(x) for x in a.S.split(",")]:
-        reps = (S + 63) // 64
-        D = base.repeat(1, reps)[:, :S].contiguous() if S != 64 else base
+        D = torch.empty((g.m, S), dtype=torch.float32, device=dev)
+        for b0 in range(0, S, 64):
+            b1 = min(S, b0 + 64)
+            D[:, b0:b1].copy_(torch.from_numpy(hfgen.scenario_delays(g, b0, b1, "ms")))
         T = torch.full((S,), g.t_req, dtype=torch.float32, device=dev)
         w = torch.empty(S, dtype=torch.float32, device=dev)
         f, b, ph = [], [], []
