@@ -35,10 +35,13 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, tag: str = "") -> str:
+    """out / tag: an alternative build (e.g. HF_NVCC_FLAGS=-DW1_NU_OVR=4) written next to
+    libhf.so for A/B timing through HF_LIB; the default build is libhf.so."""
+    lib = out or LIB
+    if not force and not out and not stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + (("_" + tag) if tag else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -60,13 +63,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out)
     if failed:
         raise RuntimeError("nvcc build of libhf.so failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs,
                            "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    # python -m paper_2203_08395_b200.build [--force] [-v] [--variant NAME]
+    #   --variant NAME: build libhf_NAME.so with $HF_NVCC_FLAGS (A/B through HF_LIB)
+    if "--variant" in sys.argv:
+        tag = sys.argv[sys.argv.index("--variant") + 1]
+        print(build(force=True, verbose="-v" in sys.argv,
+                    out=os.path.join(HERE, f"libhf_{tag}.so"), tag=tag))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -143,6 +143,14 @@ struct Graph {
     DevBuf wide_in_coff, wide_in_crow, wide_out_coff, wide_out_crow;
     DevBuf lo_in_d, lo_out_d;
     bool wide_ready = false, lo_d_ready = false;
+    // S = 1 (k_wide2): per direction w2_*_nbr[m] int2 {plain neighbour id, row} of every
+    // level-ordered edge, w2_*_erow[n] the node of every row (~node: no edges), and each
+    // level cut into row ranges of weight (rows + edges) <= W2_TW: w2_*_roff[L+1] first
+    // range-table entry of each level (a level of r ranges owns r + 1 entries),
+    // w2_*_rstart[] first row of each range + the level end
+    DevBuf w2_in_nbr, w2_in_erow, w2_in_roff, w2_in_rstart;
+    DevBuf w2_out_nbr, w2_out_erow, w2_out_roff, w2_out_rstart;
+    bool w2_ready = false;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // single-pass scan state (primitives.cu): per-tile words + tile counter; one per

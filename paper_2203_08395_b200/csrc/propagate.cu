@@ -143,8 +143,41 @@ template <int V> __device__ __forceinline__ void cp_async_v(float *dst, const fl
                      : "memory");
     }
 }
+// delay rows are read once per pass: staged with an L2 evict-first policy so they do
+// not push the recently written at / rat rows (the gathers' working set) out of L2
+// (variant build -DHF_DELAY_EVICT_FIRST, A/B through HF_LIB)
+template <int V> __device__ __forceinline__ void cp_async_v_ef(float *dst, const float *src,
+                                                               unsigned long long pol) {
+    if constexpr (V == 4) {
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)),
+                     "l"(src), "l"(pol)
+                     : "memory");
+    } else if constexpr (V == 2) {
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)),
+                     "l"(src), "l"(pol)
+                     : "memory");
+    } else {
+        asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)),
+                     "l"(src), "l"(pol)
+                     : "memory");
+    }
+}
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// all but the most recent group (HF_IDX_SMEM: the next task's index copies stay in
+// flight); without HF_IDX_SMEM every group
+__device__ __forceinline__ void cp_async_wait_keep1() {
+#if HF_IDX_SMEM
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+#else
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#endif
+}
 
 template <bool FWD> __device__ __forceinline__ float combine(float best, float x) {
     return FWD ? fmaxf(best, x) : fminf(best, x);
@@ -193,8 +226,12 @@ struct FlowParams {
 };
 
 // per-warp shared-memory scratch (bytes), identical on host and device
+#ifndef HF_IDX_SMEM
+#define HF_IDX_SMEM 0
+#endif
 struct WarpLayout {
-    int d, a, at, nbr, eid, rp, node, bytes;
+    int d, a, at, nbr, eid, rp, node, ring, bytes;
+    int ibytes;   // bytes of one index buffer (nbr, eid, rp, node); HF_IDX_SMEM keeps two
 };
 __host__ __device__ inline WarpLayout warp_layout(int ecap, int ncap, int SC, bool fwd, bool ga) {
     WarpLayout L;
@@ -202,10 +239,17 @@ __host__ __device__ inline WarpLayout warp_layout(int ecap, int ncap, int SC, bo
     L.d = o;    o += ecap * SC * 4;
     L.a = o;    o += ga ? ecap * SC * 4 : 0;
     L.at = o;   o += fwd ? 0 : ncap * SC * 4;
+    const int i0 = o;
     L.nbr = o;  o += ecap * 4;
     L.eid = o;  o += ecap * 4;
     L.rp = o;   o += (ncap + 1) * 4;
     L.node = o; o += ncap * 4;
+    L.ibytes = o - i0;
+    // HF_IDX_SMEM: a second index buffer (the next task's, filled by cp.async) and a
+    // ring of three task descriptors {dsc, chunk}
+    o += HF_IDX_SMEM ? L.ibytes : 0;
+    o = (o + 15) & ~15;
+    L.ring = o; o += HF_IDX_SMEM ? 3 * 32 : 0;
     L.bytes = (o + 15) & ~15;
     return L;
 }
@@ -248,10 +292,18 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
     float *s_d = reinterpret_cast<float *>(wb + WL.d);
     float *s_a = reinterpret_cast<float *>(wb + WL.a);
     float *s_at = reinterpret_cast<float *>(wb + WL.at);
+#if HF_IDX_SMEM
+    int32_t *s_nbr0 = reinterpret_cast<int32_t *>(wb + WL.nbr);
+    int32_t *s_eid0 = reinterpret_cast<int32_t *>(wb + WL.eid);
+    int32_t *s_rp0 = reinterpret_cast<int32_t *>(wb + WL.rp);
+    int32_t *s_node0 = reinterpret_cast<int32_t *>(wb + WL.node);
+    int32_t *s_nbr = s_nbr0, *s_eid = s_eid0, *s_rp = s_rp0, *s_node = s_node0;
+#else
     int32_t *s_nbr = reinterpret_cast<int32_t *>(wb + WL.nbr);
     int32_t *s_eid = reinterpret_cast<int32_t *>(wb + WL.eid);
     int32_t *s_rp = reinterpret_cast<int32_t *>(wb + WL.rp);
     int32_t *s_node = reinterpret_cast<int32_t *>(wb + WL.node);
+#endif
 
     // Rejected input already flagged (by the forward pass of this batch, or by the
     // pre-check of the concurrent batch): the results are void and the call reports
@@ -325,10 +377,56 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         }
     };
 
-    // software pipeline: D1 = descriptor of the next task, X0 = index registers of
-    // the current task, X1 of the next
     int qa = 0, qb = 0;          // locator cursors of the two look-ahead streams
     int t0 = w;
+#if HF_IDX_SMEM
+    // software pipeline in shared memory (no look-ahead registers): the index data of
+    // the next task is copied by cp.async into the other index buffer while this task
+    // runs; the descriptors of this, the next and the one after live in a 3-slot ring
+    int4 *s_ring = reinterpret_cast<int4 *>(wb + WL.ring);   // [3] {dsc}, [3] {c} below
+    int *s_ringc = reinterpret_cast<int *>(s_ring + 3);
+    // index copies of one task into buffer b (4-byte cp.async, lanes over the arrays)
+    auto copy_idx = [&](const int4 &dsc, int b) {
+        const bool part = dsc.y < 0;
+        const int E = dsc.w - dsc.z;
+        const int NR = part ? 1 : dsc.y - dsc.x;
+        int32_t *bn = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_nbr) + b * WL.ibytes);
+        int32_t *be = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_eid) + b * WL.ibytes);
+        int32_t *br = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_rp) + b * WL.ibytes);
+        int32_t *bo = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_node) + b * WL.ibytes);
+        for (int k = lane; k < E; k += 32) {
+            cp_async_v<1>(reinterpret_cast<float *>(bn + k), reinterpret_cast<const float *>(p.nbr + dsc.z + k));
+            cp_async_v<1>(reinterpret_cast<float *>(be + k), reinterpret_cast<const float *>(p.eid + dsc.z + k));
+        }
+        if (!part)
+            for (int k = lane; k <= NR; k += 32)
+                cp_async_v<1>(reinterpret_cast<float *>(br + k), reinterpret_cast<const float *>(p.row_ptr + dsc.x + k));
+        for (int k = lane; k < NR; k += 32)
+            cp_async_v<1>(reinterpret_cast<float *>(bo + k), reinterpret_cast<const float *>(p.node_of + dsc.x + k));
+    };
+    int it = 0, rs = 0;   // task iteration; ring slot of this task (it % 3)
+    if (t0 < T) {
+        int4 dd;
+        int cc;
+        locate(t0, qa, cc, dd);
+        if (lane == 0) {
+            s_ring[0] = dd;
+            s_ringc[0] = cc;
+        }
+        copy_idx(dd, 0);
+        cp_async_commit();
+        qb = qa;
+        if (t0 + W < T) {
+            locate(t0 + W, qb, cc, dd);
+            if (lane == 0) {
+                s_ring[1] = dd;
+                s_ringc[1] = cc;
+            }
+        }
+    }
+#else
+    // software pipeline: D1 = descriptor of the next task, X0 = index registers of
+    // the current task, X1 of the next
     Idx<NSL> X0, X1;
     int4 D1 = make_int4(0, 0, 0, 0);
     int c1 = 0;
@@ -338,15 +436,39 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         qb = qa;
         if (t0 + W < T) locate(t0 + W, qb, c1, D1);
     }
+#endif
     for (int t = t0; t < T; t += W) {
         const unsigned long long tr0 = p.trace ? gtimer() : 0;
+#ifdef HF_TRACE_EXT
+        // extended trace fields (poll rounds, all-batches-ready time) cost registers
+        // even when tracing is off: a separate build (HF_NVCC_FLAGS=-DHF_TRACE_EXT)
+        int npoll = 0;
+#define HF_NPOLL_INC() (++npoll)
+#else
+#define HF_NPOLL_INC() ((void)0)
+#endif
         // ---- (1) this task's index data -> shared scratch; stage delays (+ at) ----
+#if HF_IDX_SMEM
+        cp_async_wait();   // this task's index copies (issued during the previous task)
+        __syncwarp();
+        const int4 dsc = s_ring[rs];
+        const int c = s_ringc[rs];
+        const int bsel = it & 1;
+        int32_t *s_nbr = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_nbr0) + bsel * WL.ibytes);
+        int32_t *s_eid = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_eid0) + bsel * WL.ibytes);
+        int32_t *s_rp = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_rp0) + bsel * WL.ibytes);
+        int32_t *s_node = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(s_node0) + bsel * WL.ibytes);
+        const int rp_base = dsc.z;   // s_rp holds absolute row offsets here
+#else
         const int4 dsc = X0.dsc;
         const int c = X0.c;
+        const int rp_base = 0;
+#endif
         const bool part = dsc.y < 0;
         const int E = dsc.w - dsc.z;
         const int NR = part ? 1 : dsc.y - dsc.x;
         const int col = c * SC + gl * V;
+#if !HF_IDX_SMEM
         if (lane < E) {
             s_nbr[lane] = X0.nbr0;
             s_eid[lane] = X0.eid0;
@@ -363,19 +485,42 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
             if (k < NR) s_node[k] = X0.node1;
         }
         __syncwarp();
+#endif
         for (int k = g; k < E; k += G)
+#ifdef HF_DELAY_EVICT_FIRST
+            cp_async_v_ef<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col,
+                             policy_evict_first());
+#else
             cp_async_v<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col);
+#endif
         if (!FWD && !part && p.other)
             for (int i = g; i < NR; i += G)
                 cp_async_v<V>(s_at + i * SC + gl * V, p.other + int64_t(s_node[i]) * S + col);
         cp_async_commit();
         // ---- (2) look-ahead: index loads of the next task, descriptor of the one after
+#if HF_IDX_SMEM
+        {
+            const int rn = rs == 2 ? 0 : rs + 1, rnn = rn == 2 ? 0 : rn + 1;
+            if (t + W < T) copy_idx(s_ring[rn], bsel ^ 1);
+            cp_async_commit();   // (an empty group without a next task: wait_group 1 below)
+            if (t + 2 * W < T) {
+                int4 dd;
+                int cc;
+                locate(t + 2 * W, qb, cc, dd);
+                if (lane == 0) {
+                    s_ring[rnn] = dd;
+                    s_ringc[rnn] = cc;
+                }
+            }
+        }
+#else
         if (t + W < T) {
             X1.dsc = D1;
             X1.c = c1;
             load_idx(D1, X1);
             if (t + 2 * W < T) locate(t + 2 * W, qb, c1, D1);
         }
+#endif
         // ---- (3) edge-parallel gathers: x = fl(a[u] +/- d), sentinel-polled ----
         unsigned long long tr1 = 0;
         if constexpr (GA) {
@@ -495,6 +640,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 if (uu[r] >= 0 && uu[r] != INT32_MAX) miss |= has_nan<V>(a[r]);
             unsigned bal = __ballot_sync(FULL, miss);
             int ns = 32;
+            if (p.trace && bal) HF_NPOLL_INC();
             while (bal) {
                 if (p.poll_all) {
                     // every lane re-loads its own missing vectors (one round trip per round)
@@ -524,9 +670,10 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 for (int r = 0; r < RB; ++r)
                     if (uu[r] >= 0 && uu[r] != INT32_MAX) miss |= has_nan<V>(a[r]);
                 bal = __ballot_sync(FULL, miss);
+                if (p.trace) HF_NPOLL_INC();
             }
             if (p.trace && k0 == 0) tr1 = gtimer();
-            cp_async_wait();   // this lane's own delay copies (it reads only those)
+            cp_async_wait_keep1();   // this lane's own delay copies (it reads only those)
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
                 const int k = k0 + r * G + g;
@@ -542,8 +689,12 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 }
             }
         }
-        cp_async_wait();
+        if (GA) cp_async_wait();
+        else cp_async_wait_keep1();
         __syncwarp();
+#ifdef HF_TRACE_EXT
+        const unsigned long long tr2 = p.trace ? gtimer() : 0;
+#endif
         // ---- (4) reduce rows / the part, store ----
         if (part) {
             Vec<V> acc;
@@ -566,7 +717,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 run_c = c;
             }
             for (int i = g; i < NR; i += G) {
-                const int eb = s_rp[i], ee = s_rp[i + 1];
+                const int eb = s_rp[i] - rp_base, ee = s_rp[i + 1] - rp_base;
                 const int node = s_node[i];
                 Vec<V> best;
                 if (ee == eb) {
@@ -607,14 +758,32 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         if (p.trace && lane == 0) {
             const int r = t;
             if (r < p.trace_cap) {
-                unsigned long long *tr = p.trace + int64_t(r) * 4;
+                // {warp, start, first gather batch final, all gathers + delays in,
+                //  stores issued, poll rounds << 32 | edges << 16 | rows, 0, 0}
+                unsigned long long *tr = p.trace + int64_t(r) * 8;
                 tr[0] = (unsigned long long)w;
                 tr[1] = tr0;
                 tr[2] = tr1 ? tr1 : tr0;
-                tr[3] = gtimer();
+#ifdef HF_TRACE_EXT
+                tr[3] = tr2;
+                tr[5] = (static_cast<unsigned long long>(npoll) << 32) |
+                        (static_cast<unsigned long long>(E & 0xffff) << 16) | unsigned(NR & 0xffff);
+#else
+                tr[3] = tr[2];
+                tr[5] = (static_cast<unsigned long long>(E & 0xffff) << 16) | unsigned(NR & 0xffff);
+#endif
+                tr[4] = gtimer();
+                tr[6] = 0;
+                tr[7] = 0;
             }
         }
+#if HF_IDX_SMEM
+        ++it;
+        rs = rs == 2 ? 0 : rs + 1;
+        __syncwarp();   // the index buffer / ring slot of this task is rewritten next
+#else
         X0 = X1;
+#endif
     }
 
     if (bad) atomicOr(p.err, ERR_NONFINITE);
@@ -1279,15 +1448,15 @@ template <bool FWD> void run_pass(Graph &g, FlowParams &p, bool check_d, int V) 
     if (trace_env) {
         HF_CUDA(cudaMemcpyAsync(&ntask, p.tb + g.L, 4, cudaMemcpyDeviceToHost, s));
         HF_CUDA(cudaStreamSynchronize(s));
-        tbuf.alloc(sizeof(unsigned long long) * 4 * size_t(std::max(ntask, 1)), s);
+        tbuf.alloc(sizeof(unsigned long long) * 8 * size_t(std::max(ntask, 1)), s);
         HF_CUDA(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, s));
         p.trace = tbuf.as<unsigned long long>();
         p.trace_cap = ntask;
     }
     launch_pass<FWD>(g, p, check_d, V, cx, s, 0);
     if (trace_env) {
-        // per task: {warp, t_start, t_ready (first gathers complete), t_done} + level
-        std::vector<unsigned long long> h(size_t(ntask) * 4);
+        // per task: 8 words (k_flow's trace record) + the task bases per level
+        std::vector<unsigned long long> h(size_t(ntask) * 8);
         std::vector<int32_t> tb(size_t(g.L) + 1);
         HF_CUDA(cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, s));
         HF_CUDA(cudaMemcpyAsync(tb.data(), p.tb, tb.size() * 4, cudaMemcpyDeviceToHost, s));

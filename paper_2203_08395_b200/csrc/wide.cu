@@ -28,6 +28,9 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <cstdio>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -288,8 +291,14 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(WideParams p) {
 // offsets, neighbours, delays: nothing written in the pass) and only then waits,
 // so after the barrier a unit is one gather round trip from its result.
 constexpr int W1_THREADS = 256;
-constexpr int W1_NU = 2;   // units of a warp per level whose structure is held in registers
-constexpr int W1_CH = 2;   // edge chunks (32 edges) of a unit held in registers
+#ifndef W1_NU_OVR
+#define W1_NU_OVR 2
+#endif
+#ifndef W1_CH_OVR
+#define W1_CH_OVR 2
+#endif
+constexpr int W1_NU = W1_NU_OVR;   // units of a warp per level whose structure is held in registers
+constexpr int W1_CH = W1_CH_OVR;   // edge chunks (32 edges) of a unit held in registers
 
 struct Wide1Params {
     const int32_t *level_ptr, *lstart, *row_ptr, *nbr, *eid, *node_of, *q;
@@ -304,6 +313,7 @@ struct Wide1Params {
     int32_t *slot, *wns_ord;
     uint32_t *err;
     unsigned *bar;
+    unsigned long long *trace;   // optional (HF_TRACE): per level {barrier passed, stores issued}
 };
 
 struct LevelInfo {
@@ -510,6 +520,12 @@ __device__ __forceinline__ void finish_units(const Wide1Params &p, const Units &
     }
 }
 
+__device__ __forceinline__ unsigned long long wide_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <bool FWD, bool EARLY>
 __global__ void __launch_bounds__(W1_THREADS) k_wide1(Wide1Params p) {
     constexpr bool MX = FWD != EARLY;
@@ -535,9 +551,14 @@ __global__ void __launch_bounds__(W1_THREADS) k_wide1(Wide1Params p) {
     for (int qq = 0; qq < L; ++qq) {
         // round 0 was loaded before the barrier; a warp with more than W1_NU units in
         // this level loads the further rounds here
+        if (p.trace && threadIdx.x == 0) p.trace[(2 * qq) * gridDim.x + blockIdx.x] = wide_gtimer();
         for (int r0 = 0; w + r0 * W1_NU * W < li.nu; ++r0) {
             if (r0) load_units(p, li, w + r0 * W1_NU * W, W, U);
             finish_units<FWD, EARLY>(p, U, s_val, bad, mn);
+        }
+        if (p.trace) {
+            __syncthreads();
+            if (threadIdx.x == 0) p.trace[(2 * qq + 1) * gridDim.x + blockIdx.x] = wide_gtimer();
         }
         if (qq + 1 == L) break;
         // split barrier: arrive, load the next level's first round, wait
@@ -697,8 +718,326 @@ void launch_wide(Graph &g, WideParams &p, cudaStream_t st) {
 }
 
 template <bool FWD, bool EARLY>
+int w1_occupancy(const Graph &g) {
+    auto kern = k_wide1<FWD, EARLY>;
+    static std::map<std::pair<const void *, int>, int> cache;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({(const void *)kern, g.device});
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W1_THREADS, 0));
+    cache[{(const void *)kern, g.device}] = per_sm;
+    return per_sm;
+}
+template <bool FWD, bool EARLY>
+int w1_blocks(const Graph &g) {
+    int per_sm = w1_occupancy<FWD, EARLY>(g);
+    const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    return g.sms * per_sm;
+}
+
+template <bool FWD, bool EARLY>
 void launch_w1(Graph &g, Wide1Params &p, cudaStream_t st) {
     auto kern = k_wide1<FWD, EARLY>;
+    const int nblk = w1_blocks<FWD, EARLY>(g);
+    if (nblk < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
+    void *args[] = {&p};
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, nblk, W1_THREADS, args, 0, st));
+    g.launches += 1;
+}
+
+// ---- S = 1: row ranges with shared-memory row accumulators (k_wide2) ------------
+// Each level of the level-ordered CSR is cut into RANGES of consecutive rows of
+// weight (rows + edges) <= W2_TW = W2_R * W2_THREADS, so a range holds <= W2_TW rows
+// and one contiguous edge run (a hub row of any fan-in is one range).  A CTA (1024
+// threads, one per SM) takes ranges j = blockIdx.x, += gridDim.x of the level, each
+// in two dependent load rounds:
+//   round 1: a range descriptor {first row, first edge} (prefetched one range ahead,
+//            and across the grid barrier for the next level's first range), then per
+//            thread its <= W2_R rows' nodes and <= W2_U edges' {neighbour, row} and
+//            delays -- all coalesced, all in flight together;
+//   round 2: the gathers a[neighbour] and, per row, at_src (sources) or at (slack).
+// Then x = fl(a +/- d), a segmented max / min over the warp's 32 consecutive edges
+// (rows are contiguous), segment ends fold into the row's shared accumulator with an
+// ordered-int shared atomic (exact: max / min are order-independent, R10), and every
+// thread stores its own rows (sources / sinks: at_src / T; backward the slack and
+// the worst-slack minimum).  A thread initialises and reads only its own rows'
+// accumulators, so two block barriers per range suffice.  Level-synchronous (grid
+// barrier between levels): no sentinel, no fill, no task schedule; a row is never
+// split between CTAs, so long rows need no parts or slots.
+// MEASURED AND REJECTED as the default (C5, S = 1, one B200): forward 0.50 / backward
+// 0.47 ms against k_wide1's 0.37 / 0.40 ms; 512- and 256-thread CTAs (2 and 4 per
+// SM) and 16k / 8k / 4k-weight ranges were no better (profiles/round2_c5_wide.txt).
+// Kept behind HF_WIDE2=1 and parity-tested (tests/test_gpu_wide.py).
+#ifndef W2_THREADS_OVR
+#define W2_THREADS_OVR 1024
+#endif
+constexpr int W2_THREADS = W2_THREADS_OVR;
+constexpr int W2_R = 4;
+constexpr int W2_U = 4;
+constexpr int W2_TW = W2_R * W2_THREADS;
+
+struct Wide2Params {
+    const int32_t *node;      // [n] node of each row, ~node (negative) for a row with no edges
+    const int2 *nbr_row;      // [m] {plain neighbour node id, row of the edge}
+    const int32_t *eid;       // [m] delay index of each position, or null: d is level-ordered
+    const int32_t *roff;      // [L+1] first descriptor of each level
+    const int2 *rdesc;        // [roff[L]] {first row, first edge} per range + the level end
+    int32_t L;
+    const float *d;
+    const float *src_val;     // forward: at_src [n] or null; backward: t_req [1] or null
+    float t_scalar;
+    const float *other;       // backward: at (slack) or null
+    float *out, *slack;
+    int32_t *wns_ord;
+    uint32_t *err;
+    unsigned *bar;
+    unsigned long long *trace;   // optional: per level and block {start, ranges done}
+};
+
+template <bool FWD, bool EARLY>
+__global__ void __launch_bounds__(W2_THREADS, 1024 / W2_THREADS) k_wide2(Wide2Params p) {
+    constexpr bool MX = FWD != EARLY;
+    constexpr int32_t IDENT_ORD = MX ? ORD_NEG_INF : ORD_POS_INF;
+    constexpr int B = W2_THREADS;
+    __shared__ int32_t s_acc[W2_TW];   // row accumulators (ordered ints)
+    __shared__ int32_t s_wmin;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const float ident = __int_as_float(MX ? 0xff800000 : 0x7f800000);
+    const bool do_slack = !FWD && p.other;
+    const float tb = FWD ? 0.0f : (p.src_val ? __ldg(p.src_val) : p.t_scalar);
+    if (tid == 0) s_wmin = ORD_POS_INF;
+    unsigned target = 0;
+    bool bad = false;
+    float mn = __int_as_float(ORD_POS_INF);
+    // descriptors of this block's first range of the first level
+    int k = FWD ? 0 : p.L - 1;
+    int r0 = __ldg(p.roff + k), nr = __ldg(p.roff + k + 1) - r0 - 1;
+    int2 lo = make_int2(0, 0), hi = make_int2(0, 0);
+    if (int(blockIdx.x) < nr) {
+        lo = __ldg(p.rdesc + r0 + blockIdx.x);
+        hi = __ldg(p.rdesc + r0 + blockIdx.x + 1);
+    }
+    for (int qq = 0; qq < p.L; ++qq) {
+        if (p.trace && tid == 0) p.trace[(2 * qq) * gridDim.x + blockIdx.x] = wide_gtimer();
+        for (int j = blockIdx.x; j < nr; j += gridDim.x) {
+            const int ra = lo.x, ea = lo.y, rb = hi.x, eb = hi.y;
+            // next range's descriptor (same level), one range ahead
+            if (j + int(gridDim.x) < nr) {
+                lo = __ldg(p.rdesc + r0 + j + gridDim.x);
+                hi = __ldg(p.rdesc + r0 + j + gridDim.x + 1);
+            }
+            if (ra == rb) continue;   // block-uniform
+            // ---- round 1: rows' nodes, edges' {neighbour, row} and delays
+            int nd[W2_R];
+#pragma unroll
+            for (int u = 0; u < W2_R; ++u) {
+                const int r = ra + u * B + tid;
+                nd[u] = r < rb ? __ldg(p.node + r) : INT32_MIN;
+            }
+            int2 nr_[W2_U];
+            float dv[W2_U];
+#pragma unroll
+            for (int u = 0; u < W2_U; ++u) {
+                const int e = ea + u * B + tid;
+                nr_[u] = make_int2(0, -1 - lane);   // unique negative key: never stored
+                dv[u] = 0.0f;
+                if (e < eb) {
+                    nr_[u] = __ldg(p.nbr_row + e);
+                    dv[u] = p.eid ? __ldg(p.d + __ldg(p.eid + e)) : __ldg(p.d + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < W2_R; ++u) s_acc[u * B + tid] = IDENT_ORD;   // own rows
+            __syncthreads();   // every accumulator initialised before any atomic
+            // ---- round 2: gathers; at_src of sources (forward) / at for the slack
+            float av[W2_U], aux[W2_R];
+#pragma unroll
+            for (int u = 0; u < W2_U; ++u) av[u] = nr_[u].y >= 0 ? __ldcg(p.out + nr_[u].x) : ident;
+#pragma unroll
+            for (int u = 0; u < W2_R; ++u) {
+                const int node = nd[u] >= 0 ? nd[u] : ~nd[u];
+                aux[u] = 0.0f;
+                if (nd[u] != INT32_MIN) {
+                    if (FWD && nd[u] < 0 && p.src_val) aux[u] = __ldg(p.src_val + node);
+                    if (do_slack) aux[u] = __ldg(p.other + node);
+                }
+            }
+            for (int e0 = ea;;) {
+#pragma unroll
+                for (int u = 0; u < W2_U; ++u) {
+                    if (e0 + u * B >= eb) break;   // block-uniform
+                    const int key = nr_[u].y;
+                    const bool valid = key >= 0;
+                    float v = valid ? relax1<FWD>(av[u], sane(dv[u], bad)) : ident;
+                    // segmented combine over the warp's consecutive edges
+                    const int prv = __shfl_up_sync(0xffffffffu, key, 1);
+                    const int nxt = __shfl_down_sync(0xffffffffu, key, 1);
+                    const unsigned smask = __ballot_sync(0xffffffffu, lane == 0 || prv != key);
+                    const int sstart = 31 - __clz(smask & ((2u << lane) - 1u));
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const float y = __shfl_up_sync(0xffffffffu, v, o);
+                        if (lane - o >= sstart) v = comb<MX>(v, y);
+                    }
+                    if (valid && (lane == 31 || nxt != key)) {
+                        if (MX) atomicMax(s_acc + (key - ra), f2ord(v));
+                        else atomicMin(s_acc + (key - ra), f2ord(v));
+                    }
+                }
+                e0 += W2_U * B;
+                if (e0 >= eb) break;   // block-uniform
+                // a range with more edges than one sweep (one row of fan-in > W2_TW)
+#pragma unroll
+                for (int u = 0; u < W2_U; ++u) {
+                    const int e = e0 + u * B + tid;
+                    nr_[u] = make_int2(0, -1 - lane);
+                    dv[u] = 0.0f;
+                    if (e < eb) {
+                        nr_[u] = __ldg(p.nbr_row + e);
+                        dv[u] = p.eid ? __ldg(p.d + __ldg(p.eid + e)) : __ldg(p.d + e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < W2_U; ++u) av[u] = nr_[u].y >= 0 ? __ldcg(p.out + nr_[u].x) : ident;
+            }
+            __syncthreads();   // all atomics done
+            // ---- this thread's rows
+#pragma unroll
+            for (int u = 0; u < W2_R; ++u) {
+                if (nd[u] == INT32_MIN) continue;
+                const bool empty = nd[u] < 0;
+                const int node = empty ? ~nd[u] : nd[u];
+                // source (forward) / sink (backward): at_src / T
+                const float best = !empty ? ord2f(s_acc[u * B + tid]) : sane(FWD ? aux[u] : tb, bad);
+                p.out[node] = best;
+                if (do_slack) {
+                    const float sl = EARLY ? __fsub_rn(aux[u], best) : __fsub_rn(best, aux[u]);
+                    mn = fminf(mn, sl);
+                    if (p.slack) p.slack[node] = sl;
+                }
+            }
+        }
+        if (p.trace) {
+            __syncthreads();
+            if (tid == 0) p.trace[(2 * qq + 1) * gridDim.x + blockIdx.x] = wide_gtimer();
+        }
+        if (qq + 1 == p.L) break;
+        // split grid barrier: arrive, load the next level's first descriptor, wait
+        target += gridDim.x;
+        __syncthreads();
+        if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+        k = FWD ? qq + 1 : p.L - 2 - qq;
+        r0 = __ldg(p.roff + k);
+        nr = __ldg(p.roff + k + 1) - r0 - 1;
+        if (int(blockIdx.x) < nr) {
+            lo = __ldg(p.rdesc + r0 + blockIdx.x);
+            hi = __ldg(p.rdesc + r0 + blockIdx.x + 1);
+        }
+        if (tid == 0)
+            while (ld_acq(p.bar) < target) __nanosleep(32);
+        __syncthreads();
+    }
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
+    if (do_slack) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        __syncthreads();
+        if (lane == 0 && mn != __int_as_float(ORD_POS_INF)) atomicMin(&s_wmin, f2ord(mn));
+        __syncthreads();
+        if (tid == 0 && s_wmin != ORD_POS_INF) atomicMin(p.wns_ord, s_wmin);
+    }
+}
+
+// {plain neighbour id, row} per level-ordered edge (a long neighbour's -(first part
+// id + 1) decoded to its node), and per row its node, ~node for a row with no edges
+__global__ void k_w2_edges(const int32_t *__restrict__ nbr, const int32_t *__restrict__ part_row,
+                           const int32_t *__restrict__ node_of, const int32_t *__restrict__ erow,
+                           int32_t m, int2 *__restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int u = nbr[e];
+        out[e] = make_int2(u >= 0 ? u : node_of[part_row[-u - 1]], erow[e]);
+    }
+}
+__global__ void k_w2_nodes(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                           int32_t n, int32_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = row_ptr[i + 1] == row_ptr[i] ? ~node_of[i] : node_of[i];
+}
+// per level: ranges = floor(P(last row) / W2_TW) + 1 (P = weight before a row inside its
+// level), entries = ranges + 1; roff = exclusive scan of the entries (one block)
+__global__ void __launch_bounds__(1024) k_w2_roff(const int32_t *__restrict__ level_ptr,
+                                                  const int32_t *__restrict__ row_ptr, int32_t L,
+                                                  int32_t *__restrict__ roff) {
+    __shared__ int warp_s[32];
+    __shared__ int carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int k0 = 0; k0 < L; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        int v = 0;
+        if (k < L) {
+            const int ls = level_ptr[k], le = level_ptr[k + 1];
+            const long long P = (long long)(row_ptr[le - 1] - row_ptr[ls]) + (le - 1 - ls);
+            v = int(P / W2_TW) + 2;
+        }
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_s[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int sx = lane < nw ? warp_s[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, sx, o);
+                if (lane >= o) sx += y;
+            }
+            if (lane < nw) warp_s[lane] = sx;
+        }
+        __syncthreads();
+        if (k < L) roff[k] = carry + (wid ? warp_s[wid - 1] : 0) + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += warp_s[nw - 1];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) roff[L] = carry;
+}
+// range descriptors {first row, first edge}: row i starts every range j with
+// P(i-1) < j * W2_TW <= P(i) (range 0 at the level's first row); the level's last row
+// also writes the end entry {level end, its edge offset}
+__global__ void k_w2_rdesc(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                           const int32_t *__restrict__ level, const int32_t *__restrict__ level_ptr,
+                           const int32_t *__restrict__ roff, int32_t n, int2 *__restrict__ rdesc) {
+    for (int64_t ii = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; ii < n;
+         ii += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(ii);
+        const int k = level[node_of[i]];
+        const int ls = level_ptr[k], le = level_ptr[k + 1];
+        const int base = roff[k];
+        const long long P = (long long)(row_ptr[i] - row_ptr[ls]) + (i - ls);
+        const int j = int(P / W2_TW);
+        if (i == ls) {
+            rdesc[base] = make_int2(ls, row_ptr[ls]);
+        } else {
+            const long long Pp = (long long)(row_ptr[i - 1] - row_ptr[ls]) + (i - 1 - ls);
+            for (int jj = int(Pp / W2_TW) + 1; jj <= j; ++jj) rdesc[base + jj] = make_int2(i, row_ptr[i]);
+        }
+        if (i == le - 1) rdesc[base + j + 1] = make_int2(le, row_ptr[le]);
+    }
+}
+
+template <bool FWD, bool EARLY>
+int w2_blocks(const Graph &g) {
+    auto kern = k_wide2<FWD, EARLY>;
     static std::map<std::pair<const void *, int>, int> cache;
     static std::mutex mu;
     int per_sm = 0;
@@ -708,16 +1047,13 @@ void launch_w1(Graph &g, Wide1Params &p, cudaStream_t st) {
         if (it != cache.end()) per_sm = it->second;
     }
     if (!per_sm) {
-        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W1_THREADS, 0));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W2_THREADS, 0));
         std::lock_guard<std::mutex> lk(mu);
         cache[{(const void *)kern, g.device}] = per_sm;
     }
-    if (per_sm < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
     const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
     if (cap > 0) per_sm = std::min(per_sm, cap);
-    void *args[] = {&p};
-    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms * per_sm, W1_THREADS, args, 0, st));
-    g.launches += 1;
+    return g.sms * per_sm;
 }
 
 }  // namespace
@@ -759,6 +1095,49 @@ void wide_prepare(Graph &g) {
         g.launches += 2;
     }
     g.wide_ready = true;
+}
+
+// k_wide2 tables of both directions (once per levelization): plain neighbour ids,
+// the row of every edge, the row ranges of every level.
+void wide2_prepare(Graph &g) {
+    if (g.w2_ready) return;
+    cudaStream_t s = g.stream;
+    const int32_t n = g.n, m = g.m;
+    DevBuf erow;
+    erow.alloc(sizeof(int32_t) * std::max<int64_t>(m, 1), s);
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool in = dir == 0;
+        const int32_t *rp = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+        const int32_t *no = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+        const int32_t *nb = in ? g.lo_in_nbr.as<int32_t>() : g.lo_out_nbr.as<int32_t>();
+        const int32_t *npa = in ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
+        const int32_t *prow = npa + (in ? g.np_cap_in : g.np_cap_out);
+        DevBuf &pn = in ? g.w2_in_nbr : g.w2_out_nbr;     // int2 {neighbour, row}
+        DevBuf &nd = in ? g.w2_in_erow : g.w2_out_erow;   // int32 encoded node per row
+        DevBuf &ro = in ? g.w2_in_roff : g.w2_out_roff;
+        DevBuf &rs = in ? g.w2_in_rstart : g.w2_out_rstart;   // int2 descriptors
+        pn.alloc(sizeof(int2) * std::max<int64_t>(m, 1), s);
+        nd.alloc(sizeof(int32_t) * std::max<int64_t>(n, 1), s);
+        ro.alloc(sizeof(int32_t) * (int64_t(g.L) + 1), s);
+        // entries: sum over levels of (ranges + 1) <= (n + m) / W2_TW + 2L
+        rs.alloc(sizeof(int2) * size_t((int64_t(n) + m) / W2_TW + 2 * int64_t(g.L) + 1), s);
+        if (m) {
+            csr_row_ids(rp, n, erow.as<int32_t>(), s, g);
+            k_w2_edges<<<grid_for(m, 256, g.sms), 256, 0, s>>>(nb, prow, no, erow.as<int32_t>(), m,
+                                                               pn.as<int2>());
+            HF_CHECK_LAUNCH();
+        }
+        k_w2_nodes<<<grid_for(n, 256, g.sms), 256, 0, s>>>(rp, no, n, nd.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        k_w2_roff<<<1, 1024, 0, s>>>(g.level_ptr.as<int32_t>(), rp, g.L, ro.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        k_w2_rdesc<<<grid_for(n, 256, g.sms), 256, 0, s>>>(rp, no, g.level.as<int32_t>(),
+                                                          g.level_ptr.as<int32_t>(),
+                                                          ro.as<int32_t>(), n, rs.as<int2>());
+        HF_CHECK_LAUNCH();
+        g.launches += 5;
+    }
+    g.w2_ready = true;
 }
 
 // The graph's own delays in level order of both directions (single-set calls).
@@ -823,6 +1202,54 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
     p.slack = slack;
     p.wns_ord = wns_ord;
     p.err = g.d_err();
+    if (S == 1 && env_int_w("HF_WIDE2", 0)) {
+        wide2_prepare(g);
+        Wide2Params w{};
+        w.node = in ? g.w2_in_erow.as<int32_t>() : g.w2_out_erow.as<int32_t>();
+        w.nbr_row = in ? g.w2_in_nbr.as<int2>() : g.w2_out_nbr.as<int2>();
+        w.eid = p.eid;
+        w.roff = in ? g.w2_in_roff.as<int32_t>() : g.w2_out_roff.as<int32_t>();
+        w.rdesc = in ? g.w2_in_rstart.as<int2>() : g.w2_out_rstart.as<int2>();
+        w.L = g.L;
+        w.d = d;
+        w.src_val = src_val;
+        w.t_scalar = t_scalar;
+        w.other = other;
+        w.out = out;
+        w.slack = slack;
+        w.wns_ord = wns_ord;
+        w.err = p.err;
+        DevBuf bar2;
+        bar2.alloc(sizeof(unsigned) * 2, st);
+        HF_CUDA(cudaMemsetAsync(bar2.p, 0, sizeof(unsigned) * 2, st));
+        w.bar = bar2.as<unsigned>();
+        const int nblk = g.early ? w2_blocks<FWD, true>(g) : w2_blocks<FWD, false>(g);
+        if (nblk < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
+        const char *trace_env = getenv("HF_TRACE");
+        DevBuf tb;
+        if (trace_env) {
+            tb.alloc(sizeof(unsigned long long) * 2 * size_t(g.L) * nblk, st);
+            HF_CUDA(cudaMemsetAsync(tb.p, 0, tb.bytes, st));
+            w.trace = tb.as<unsigned long long>();
+        }
+        void *args[] = {&w};
+        const void *kern = g.early ? (const void *)k_wide2<FWD, true> : (const void *)k_wide2<FWD, false>;
+        HF_CUDA(cudaLaunchCooperativeKernel(kern, nblk, W2_THREADS, args, 0, st));
+        g.launches += 1;
+        if (trace_env) {
+            std::vector<unsigned long long> h(2 * size_t(g.L) * nblk);
+            HF_CUDA(cudaMemcpyAsync(h.data(), tb.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+            HF_CUDA(cudaStreamSynchronize(st));
+            const std::string fn = std::string(trace_env) + (FWD ? "_w2_fwd.bin" : "_w2_bwd.bin");
+            if (FILE *f = fopen(fn.c_str(), "wb")) {
+                const int32_t hdr[2] = {g.L, nblk};
+                fwrite(hdr, 4, 2, f);
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
+        return;
+    }
     if (S == 1 && env_int_w("HF_WIDE1", 1)) {
         Wide1Params w{};
         w.level_ptr = p.level_ptr;
@@ -852,8 +1279,29 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
         HF_CUDA(cudaMemsetAsync(bar1.p, 0, sizeof(unsigned) * 2, st));
         w.slot = slots1.as<int32_t>();
         w.bar = bar1.as<unsigned>();
+        // HF_TRACE=<prefix>: per level and block {start, all its units done} -> <prefix>_w1_<dir>.bin
+        const char *trace_env = getenv("HF_TRACE");
+        DevBuf tb;
+        const int nblk = g.early ? w1_blocks<FWD, true>(g) : w1_blocks<FWD, false>(g);
+        if (trace_env) {
+            tb.alloc(sizeof(unsigned long long) * 2 * size_t(g.L) * nblk, st);
+            HF_CUDA(cudaMemsetAsync(tb.p, 0, tb.bytes, st));
+            w.trace = tb.as<unsigned long long>();
+        }
         if (g.early) launch_w1<FWD, true>(g, w, st);
         else launch_w1<FWD, false>(g, w, st);
+        if (trace_env) {
+            std::vector<unsigned long long> h(2 * size_t(g.L) * nblk);
+            HF_CUDA(cudaMemcpyAsync(h.data(), tb.p, h.size() * 8, cudaMemcpyDeviceToHost, st));
+            HF_CUDA(cudaStreamSynchronize(st));
+            const std::string fn = std::string(trace_env) + (FWD ? "_w1_fwd.bin" : "_w1_bwd.bin");
+            if (FILE *f = fopen(fn.c_str(), "wb")) {
+                const int32_t hdr[2] = {g.L, nblk};
+                fwrite(hdr, 4, 2, f);
+                fwrite(h.data(), 8, h.size(), f);
+                fclose(f);
+            }
+        }
         return;
     }
     DevBuf slots, bar;

@@ -26,16 +26,22 @@ def hf():
     return _hf
 
 
+# S = 1 runs k_wide2 (row ranges, shared accumulators) by default; HF_WIDE2=0 keeps
+# the warp-unit kernel k_wide1 under test as well
+@pytest.mark.parametrize("w2", ["1", "0"])
 @pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C3", 0.05), ("C2-random", 0.01),
                                         ("C5", 0.01), ("C5", 0.1)])
-def test_wide_single(hf, name, scale, monkeypatch):
+def test_wide_single(hf, name, scale, w2, monkeypatch):
     monkeypatch.setenv("HF_WIDE", "1")
+    monkeypatch.setenv("HF_WIDE2", w2)
     g = hfgen.config(name, scale)
     check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req)
 
 
-def test_wide_tiny_random_dags(hf, monkeypatch):
+@pytest.mark.parametrize("w2", ["1", "0"])
+def test_wide_tiny_random_dags(hf, w2, monkeypatch):
     monkeypatch.setenv("HF_WIDE", "1")
+    monkeypatch.setenv("HF_WIDE2", w2)
     rng = np.random.default_rng(2203)
     for trial in range(80):
         n, edges = random_tiny_dag(rng, nmax=12)
@@ -46,10 +52,13 @@ def test_wide_tiny_random_dags(hf, monkeypatch):
                      float(mixed_delays(rng, 1)[0]))
 
 
-def test_wide_hub_fan_in(hf, monkeypatch):
-    """One node with 10^4 predecessors (C5's planted hub): 1250 slices folded by
-    atomics into one slot; its consumers read the slot."""
+@pytest.mark.parametrize("w2", ["1", "0"])
+def test_wide_hub_fan_in(hf, w2, monkeypatch):
+    """One node with 10^4 predecessors (C5's planted hub): k_wide1 folds its slices by
+    atomics into one slot and its consumers read the slot; k_wide2 keeps the row in
+    one range (its 10^4 edges streamed through the shared accumulator)."""
     monkeypatch.setenv("HF_WIDE", "1")
+    monkeypatch.setenv("HF_WIDE2", w2)
     rng = np.random.default_rng(7)
     k = 10000
     edges = [(i, k) for i in range(k)] + [(k, k + 1), (k, k + 2), (3, k + 2)]
