@@ -261,6 +261,177 @@ __global__ void k_lev_kahn(const int32_t *__restrict__ cptr, const int32_t *__re
     }
 }
 
+// ---- barrier-free Kahn over the junctions (HF_KAHN_ASYNC) -----------------------
+// One list of contracted-edge entries {edge, level of its source} (64-bit words,
+// pre-filled with the all-ones sentinel), appended in readiness order: position i
+// is claimed by an atomic counter A and written once.  Warp w owns positions
+// w*32 + lane + k*(warps*32): it polls its 32 positions, processes every entry that
+// has arrived (cdst / cw / the target's out-edge range, atomicMax of the level,
+// acq_rel decrement of the join counter); the lane that readies a junction reads its
+// now final level and appends the junction's out-edges (warp-aggregated claim).
+// There are no rounds and no grid barrier: the chain of dependent hops is the
+// junction depth, every hop ~4 L2 round trips.  Termination: P counts processed
+// entries (flushed by a warp once it has idled >= 4 us, so P stays off the hot path),
+// appends precede their entry's P increment, so P == A (read in that order) means no
+// entry is in flight and none can appear.  Cycles leave counters > 0 and simply end
+// the same way.  A watchdog (globaltimer, HF_KAHN_WATCHDOG_MS, default 2000) aborts
+// instead of hanging; the host then reports HF_ERR_CUDA.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int atom_add_acq_rel(int *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int ld_acquire_s32(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ctr: [0] A (appended), [1] P (processed), [2] abort flag
+__global__ void __launch_bounds__(256) k_lev_kahn_async(
+    const int32_t *__restrict__ cptr, const int32_t *__restrict__ cdst,
+    const int32_t *__restrict__ cw, int32_t *__restrict__ cnt, int32_t *__restrict__ lev,
+    unsigned long long *__restrict__ list, int64_t cap, int32_t *ctr,
+    unsigned long long watchdog_ns) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t wid = int64_t(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    int myp = 0;                    // processed entries not yet published to P
+    unsigned long long idle_since = 0;
+    const unsigned long long t_start = lev_gtimer();
+    for (int64_t base = wid * 32; base < cap; base += nwarps * 32) {
+        const int64_t i = base + lane;
+        bool pending = i < cap;
+        int ns = 32;
+        int a_seen = 0;   // a recent value of A: positions below it are claimed
+        for (;;) {
+            // poll only claimed positions (a claimed entry is written right after its
+            // claim); a batch wholly past A waits on the counter alone
+            const unsigned long long ev =
+                (pending && i < a_seen) ? ld_relaxed_u64(list + i) : ~0ull;
+            const bool have = ev != ~0ull;
+            const unsigned hm = __ballot_sync(0xffffffffu, have);
+            if (hm) {
+                int nch = 0, ks = 0, lk = 0;
+                if (have) {
+                    const int e = int(unsigned(ev));
+                    const int lj = int(unsigned(ev >> 32));
+                    const int k = __ldg(cdst + e);
+                    const int w = __ldg(cw + e);
+                    ks = __ldg(cptr + k);
+                    const int ke = __ldg(cptr + k + 1);
+                    atomicMax(lev + k, lj + w);
+                    // release: this level contribution before the decrement; acquire:
+                    // the last decrementer sees every contribution
+                    if (atom_add_acq_rel(cnt + k, -1) == 1) {
+                        nch = ke - ks;
+                        lk = ld_relaxed_s32(lev + k);   // final (ordered after the acquire)
+                    }
+                    pending = false;
+                }
+                // warp-aggregated claim of the readied junctions' out-edges
+                int incl = nch;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total) {
+                    int b0 = 0;
+                    if (lane == 31) b0 = atomicAdd(ctr + 0, total);
+                    b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - nch;
+                    const unsigned long long hi = (unsigned long long)unsigned(lk) << 32;
+                    for (int t = 0; t < nch; ++t)
+                        st_relaxed_u64(list + b0 + t, hi | unsigned(ks + t));
+                }
+                myp += __popc(hm);
+                idle_since = 0;
+                ns = 32;
+            }
+            if (!__any_sync(0xffffffffu, pending)) break;
+            // waiting: publish the processed count after a while, test for the end
+            const unsigned long long now = lev_gtimer();
+            if (idle_since == 0) idle_since = now;
+            if (lane == 0 && myp && now - idle_since > 4000) {
+                __threadfence();   // this warp's appends before its processed count
+                atomicAdd(ctr + 1, myp);
+                myp = 0;
+            }
+            myp = __shfl_sync(0xffffffffu, myp, 0);
+            int done = 0, a = 0;
+            if (lane == 0) {
+                // P before A: P == A then means no entry was in flight when P was read,
+                // so none can ever be appended (every pending position is >= A)
+                const int pr = ld_acquire_s32(ctr + 1);
+                a = ld_acquire_s32(ctr + 0);
+                done = pr == a ? 1 : 0;
+                if (ld_relaxed_s32(ctr + 2)) done = 2;
+                if (now - t_start > watchdog_ns) {
+                    atomicExch(ctr + 2, 1);
+                    done = 2;
+                }
+            }
+            done = __shfl_sync(0xffffffffu, done, 0);
+            a_seen = __shfl_sync(0xffffffffu, a, 0);
+            if (done == 2) return;
+            if (done == 1) {
+                // only lanes past the end remain: positions >= a never arrive
+                if (lane == 0 && myp) atomicAdd(ctr + 1, myp);
+                return;
+            }
+            // claimed positions pending: poll soon; otherwise the batch waits for appends
+            const bool claimed = __any_sync(0xffffffffu, pending && i < a_seen);
+            __nanosleep(claimed ? 32 : ns);
+            ns = min(ns * 2, 1024);
+        }
+    }
+    if (lane == 0 && myp) atomicAdd(ctr + 1, myp);
+}
+
+// seeds of the barrier-free Kahn: the sources' contracted out-edges {edge, level 0}
+__global__ void k_lev_seed_async(const int32_t *__restrict__ src_list, const int32_t *__restrict__ cptr,
+                                 const int32_t *sc, unsigned long long *__restrict__ list,
+                                 int32_t *ctr) {
+    const int size = sc[SC_FR + 1];
+    const int lane = threadIdx.x & 31;
+    const int64_t lim = (int64_t(size) + 31) / 32 * 32;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < lim;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int nch = 0, st = 0;
+        if (i < size) {
+            const int v = src_list[i];
+            st = cptr[v];
+            nch = cptr[v + 1] - st;
+        }
+        int incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total == 0) continue;
+        int b0 = 0;
+        if (lane == 31) b0 = atomicAdd(ctr + 0, total);
+        b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - nch;
+        for (int t = 0; t < nch; ++t) list[b0 + t] = (unsigned long long)unsigned(st + t);
+    }
+}
+
 // initial frontier: the sources' contracted out-edges as chunk entries
 __global__ void k_lev_seed(const int32_t *__restrict__ src_list, const int32_t *__restrict__ cptr,
                            int2 *__restrict__ out, int32_t *sc) {
@@ -476,6 +647,11 @@ __global__ void k_set_scalars(int32_t *sc) {
     if (threadIdx.x == 0) sc[SC_MAXLV] = -1;
 }
 
+int env_int_l(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 // Persistent cooperative grid: at most `cap` CTAs per SM (fewer CTAs = cheaper
 // grid barrier; the per-round work of these loops is small).
 int coop_grid(const void *func, int block, int sms, int cap = 2) {
@@ -577,7 +753,37 @@ int64_t levelize_device(Graph &g) {
             g.launches += 1;
         }
     }
-    {
+    if (env_int_l("HF_KAHN_ASYNC", 0)) {
+        // barrier-free Kahn: one list of all contracted-edge entries (<= cptr[n] <= m)
+        DevBuf lst, ctr;
+        const int64_t cap = std::max<int64_t>(m, 1);
+        lst.alloc(sizeof(unsigned long long) * size_t(cap), s);
+        ctr.alloc(sizeof(int32_t) * 4, s);
+        HF_CUDA(cudaMemsetAsync(lst.p, 0xff, sizeof(unsigned long long) * size_t(cap), s));
+        HF_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(int32_t) * 4, s));
+        k_lev_seed_async<<<grid_for(n, 256, g.sms), 256, 0, s>>>(lb.as<int32_t>(), cptr.as<int32_t>(),
+                                                                sc, lst.as<unsigned long long>(),
+                                                                ctr.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        lt.mark("contract+seed", s);
+        const int per_sm = std::max(1, env_int_l("HF_KAHN_ASYNC_CTAS", 4));
+        int grid = coop_grid((const void *)k_lev_kahn_async, 256, g.sms, per_sm);
+        const int32_t *cp = cptr.as<int32_t>(), *cd = cdst.as<int32_t>(), *cwp = cw.as<int32_t>();
+        int32_t *cn = cnt.as<int32_t>(), *lv = lev.as<int32_t>();
+        unsigned long long *lp = lst.as<unsigned long long>();
+        int32_t *cp2 = ctr.as<int32_t>();
+        int64_t capv = cap;
+        unsigned long long wd = 1000000ull * (unsigned long long)env_int_l("HF_KAHN_WATCHDOG_MS", 2000);
+        void *args[] = {&cp, &cd, &cwp, &cn, &lv, &lp, &capv, &cp2, &wd};
+        // cooperative launch only for the co-residency guarantee (the wait is a poll)
+        HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_lev_kahn_async, grid, 256, args, 0, s));
+        g.launches += 3;
+        lt.mark("kahn", s);
+        int32_t abort_flag = 0;
+        HF_CUDA(cudaMemcpyAsync(&abort_flag, cp2 + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        HF_CUDA(cudaStreamSynchronize(s));
+        if (abort_flag) fail(HF_ERR_CUDA, "levelizer watchdog expired (barrier-free Kahn)");
+    } else {
         // frontier entries {first contracted edge, node}: at most n + m/KCH per round
         DevBuf ea, eb2;
         const size_t ecap = size_t(n) + size_t(m) / KCH + 1;
