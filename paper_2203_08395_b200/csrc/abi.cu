@@ -111,6 +111,10 @@ static hf_status latch(Graph &g) {
     if (e) {
         HF_CUDA(cudaMemsetAsync(g.d_err(), 0, sizeof(uint32_t), g.stream));
         HF_CUDA(cudaStreamSynchronize(g.stream));
+        if (e & ERR_WATCHDOG) {
+            set_error("internal: a propagation pass waited past its watchdog deadline (results void)");
+            return HF_ERR_CUDA;
+        }
         set_error("device-side validation: NaN or inf in delays, source arrival times or required "
                   "times");
         return HF_ERR_INVALID_ARG;

@@ -45,6 +45,7 @@ enum : uint32_t {
     ERR_NONFINITE = 4u,  // NaN / inf value
     ERR_FO_PTR = 8u,     // fan-out ptr malformed / mismatch
     ERR_FO_DST = 16u,    // fan-out dst out of range / not a transpose
+    ERR_WATCHDOG = 32u,  // a dataflow pass waited past its deadline (must never happen)
 };
 
 // ---- stream-ordered scratch memory ----------------------------------------
@@ -151,6 +152,10 @@ struct Graph {
     DevBuf w2_in_nbr, w2_in_erow, w2_in_roff, w2_in_rstart;
     DevBuf w2_out_nbr, w2_out_erow, w2_out_roff, w2_out_rstart;
     bool w2_ready = false;
+    // dataflow passes (HF_LASTPART): plain neighbour ids of the level-ordered CSRs (a long
+    // neighbour's -(first part id + 1) decoded to its node)
+    DevBuf lo_in_pnbr, lo_out_pnbr;
+    bool pnbr_ready = false;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // single-pass scan state (primitives.cu): per-tile words + tile counter; one per

@@ -189,6 +189,32 @@ template <bool FWD> __device__ __forceinline__ float ident() {
     return __int_as_float(FWD ? 0xff800000 : 0x7f800000);   // -inf for max, +inf for min
 }
 
+__device__ __forceinline__ int atom_add_acq_rel_i(int *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+template <int V> __device__ __forceinline__ Vec<V> ld_ord_relaxed(const int32_t *p) {
+    Vec<V> r;
+    if constexpr (V == 4) {
+        int a, b, c, d;
+        asm volatile("ld.relaxed.gpu.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                     : "l"(p)
+                     : "memory");
+        r.x[0] = ord2f(a); r.x[1] = ord2f(b); r.x[2] = ord2f(c); r.x[3] = ord2f(d);
+    } else if constexpr (V == 2) {
+        int a, b;
+        asm volatile("ld.relaxed.gpu.global.v2.s32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p) : "memory");
+        r.x[0] = ord2f(a); r.x[1] = ord2f(b);
+    } else {
+        int a;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(a) : "l"(p) : "memory");
+        r.x[0] = ord2f(a);
+    }
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -208,7 +234,9 @@ struct FlowParams {
     int32_t L, S, nch;
     int32_t ecap, ncap;       // per-warp scratch capacity (edges, rows)
     const int32_t *part_np;   // [parts] by first part id
-    float *part_buf;          // [parts][S]
+    float *part_buf;          // [parts][S]   (HF_LASTPART = 0)
+    int32_t *part_acc;        // [parts][S] ordered ints, by first part id (HF_LASTPART)
+    int32_t *part_cnt;        // [parts][nch] finished parts per scenario chunk, by first part id
     const float *d;           // [m][S] by edge id
     const float *src_val;     // forward: at_src [n] (or null); backward: t_req [S] (or null)
     float t_scalar;           // backward: T when t_req is null
@@ -220,6 +248,7 @@ struct FlowParams {
     int32_t *wns_ord;         // backward: [S] ordered-int minima
     uint32_t *err;
     int32_t sleep_max;        // ns, cap of the poll back-off
+    int32_t watchdog_spins;   // poll rounds after which one wait gives up (ERR_WATCHDOG)
     int32_t poll_all;         // 1: every lane re-polls its missing vectors; 0: one lane polls
     unsigned long long *trace;   // optional: per task {t, level, t_start, t_ready, t_done}
     int32_t trace_cap;
@@ -228,6 +257,15 @@ struct FlowParams {
 // per-warp shared-memory scratch (bytes), identical on host and device
 #ifndef HF_IDX_SMEM
 #define HF_IDX_SMEM 0
+#endif
+// HF_LASTPART (default): the part tasks of a long row fold their partial max / min into
+// one ordered-int accumulator row (red.max / red.min) and count themselves on an
+// acq_rel counter; the last one writes the row's final value (and, backward, its
+// slack), so a long row is read by its consumers like any other row (plain neighbour
+// ids) and no finalisation kernel runs after the pass.  0: partial rows in part_buf,
+// every consumer combines them (PW at a time), k_finalize_split after the pass.
+#ifndef HF_LASTPART
+#define HF_LASTPART 0
 #endif
 struct WarpLayout {
     int d, a, at, nbr, eid, rp, node, ring, bytes;
@@ -269,8 +307,14 @@ template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 // 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured); the
 // backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
 template <int V, int LPN, bool FWD, bool GA, bool EARLY>
-#ifdef FLOW_MINB_BWD
-__global__ void __launch_bounds__(FLOW_THREADS, FWD ? 1 : FLOW_MINB_BWD) k_flow(FlowParams p) {
+#if defined(FLOW_MINB_FWD) || defined(FLOW_MINB_BWD)
+#ifndef FLOW_MINB_FWD
+#define FLOW_MINB_FWD 0
+#endif
+#ifndef FLOW_MINB_BWD
+#define FLOW_MINB_BWD 0
+#endif
+__global__ void __launch_bounds__(FLOW_THREADS, FWD ? FLOW_MINB_FWD : FLOW_MINB_BWD) k_flow(FlowParams p) {
 #else
 __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 #endif
@@ -351,12 +395,12 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
         const int k0 = lane, k1 = lane + 32;
         x.nbr0 = k0 < E ? __ldg(p.nbr + dsc.z + k0) : 0;
         x.eid0 = k0 < E ? __ldg(p.eid + dsc.z + k0) : 0;
-        x.rp0 = (!part && k0 <= NR) ? __ldg(p.row_ptr + dsc.x + k0) : 0;
+        x.rp0 = ((HF_LASTPART || !part) && k0 <= NR) ? __ldg(p.row_ptr + dsc.x + k0) : 0;
         x.node0 = k0 < NR ? __ldg(p.node_of + dsc.x + k0) : 0;
         if (NSL == 2) {
             x.nbr1 = k1 < E ? __ldg(p.nbr + dsc.z + k1) : 0;
             x.eid1 = k1 < E ? __ldg(p.eid + dsc.z + k1) : 0;
-            x.rp1 = (!part && k1 <= NR) ? __ldg(p.row_ptr + dsc.x + k1) : 0;
+            x.rp1 = ((HF_LASTPART || !part) && k1 <= NR) ? __ldg(p.row_ptr + dsc.x + k1) : 0;
             x.node1 = k1 < NR ? __ldg(p.node_of + dsc.x + k1) : 0;
         }
     };
@@ -398,7 +442,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
             cp_async_v<1>(reinterpret_cast<float *>(bn + k), reinterpret_cast<const float *>(p.nbr + dsc.z + k));
             cp_async_v<1>(reinterpret_cast<float *>(be + k), reinterpret_cast<const float *>(p.eid + dsc.z + k));
         }
-        if (!part)
+        if (HF_LASTPART || !part)
             for (int k = lane; k <= NR; k += 32)
                 cp_async_v<1>(reinterpret_cast<float *>(br + k), reinterpret_cast<const float *>(p.row_ptr + dsc.x + k));
         for (int k = lane; k < NR; k += 32)
@@ -473,7 +517,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
             s_nbr[lane] = X0.nbr0;
             s_eid[lane] = X0.eid0;
         }
-        if (!part && lane <= NR) s_rp[lane] = X0.rp0 - dsc.z;
+        if ((HF_LASTPART || !part) && lane <= NR) s_rp[lane] = X0.rp0 - dsc.z;
         if (lane < NR) s_node[lane] = X0.node0;
         if (NSL == 2) {
             const int k = lane + 32;
@@ -481,7 +525,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 s_nbr[k] = X0.nbr1;
                 s_eid[k] = X0.eid1;
             }
-            if (!part && k <= NR) s_rp[k] = X0.rp1 - dsc.z;
+            if ((HF_LASTPART || !part) && k <= NR) s_rp[k] = X0.rp1 - dsc.z;
             if (k < NR) s_node[k] = X0.node1;
         }
         __syncwarp();
@@ -531,7 +575,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 if (u >= 0) cp_async_v<V>(s_a + k * SC + gl * V, p.out + int64_t(u) * S + col);
             }
             cp_async_commit();
-            for (int k = g; k < E; k += G) {   // neighbours cut into parts (rare)
+            for (int k = g; !HF_LASTPART && k < E; k += G) {   // neighbours cut into parts (rare)
                 const int u = s_nbr[k];
                 if (u < 0) {
                     const int q0 = -u - 1;
@@ -594,10 +638,11 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 if (uu[r] >= 0 && uu[r] != INT32_MAX)
                     a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);
             }
-            // neighbours cut into parts: combine of their partials (rare)
+            // neighbours cut into parts: combine of their partials (rare; HF_LASTPART:
+            // never -- a long row's last part writes it like any other row)
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
-                if (uu[r] < 0) {
+                if (!HF_LASTPART && uu[r] < 0) {
                     const int q0 = -uu[r] - 1;
                     const int np = __ldg(p.part_np + q0);
 #pragma unroll
@@ -641,7 +686,19 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
             unsigned bal = __ballot_sync(FULL, miss);
             int ns = 32;
             if (p.trace && bal) HF_NPOLL_INC();
+            int spins = 0;
             while (bal) {
+                // watchdog: a wait of more than watchdog_spins poll rounds (each >= one
+                // L2 round trip: seconds; a schedule bug, never a legal input) gives
+                // up instead of hanging the GPU
+                if (++spins > p.watchdog_spins) {
+                    atomicOr(p.err, ERR_WATCHDOG);
+#pragma unroll
+                    for (int r = 0; r < RB; ++r)
+#pragma unroll
+                        for (int j = 0; j < V; ++j) a[r].x[j] = 0.0f;
+                    break;
+                }
                 if (p.poll_all) {
                     // every lane re-loads its own missing vectors (one round trip per round)
                     __nanosleep(ns);
@@ -710,7 +767,50 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 #pragma unroll
                 for (int j = 0; j < V; ++j)
                     acc.x[j] = combine<MX>(acc.x[j], __shfl_xor_sync(FULL, acc.x[j], o));
+#if HF_LASTPART
+            // this part's partial -> the row's accumulator; the last part writes the row
+            const int rb_rel = s_rp[0] - rp_base, re_rel = s_rp[1] - rp_base;   // row - task edge base
+            const int np = (re_rel - rb_rel + LO_PE - 1) / LO_PE;
+            const int q0 = (-dsc.y - 1) - (-rb_rel) / LO_PE;   // first part id of the row
+            int32_t *ap = p.part_acc + int64_t(q0) * S + col;
+            if (g == 0) {
+#pragma unroll
+                for (int j = 0; j < V; ++j) {
+                    if (MX) atomicMax(ap + j, f2ord(acc.x[j]));
+                    else atomicMin(ap + j, f2ord(acc.x[j]));
+                }
+            }
+            __syncwarp();   // every lane's red before lane 0's release
+            int last = 0;
+            // one counter per (row, scenario chunk): every chunk has its own np part tasks
+            if (lane == 0) last = atom_add_acq_rel_i(p.part_cnt + int64_t(q0) * p.nch + c, 1) == np - 1;
+            last = __shfl_sync(FULL, last, 0);
+            if (last) {
+                __syncwarp();   // lane 0's acquire before the accumulator loads
+                if (!FWD && c != run_c) {
+                    flush_run();
+                    run_c = c;
+                }
+                if (g == 0) {
+                    const Vec<V> best = ld_ord_relaxed<V>(ap);
+                    const int node = s_node[0];
+                    st_relaxed<V>(p.out + int64_t(node) * S + col, best);
+                    if (FWD && p.prefill) st_plain<V>(p.prefill + int64_t(node) * S + col, nan_vec<V>());
+                    if (!FWD && p.other) {
+                        const Vec<V> av = ld_relaxed<V>(p.other + int64_t(node) * S + col);
+                        Vec<V> sl;
+#pragma unroll
+                        for (int j = 0; j < V; ++j) {
+                            sl.x[j] = EARLY ? __fsub_rn(av.x[j], best.x[j]) : __fsub_rn(best.x[j], av.x[j]);
+                            run.x[j] = fminf(run.x[j], sl.x[j]);
+                        }
+                        if (p.slack) st_plain<V>(p.slack + int64_t(node) * S + col, sl);
+                    }
+                }
+            }
+#else
             if (g == 0) st_relaxed<V>(p.part_buf + int64_t(-dsc.y - 1) * S + col, acc);
+#endif
         } else {
             if (!FWD && c != run_c) {
                 flush_run();
@@ -894,6 +994,26 @@ __global__ void k_finalize_split(const int32_t *__restrict__ np_arr, const int32
         __syncthreads();
         for (int s = threadIdx.x; s < S; s += blockDim.x)
             if (s_wmin[s] != 0x7f800000) atomicMin(wns_ord + s, s_wmin[s]);
+    }
+}
+
+// plain neighbour ids (HF_LASTPART): a long neighbour's -(first part id + 1) -> its node
+__global__ void k_plain_nbr(const int32_t *__restrict__ nbr, const int32_t *__restrict__ part_row,
+                            const int32_t *__restrict__ node_of, int32_t m, int32_t *__restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int u = nbr[e];
+        out[e] = u >= 0 ? u : node_of[part_row[-u - 1]];
+    }
+}
+// the long rows' accumulators at the combine's identity and their part counters at 0
+__global__ void k_fill_acc(int32_t *acc, int32_t *cnt, const int32_t *count, int32_t S, int32_t nch,
+                           int32_t ident) {
+    const int64_t np = *count, total = np * S;   // nch <= S: the counters fit the same sweep
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        acc[i] = ident;
+        if (i < np * nch) cnt[i] = 0;
     }
 }
 
@@ -1347,6 +1467,25 @@ void fill_nan(Graph &g, float *buf, size_t cnt, cudaStream_t st) {
     }
 }
 
+void pnbr_prepare(Graph &g) {
+    if (g.pnbr_ready) return;
+    cudaStream_t s = g.stream;
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool in = dir == 0;
+        DevBuf &pn = in ? g.lo_in_pnbr : g.lo_out_pnbr;
+        pn.alloc(sizeof(int32_t) * std::max<int64_t>(g.m, 1), s);
+        if (!g.m) continue;
+        const int32_t *npa = in ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
+        k_plain_nbr<<<grid_for(g.m, 256, g.sms), 256, 0, s>>>(
+            in ? g.lo_in_nbr.as<int32_t>() : g.lo_out_nbr.as<int32_t>(),
+            npa + (in ? g.np_cap_in : g.np_cap_out),
+            in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>(), g.m, pn.as<int32_t>());
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+    g.pnbr_ready = true;
+}
+
 // task schedule, bases, partial buffer and the sentinel fill of the output (on the
 // graph's stream)
 template <bool FWD>
@@ -1370,6 +1509,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     p.ecap = tw + LO_SPLIT;
     p.ncap = tw;
     p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
+    p.watchdog_spins = std::max(1, env_int("HF_WATCHDOG_SPINS", 1 << 22));
     p.poll_all = env_int("HF_POLL_ALL", 1);
     TaskSched &ts = FWD ? g.ts_f : g.ts_b;
     cx.nparts = FWD ? g.np_cap_in : g.np_cap_out;   // bound; exact count on the device
@@ -1391,7 +1531,24 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     p.part_np = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
     p.L = g.L;
     p.err = g.d_err();
+#if HF_LASTPART
+    pnbr_prepare(g);
+    p.nbr = FWD ? g.lo_in_pnbr.as<int32_t>() : g.lo_out_pnbr.as<int32_t>();
     if (cx.nparts > 0) {
+        cx.part_buf.alloc(sizeof(int32_t) * size_t(cx.nparts) * (size_t(p.S) + size_t(p.nch)), s);
+        p.part_acc = cx.part_buf.as<int32_t>();
+        p.part_cnt = p.part_acc + size_t(cx.nparts) * p.S;
+        const bool mx = FWD != g.early;   // max for late forward / early backward
+        k_fill_acc<<<grid_for(int64_t(cx.nparts) * p.S, 256, g.sms), 256, 0, s>>>(
+            p.part_acc, p.part_cnt, nparts_dev, p.S, p.nch,
+            mx ? int32_t(0x807fffff) : int32_t(0x7f800000));
+        HF_CHECK_LAUNCH();
+        g.launches += 1;
+    }
+    if (false) {
+#else
+    if (cx.nparts > 0) {
+#endif
         cx.part_buf.alloc(sizeof(float) * size_t(cx.nparts) * p.S, s);
         p.part_buf = cx.part_buf.as<float>();
         // NaN sentinel over the partials actually used (count read on the device)
@@ -1409,7 +1566,7 @@ template <bool FWD>
 void launch_pass(Graph &g, FlowParams &p, bool check_d, int V, PassCtx &cx, cudaStream_t st,
                  int cap) {
     dispatch<FWD>(g, p, V, cx.LPN, st, cap);
-    if (cx.nparts > 0) {
+    if (!HF_LASTPART && cx.nparts > 0) {
         const int32_t *npa = FWD ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
         const int32_t *prow = npa + (FWD ? g.np_cap_in : g.np_cap_out);
         const int32_t *nparts_dev = g.nparts_d + (FWD ? 0 : 1);

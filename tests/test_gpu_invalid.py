@@ -12,6 +12,8 @@
   long-row finalisation and the slack epilogue): S = 257 (V = 1), 514 (V = 2),
   2048 (V = 4) on a graph with long rows, all at/rat/wns 0 ULP against the oracle.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -227,4 +229,34 @@ def test_wide_rows_finalisation(hf, g, S, concurrent, monkeypatch):
     assert np.array_equal(bits(at.cpu().numpy().reshape(g.n, S)), bits(ato))
     assert np.array_equal(bits(rat.cpu().numpy().reshape(g.n, S)), bits(rato))
     assert np.array_equal(bits(w.cpu().numpy()), bits(wo))
+    G.close()
+
+
+def test_watchdog_turns_a_stuck_wait_into_an_error(hf, monkeypatch):
+    """HF_WATCHDOG_SPINS=1: every dataflow wait gives up after one poll round, as a
+    schedule bug would after seconds -- the call must return HF_ERR_CUDA ('watchdog')
+    instead of hanging, and the next call on the same graph must be clean."""
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.config("C3")
+    S = 64
+    D = torch.from_numpy(hfgen.scenario_delays(g, 0, S, "ms")).to(dev)
+    T = torch.full((S,), float(g.t_req), dtype=torch.float32, device=dev)
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_levelize(G)
+    at_src = torch.from_numpy(g.at_src).to(dev)
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    monkeypatch.setenv("HF_WATCHDOG_SPINS", "1")
+    with pytest.raises(hf.HFError) as ei:
+        hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, at_src, w)
+        hf.hf_sync(G)
+    assert ei.value.status == hf.HF_ERR_CUDA and "watchdog" in str(ei.value)
+    monkeypatch.delenv("HF_WATCHDOG_SPINS")
+    hf.hf_run_batch(G, S, D, hf.HF_LAYOUT_MS, T, at_src, w)
+    hf.hf_sync(G)
+    wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D.cpu().numpy(), T.cpu().numpy(), g.at_src,
+                      "ms", threads=os.cpu_count() or 1)
+    assert np.array_equal(w.cpu().numpy().view(np.uint32), wo.view(np.uint32))
     G.close()
