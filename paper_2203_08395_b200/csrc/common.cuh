@@ -156,6 +156,9 @@ struct Graph {
     // neighbour's -(first part id + 1) decoded to its node)
     DevBuf lo_in_pnbr, lo_out_pnbr;
     bool pnbr_ready = false;
+    // S = 1 (k_wide3): {plain neighbour, destination node} per level-ordered edge
+    DevBuf w3_in_edge, w3_out_edge;
+    bool w3_ready = false;
     // batch workspace (at / rat when the caller does not want them), grows on demand
     DevBuf ws_at, ws_rat, ws_sync, ws_wns;
     // single-pass scan state (primitives.cu): per-tile words + tile counter; one per

@@ -926,7 +926,7 @@ int64_t levelize_device(Graph &g) {
     // np_cap and read the exact part counts (sc[12], sc[13]) on the device
     g.nparts_d = sc + 12;
     g.ts_f.key = g.ts_b.key = -1;   // task schedules depend on the levels
-    g.wide_ready = g.lo_d_ready = g.w2_ready = g.pnbr_ready = false;
+    g.wide_ready = g.lo_d_ready = g.w2_ready = g.pnbr_ready = g.w3_ready = false;
     g.L = L;
     g.levelized = true;
     return 0;

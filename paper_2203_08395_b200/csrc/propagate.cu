@@ -325,7 +325,13 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
     constexpr int NSL = idx_slots<LPN>();
     // GA: gathers land in shared memory by cp.async (16-byte pieces, V == 4);
     // else in registers, RB per lane per batch
-    constexpr int RB = V == 4 ? 4 : 8;
+#ifndef RB4_FWD
+#define RB4_FWD 4
+#endif
+#ifndef RB4_BWD
+#define RB4_BWD 4
+#endif
+    constexpr int RB = V == 4 ? (FWD ? RB4_FWD : RB4_BWD) : 8;
     extern __shared__ __align__(16) unsigned char smem[];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane / LPN, gl = lane % LPN;

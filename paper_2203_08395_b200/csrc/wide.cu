@@ -1056,6 +1056,213 @@ int w2_blocks(const Graph &g) {
     return g.sms * per_sm;
 }
 
+// ---- S = 1: edge units, ordered-int row accumulation in place (k_wide3) ----------
+// The output array holds ORDERED INTS during the pass (f2ord: order-preserving for
+// every non-NaN float), initialised to the combine's identity, or to at_src / T for
+// the rows without edges.  A level of the level-ordered CSR is one contiguous edge
+// run [row_ptr[level start], row_ptr[level end]); warp units are 32 consecutive
+// edges of it -- no row structure is needed, every address is arithmetic: per edge
+// one {plain neighbour, destination node} int2 and the delay (coalesced), then the
+// gather out[neighbour] (an ordered int: ord2f).  x = fl(a +/- d); a segmented max /
+// min over the lanes (a row's edges are consecutive) leaves one value per row piece:
+// a row wholly inside the unit is stored, a row that continues into a neighbouring
+// unit is folded in with an ordered-int atomic max / min (exact: R10).  W3_U units
+// per warp are in flight together.  Grid barrier between levels, split: a block
+// arrives, loads its first units of the next level, then waits.  After the pass one
+// streaming kernel turns the ordered ints back into floats in place (backward: the
+// slack and the worst slack fused).
+constexpr int W3_THREADS = 256;
+#ifndef W3_U_OVR
+#define W3_U_OVR 4
+#endif
+constexpr int W3_U = W3_U_OVR;
+
+struct Wide3Params {
+    const int32_t *level_ptr;   // [L+1]
+    const int32_t *row_ptr;     // [n+1] level-ordered CSR of this direction
+    const int2 *edge;           // [m] {plain neighbour node, destination node}
+    const int32_t *eid;         // [m] delay index of each position, or null: d level-ordered
+    const float *d;
+    int32_t L;
+    int32_t *out;               // [n] ordered ints during the pass
+    uint32_t *err;
+    unsigned *bar;
+};
+
+template <bool FWD, bool EARLY>
+__global__ void __launch_bounds__(W3_THREADS) k_wide3(Wide3Params p) {
+    constexpr bool MX = FWD != EARLY;
+    const int lane = threadIdx.x & 31;
+    const int W = (gridDim.x * blockDim.x) >> 5;
+    const int w = (threadIdx.x >> 5) * gridDim.x + blockIdx.x;   // consecutive units on different SMs
+    const float ident = __int_as_float(MX ? 0xff800000 : 0x7f800000);
+    unsigned target = 0;
+    bool bad = false;
+    int k = FWD ? 0 : p.L - 1;
+    int eb = __ldg(p.row_ptr + __ldg(p.level_ptr + k)), ee = __ldg(p.row_ptr + __ldg(p.level_ptr + k + 1));
+    // round-1 loads of U units: {neighbour, destination}, delay, the keys next to the unit
+    int2 ed[W3_U];
+    float dv[W3_U];
+    int kprev[W3_U], knext[W3_U];
+    auto load_units = [&](int ubase) {
+#pragma unroll
+        for (int i = 0; i < W3_U; ++i) {
+            const int e0 = eb + ((ubase + i * W) << 5);
+            const int e = e0 + lane;
+            ed[i] = make_int2(0, -1 - lane);   // unique negative key: never stored
+            dv[i] = 0.0f;
+            kprev[i] = knext[i] = -1;
+            if (e < ee) {
+                ed[i] = __ldg(p.edge + e);
+                dv[i] = p.eid ? __ldg(p.d + __ldg(p.eid + e)) : __ldg(p.d + e);
+            }
+            if (e0 < ee) {
+                if (lane == 0 && e0 > eb) kprev[i] = __ldg(p.edge + e0 - 1).y;
+                if (lane == 31 && e0 + 32 < ee) knext[i] = __ldg(p.edge + e0 + 32).y;
+            }
+        }
+    };
+    load_units(w);
+    for (int qq = 0; qq < p.L; ++qq) {
+        const int nunits = (ee - eb + 31) >> 5;
+        for (int ub = w; ub < nunits; ub += W3_U * W) {
+            if (ub != w) load_units(ub);
+            float av[W3_U];
+#pragma unroll
+            for (int i = 0; i < W3_U; ++i)
+                av[i] = ed[i].y >= 0 ? ord2f(__ldcg(p.out + ed[i].x)) : ident;
+#pragma unroll
+            for (int i = 0; i < W3_U; ++i) {
+                if (ub + i * W >= nunits) break;   // warp-uniform
+                const int key = ed[i].y;
+                const bool valid = key >= 0;
+                float v = valid ? relax1<FWD>(av[i], sane(dv[i], bad)) : ident;
+                const int prv = __shfl_up_sync(0xffffffffu, key, 1);
+                const int nxt = __shfl_down_sync(0xffffffffu, key, 1);
+                const unsigned smask = __ballot_sync(0xffffffffu, lane == 0 || prv != key);
+                const int sstart = 31 - __clz(smask & ((2u << lane) - 1u));
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float y = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane - o >= sstart) v = comb<MX>(v, y);
+                }
+                const bool seg_end = valid && (lane == 31 || nxt != key);
+                // the row continues into the previous / next unit?
+                const int kp = __shfl_sync(0xffffffffu, kprev[i], 0);
+                const int kn = __shfl_sync(0xffffffffu, knext[i], 31);
+                const bool open = (sstart == 0 && kp == key) || (lane == 31 && kn == key);
+                if (seg_end) {
+                    if (open) {
+                        if (MX) atomicMax(p.out + key, f2ord(v));
+                        else atomicMin(p.out + key, f2ord(v));
+                    } else {
+                        p.out[key] = f2ord(v);
+                    }
+                }
+            }
+        }
+        if (qq + 1 == p.L) break;
+        // split grid barrier: arrive, load the first units of the next level, wait
+        target += gridDim.x;
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+        k = FWD ? qq + 1 : p.L - 2 - qq;
+        eb = __ldg(p.row_ptr + __ldg(p.level_ptr + k));
+        ee = __ldg(p.row_ptr + __ldg(p.level_ptr + k + 1));
+        load_units(w);
+        if (threadIdx.x == 0)
+            while (ld_acq(p.bar) < target) __nanosleep(32);
+        __syncthreads();
+    }
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
+}
+
+// before a k_wide3 pass: every row's accumulator at the identity, rows without edges
+// at their value (forward: at_src or +0; backward: T)
+template <bool FWD, bool EARLY>
+__global__ void k_w3_init(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
+                          int32_t n, const float *__restrict__ src_val, float t_scalar,
+                          int32_t *__restrict__ out, uint32_t *err) {
+    constexpr bool MX = FWD != EARLY;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int node = node_of[i];
+        int32_t v;
+        if (row_ptr[i + 1] != row_ptr[i]) {
+            v = MX ? ORD_NEG_INF : ORD_POS_INF;
+        } else {
+            const float x = FWD ? (src_val ? sane(src_val[node], bad) : 0.0f)
+                                : sane(src_val ? src_val[0] : t_scalar, bad);
+            v = f2ord(x);
+        }
+        out[node] = v;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, ERR_NONFINITE);
+}
+
+// after a k_wide3 pass: ordered ints back to floats in place; backward: slack and the
+// worst slack (ordered-int atomicMin per block)
+template <bool FWD, bool EARLY>
+__global__ void k_w3_final(int32_t *__restrict__ out, int32_t n, const float *__restrict__ other,
+                           float *__restrict__ slack, int32_t *__restrict__ wns_ord) {
+    __shared__ int32_t s_wmin;
+    const bool do_slack = !FWD && other;
+    if (threadIdx.x == 0) s_wmin = ORD_POS_INF;
+    __syncthreads();
+    float mn = __int_as_float(ORD_POS_INF);
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n;
+         v += int64_t(gridDim.x) * blockDim.x) {
+        const float x = ord2f(out[v]);
+        reinterpret_cast<float *>(out)[v] = x;
+        if (do_slack) {
+            const float a = other[v];
+            const float sl = EARLY ? __fsub_rn(a, x) : __fsub_rn(x, a);
+            mn = fminf(mn, sl);
+            if (slack) slack[v] = sl;
+        }
+    }
+    if (do_slack) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if ((threadIdx.x & 31) == 0 && mn != __int_as_float(ORD_POS_INF)) atomicMin(&s_wmin, f2ord(mn));
+        __syncthreads();
+        if (threadIdx.x == 0 && s_wmin != ORD_POS_INF) atomicMin(wns_ord, s_wmin);
+    }
+}
+
+// {plain neighbour, destination node} per level-ordered edge (k_wide3)
+__global__ void k_w3_edges(const int32_t *__restrict__ nbr, const int32_t *__restrict__ part_row,
+                           const int32_t *__restrict__ node_of, const int32_t *__restrict__ erow,
+                           int32_t m, int2 *__restrict__ out) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int u = nbr[e];
+        out[e] = make_int2(u >= 0 ? u : node_of[part_row[-u - 1]], node_of[erow[e]]);
+    }
+}
+
+template <bool FWD, bool EARLY>
+int w3_blocks(const Graph &g) {
+    auto kern = k_wide3<FWD, EARLY>;
+    static std::map<std::pair<const void *, int>, int> cache;
+    static std::mutex mu;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({(const void *)kern, g.device});
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W3_THREADS, 0));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[{(const void *)kern, g.device}] = per_sm;
+    }
+    const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
+    if (cap > 0) per_sm = std::min(per_sm, cap);
+    return g.sms * per_sm;
+}
+
 }  // namespace
 
 // Build (once per levelization) the slices of both directions.
@@ -1140,6 +1347,32 @@ void wide2_prepare(Graph &g) {
     g.w2_ready = true;
 }
 
+// k_wide3 edge table of both directions (once per levelization)
+void wide3_prepare(Graph &g) {
+    if (g.w3_ready) return;
+    cudaStream_t s = g.stream;
+    const int32_t n = g.n, m = g.m;
+    DevBuf erow;
+    erow.alloc(sizeof(int32_t) * std::max<int64_t>(m, 1), s);
+    for (int dir = 0; dir < 2; ++dir) {
+        const bool in = dir == 0;
+        DevBuf &ed = in ? g.w3_in_edge : g.w3_out_edge;
+        ed.alloc(sizeof(int2) * std::max<int64_t>(m, 1), s);
+        if (!m) continue;
+        const int32_t *rp = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+        const int32_t *npa = in ? g.lo_in_np.as<int32_t>() : g.lo_out_np.as<int32_t>();
+        csr_row_ids(rp, n, erow.as<int32_t>(), s, g);
+        k_w3_edges<<<grid_for(m, 256, g.sms), 256, 0, s>>>(
+            in ? g.lo_in_nbr.as<int32_t>() : g.lo_out_nbr.as<int32_t>(),
+            npa + (in ? g.np_cap_in : g.np_cap_out),
+            in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>(), erow.as<int32_t>(), m,
+            ed.as<int2>());
+        HF_CHECK_LAUNCH();
+        g.launches += 2;
+    }
+    g.w3_ready = true;
+}
+
 // The graph's own delays in level order of both directions (single-set calls).
 void lo_delays_prepare(Graph &g) {
     if (g.lo_d_ready) return;
@@ -1202,6 +1435,44 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
     p.slack = slack;
     p.wns_ord = wns_ord;
     p.err = g.d_err();
+    if (S == 1 && env_int_w("HF_WIDE3", 1)) {
+        wide3_prepare(g);
+        const int32_t *rp = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
+        const int32_t *no = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
+        int32_t *acc = reinterpret_cast<int32_t *>(out);   // ordered ints during the pass
+#define HF_W3(EE)                                                                                  \
+    do {                                                                                           \
+        k_w3_init<FWD, EE><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(rp, no, g.n, src_val,        \
+                                                                      t_scalar, acc, p.err);       \
+        HF_CHECK_LAUNCH();                                                                         \
+        Wide3Params w{};                                                                           \
+        w.level_ptr = g.level_ptr.as<int32_t>();                                                   \
+        w.row_ptr = rp;                                                                            \
+        w.edge = in ? g.w3_in_edge.as<int2>() : g.w3_out_edge.as<int2>();                         \
+        w.eid = p.eid;                                                                             \
+        w.d = d;                                                                                   \
+        w.L = g.L;                                                                                 \
+        w.out = acc;                                                                               \
+        w.err = p.err;                                                                             \
+        DevBuf bar3;                                                                               \
+        bar3.alloc(sizeof(unsigned) * 2, st);                                                      \
+        HF_CUDA(cudaMemsetAsync(bar3.p, 0, sizeof(unsigned) * 2, st));                             \
+        w.bar = bar3.as<unsigned>();                                                               \
+        const int nblk = w3_blocks<FWD, EE>(g);                                                    \
+        if (nblk < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");         \
+        void *args[] = {&w};                                                                       \
+        HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_wide3<FWD, EE>, nblk, W3_THREADS, args, \
+                                            0, st));                                               \
+        k_w3_final<FWD, EE><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(acc, g.n, other, slack,     \
+                                                                       wns_ord);                   \
+        HF_CHECK_LAUNCH();                                                                         \
+        g.launches += 3;                                                                           \
+    } while (0)
+        if (g.early) HF_W3(true);
+        else HF_W3(false);
+#undef HF_W3
+        return;
+    }
     if (S == 1 && env_int_w("HF_WIDE2", 0)) {
         wide2_prepare(g);
         Wide2Params w{};

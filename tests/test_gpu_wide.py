@@ -26,22 +26,32 @@ def hf():
     return _hf
 
 
-# S = 1 runs k_wide2 (row ranges, shared accumulators) by default; HF_WIDE2=0 keeps
-# the warp-unit kernel k_wide1 under test as well
-@pytest.mark.parametrize("w2", ["1", "0"])
+# S = 1 runs k_wide3 (edge units, ordered-int accumulation in place) by default; the
+# warp-unit kernel k_wide1 (HF_WIDE3=0) and the row-range kernel k_wide2 (HF_WIDE2=1)
+# stay under test
+KERNELS = {"w3": {"HF_WIDE3": "1"}, "w1": {"HF_WIDE3": "0", "HF_WIDE2": "0"},
+           "w2": {"HF_WIDE3": "0", "HF_WIDE2": "1"}}
+
+
+def use_kernel(monkeypatch, name):
+    for k, v in KERNELS[name].items():
+        monkeypatch.setenv(k, v)
+
+
+@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
 @pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C3", 0.05), ("C2-random", 0.01),
                                         ("C5", 0.01), ("C5", 0.1)])
 def test_wide_single(hf, name, scale, w2, monkeypatch):
     monkeypatch.setenv("HF_WIDE", "1")
-    monkeypatch.setenv("HF_WIDE2", w2)
+    use_kernel(monkeypatch, w2)
     g = hfgen.config(name, scale)
     check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req)
 
 
-@pytest.mark.parametrize("w2", ["1", "0"])
+@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
 def test_wide_tiny_random_dags(hf, w2, monkeypatch):
     monkeypatch.setenv("HF_WIDE", "1")
-    monkeypatch.setenv("HF_WIDE2", w2)
+    use_kernel(monkeypatch, w2)
     rng = np.random.default_rng(2203)
     for trial in range(80):
         n, edges = random_tiny_dag(rng, nmax=12)
@@ -52,13 +62,14 @@ def test_wide_tiny_random_dags(hf, w2, monkeypatch):
                      float(mixed_delays(rng, 1)[0]))
 
 
-@pytest.mark.parametrize("w2", ["1", "0"])
+@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
 def test_wide_hub_fan_in(hf, w2, monkeypatch):
     """One node with 10^4 predecessors (C5's planted hub): k_wide1 folds its slices by
     atomics into one slot and its consumers read the slot; k_wide2 keeps the row in
-    one range (its 10^4 edges streamed through the shared accumulator)."""
+    one range (its 10^4 edges streamed through the shared accumulator); k_wide3 spans
+    313 edge units whose pieces meet in ordered-int atomics."""
     monkeypatch.setenv("HF_WIDE", "1")
-    monkeypatch.setenv("HF_WIDE2", w2)
+    use_kernel(monkeypatch, w2)
     rng = np.random.default_rng(7)
     k = 10000
     edges = [(i, k) for i in range(k)] + [(k, k + 1), (k, k + 2), (3, k + 2)]
