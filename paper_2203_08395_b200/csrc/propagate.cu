@@ -540,6 +540,10 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 #ifdef HF_DELAY_EVICT_FIRST
             cp_async_v_ef<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col,
                              policy_evict_first());
+#elif defined(HF_DBG_FAKE_DELAY)
+            // diagnostic build only (wrong results): every task reads delay row k of a
+            // tiny L2-resident set -- how much of a pass is the delay rows' latency?
+            cp_async_v<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k] & 8191) * S + col);
 #else
             cp_async_v<V>(s_d + k * SC + gl * V, p.d + int64_t(s_eid[k]) * S + col);
 #endif

@@ -1073,7 +1073,7 @@ int w2_blocks(const Graph &g) {
 // slack and the worst slack fused).
 constexpr int W3_THREADS = 256;
 #ifndef W3_U_OVR
-#define W3_U_OVR 4
+#define W3_U_OVR 8
 #endif
 constexpr int W3_U = W3_U_OVR;
 
@@ -1177,26 +1177,26 @@ __global__ void __launch_bounds__(W3_THREADS) k_wide3(Wide3Params p) {
     if (bad) atomicOr(p.err, ERR_NONFINITE);
 }
 
-// before a k_wide3 pass: every row's accumulator at the identity, rows without edges
-// at their value (forward: at_src or +0; backward: T)
+// before a k_wide3 pass: every node's accumulator at the identity, nodes without edges
+// in this direction at their value (forward: at_src or +0; backward: T) -- by node id,
+// so every access is coalesced (ptr = the node-indexed CSR of this direction)
 template <bool FWD, bool EARLY>
-__global__ void k_w3_init(const int32_t *__restrict__ row_ptr, const int32_t *__restrict__ node_of,
-                          int32_t n, const float *__restrict__ src_val, float t_scalar,
+__global__ void k_w3_init(const int32_t *__restrict__ ptr, int32_t n,
+                          const float *__restrict__ src_val, float t_scalar,
                           int32_t *__restrict__ out, uint32_t *err) {
     constexpr bool MX = FWD != EARLY;
     bool bad = false;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int node = node_of[i];
-        int32_t v;
-        if (row_ptr[i + 1] != row_ptr[i]) {
-            v = MX ? ORD_NEG_INF : ORD_POS_INF;
+    const float tb = FWD ? 0.0f : (src_val ? src_val[0] : t_scalar);
+    for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n;
+         v += int64_t(gridDim.x) * blockDim.x) {
+        int32_t o;
+        if (ptr[v + 1] != ptr[v]) {
+            o = MX ? ORD_NEG_INF : ORD_POS_INF;
         } else {
-            const float x = FWD ? (src_val ? sane(src_val[node], bad) : 0.0f)
-                                : sane(src_val ? src_val[0] : t_scalar, bad);
-            v = f2ord(x);
+            const float x = FWD ? (src_val ? sane(src_val[v], bad) : 0.0f) : sane(tb, bad);
+            o = f2ord(x);
         }
-        out[node] = v;
+        out[v] = o;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, ERR_NONFINITE);
 }
@@ -1438,12 +1438,12 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
     if (S == 1 && env_int_w("HF_WIDE3", 1)) {
         wide3_prepare(g);
         const int32_t *rp = in ? g.lo_in_ptr.as<int32_t>() : g.lo_out_ptr.as<int32_t>();
-        const int32_t *no = in ? g.lo_in_node.as<int32_t>() : g.lo_out_node.as<int32_t>();
         int32_t *acc = reinterpret_cast<int32_t *>(out);   // ordered ints during the pass
 #define HF_W3(EE)                                                                                  \
     do {                                                                                           \
-        k_w3_init<FWD, EE><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(rp, no, g.n, src_val,        \
-                                                                      t_scalar, acc, p.err);       \
+        k_w3_init<FWD, EE><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(                            \
+            in ? g.in_ptr.as<int32_t>() : g.out_ptr.as<int32_t>(), g.n, src_val, t_scalar, acc,     \
+            p.err);                                                                                \
         HF_CHECK_LAUNCH();                                                                         \
         Wide3Params w{};                                                                           \
         w.level_ptr = g.level_ptr.as<int32_t>();                                                   \
