@@ -1177,6 +1177,202 @@ __global__ void __launch_bounds__(W3_THREADS) k_wide3(Wide3Params p) {
     if (bad) atomicOr(p.err, ERR_NONFINITE);
 }
 
+// ---- S = 1: k_wide4 -- k_wide3's edge units with the structure staged in shared memory
+// Each CTA (1024 threads, one per SM) owns one contiguous share of every level's edge
+// run, processed in tiles of W4_TE edges.  A tile's {neighbour, destination} int2s and
+// delays (or delay ids) are copied into shared memory by cp.async one tile AHEAD --
+// the next tile of the level, or the next level's first tile (structure is never
+// written by the pass, so it may be fetched before the grid barrier) -- so after the
+// barrier a tile costs one gather round trip: every thread issues the gathers of its
+// up to W4_K edges at once, then the segmented combine / store / ordered-int atomic
+// of k_wide3 (a row that continues past the tile or the CTA's share is folded in
+// atomically).  Two tile buffers (2 x 73 KB).
+// MEASURED AND NOT TAKEN (C5): 0.367 + 0.349 ms against k_wide3's 0.313 + 0.302 -- one
+// gather round trip per tile does not help because the level is bound by the random
+// 32-byte sector traffic (one sector per 4-byte gather and per row store), not by the
+// number of dependent round trips; kept behind HF_WIDE4=1 and parity-tested.
+constexpr int W4_THREADS = 1024;
+constexpr int W4_TE = 6144;
+constexpr int W4_K = W4_TE / W4_THREADS;   // edges per thread per tile
+
+struct Wide4Params {
+    const int32_t *level_ptr, *row_ptr;   // level-ordered CSR of this direction
+    const int2 *edge;                     // [m] {plain neighbour node, destination node}
+    const int32_t *eid;                   // [m] delay index per position, or null: d level-ordered
+    const float *d;
+    int32_t L;
+    int32_t *out;                         // [n] ordered ints during the pass
+    uint32_t *err;
+    unsigned *bar;
+};
+
+__device__ __forceinline__ void cp_async_8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+template <bool FWD, bool EARLY>
+__global__ void __launch_bounds__(W4_THREADS, 1) k_wide4(Wide4Params p) {
+    constexpr bool MX = FWD != EARLY;
+    extern __shared__ __align__(16) unsigned char w4_smem[];
+    int2 *s_e[2] = {reinterpret_cast<int2 *>(w4_smem), reinterpret_cast<int2 *>(w4_smem) + W4_TE};
+    int32_t *s_d[2] = {reinterpret_cast<int32_t *>(s_e[1] + W4_TE),
+                       reinterpret_cast<int32_t *>(s_e[1] + W4_TE) + W4_TE};
+    __shared__ int s_keys[2][2];   // destination of the edge before / after the tile (-1: none)
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nC = gridDim.x, c = blockIdx.x;
+    const float ident = __int_as_float(MX ? 0xff800000 : 0x7f800000);
+    unsigned target = 0;
+    bool bad = false;
+    // a tile: [ta, tb) of level edge run [eb, ee)
+    auto share = [&](int k, int &sa, int &sb, int &eb, int &ee) {
+        eb = __ldg(p.row_ptr + __ldg(p.level_ptr + k));
+        ee = __ldg(p.row_ptr + __ldg(p.level_ptr + k + 1));
+        const int len = ee - eb, sz = (len + nC - 1) / nC;
+        sa = min(ee, eb + c * sz);
+        sb = min(ee, sa + sz);
+    };
+    auto issue = [&](int buf, int ta, int tb, int eb, int ee) {
+        for (int j = tid; j < tb - ta; j += W4_THREADS) {
+            cp_async_8(s_e[buf] + j, p.edge + ta + j);
+            cp_async_4(s_d[buf] + j, p.eid ? reinterpret_cast<const void *>(p.eid + ta + j)
+                                           : reinterpret_cast<const void *>(p.d + ta + j));
+        }
+        if (tid == 0) {
+            if (ta > eb && ta < tb) cp_async_4(&s_keys[buf][0], &p.edge[ta - 1].y);
+            else s_keys[buf][0] = -1;
+            if (tb < ee && ta < tb) cp_async_4(&s_keys[buf][1], &p.edge[tb].y);
+            else s_keys[buf][1] = -1;
+        }
+    };
+    // first tile of the first level
+    int qq = 0;
+    int k = FWD ? 0 : p.L - 1;
+    int sa, sb, eb, ee;
+    share(k, sa, sb, eb, ee);
+    int t = 0, cur = 0;
+    issue(0, sa, min(sb, sa + W4_TE), eb, ee);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (;;) {
+        const int ntiles = max(1, (sb - sa + W4_TE - 1) / W4_TE);
+        const int ta = min(sb, sa + t * W4_TE), tb = min(sb, ta + W4_TE);
+        // the next item: the next tile of this level, or the next level's first tile
+        int nk = k, nsa = sa, nsb = sb, neb = eb, nee = ee, nt = t + 1;
+        const bool more = t + 1 < ntiles || qq + 1 < p.L;
+        if (t + 1 >= ntiles && qq + 1 < p.L) {
+            nk = FWD ? qq + 1 : p.L - 2 - qq;
+            share(nk, nsa, nsb, neb, nee);
+            nt = 0;
+        }
+        if (more) {
+            const int nta = min(nsb, nsa + nt * W4_TE);
+            issue(cur ^ 1, nta, min(nsb, nta + W4_TE), neb, nee);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");   // this tile's copies
+        __syncthreads();
+        // ---- the tile: all gathers in flight, then the combine
+        const int nt_e = tb - ta;
+        const int2 *E = s_e[cur];
+        const int32_t *Dd = s_d[cur];
+        float av[W4_K], dv[W4_K];
+#pragma unroll
+        for (int i = 0; i < W4_K; ++i) {
+            const int j = tid + i * W4_THREADS;
+            av[i] = ident;
+            dv[i] = 0.0f;
+            if (j < nt_e) {
+                av[i] = ord2f(__ldcg(p.out + E[j].x));
+                dv[i] = p.eid ? __ldg(p.d + Dd[j]) : __int_as_float(Dd[j]);
+            }
+        }
+        const int kb = s_keys[cur][0], ka = s_keys[cur][1];
+#pragma unroll
+        for (int i = 0; i < W4_K; ++i) {
+            if (i * W4_THREADS >= nt_e) break;   // block-uniform
+            const int j = tid + i * W4_THREADS;
+            const bool valid = j < nt_e;
+            const int key = valid ? E[j].y : -1 - lane;
+            float v = valid ? relax1<FWD>(av[i], sane(dv[i], bad)) : ident;
+            const int prv = __shfl_up_sync(0xffffffffu, key, 1);
+            const int nxt = __shfl_down_sync(0xffffffffu, key, 1);
+            const unsigned smask = __ballot_sync(0xffffffffu, lane == 0 || prv != key);
+            const int sstart = 31 - __clz(smask & ((2u << lane) - 1u));
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const float y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane - o >= sstart) v = comb<MX>(v, y);
+            }
+            if (valid && (lane == 31 || nxt != key)) {
+                // the key of the edge before this segment / after it (tile boundary: the
+                // neighbouring tile's or share's edge)
+                const int j0 = j - (lane - sstart);
+                const int kprev = j0 > 0 ? E[j0 - 1].y : kb;
+                const int knext = j + 1 < nt_e ? E[j + 1].y : ka;
+                if (kprev == key || knext == key) {
+                    if (MX) atomicMax(p.out + key, f2ord(v));
+                    else atomicMin(p.out + key, f2ord(v));
+                } else {
+                    p.out[key] = f2ord(v);
+                }
+            }
+        }
+        __syncthreads();   // buffer `cur` is refilled two items from now
+        cur ^= 1;
+        if (!more) break;
+        if (t + 1 < ntiles) {
+            ++t;
+            continue;
+        }
+        // level done: grid barrier, then the next level (its first tile is in flight)
+        target += gridDim.x;
+        if (tid == 0) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.bar) : "memory");
+            while (ld_acq(p.bar) < target) __nanosleep(32);
+        }
+        __syncthreads();
+        ++qq;
+        k = nk;
+        sa = nsa;
+        sb = nsb;
+        eb = neb;
+        ee = nee;
+        t = 0;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (bad) atomicOr(p.err, ERR_NONFINITE);
+}
+
+template <bool FWD, bool EARLY>
+void launch_w4(Graph &g, Wide4Params &w, cudaStream_t st) {
+    auto kern = k_wide4<FWD, EARLY>;
+    const int smem = int(2 * W4_TE * (sizeof(int2) + sizeof(int32_t)));
+    static std::map<std::pair<const void *, int>, int> cache;
+    static std::mutex mu;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({(const void *)kern, g.device});
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (!per_sm) {
+        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W4_THREADS, smem));
+        std::lock_guard<std::mutex> lk(mu);
+        cache[{(const void *)kern, g.device}] = per_sm;
+    }
+    if (per_sm < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
+    void *args[] = {&w};
+    HF_CUDA(cudaLaunchCooperativeKernel((const void *)kern, g.sms, W4_THREADS, args, smem, st));
+    g.launches += 1;
+}
+
 // before a k_wide3 pass: every node's accumulator at the identity, nodes without edges
 // in this direction at their value (forward: at_src or +0; backward: T) -- by node id,
 // so every access is coalesced (ptr = the node-indexed CSR of this direction)
@@ -1458,11 +1654,25 @@ void wide_pass(Graph &g, const float *d, bool lo_delays, int32_t S, const float 
         bar3.alloc(sizeof(unsigned) * 2, st);                                                      \
         HF_CUDA(cudaMemsetAsync(bar3.p, 0, sizeof(unsigned) * 2, st));                             \
         w.bar = bar3.as<unsigned>();                                                               \
-        const int nblk = w3_blocks<FWD, EE>(g);                                                    \
-        if (nblk < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");         \
-        void *args[] = {&w};                                                                       \
-        HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_wide3<FWD, EE>, nblk, W3_THREADS, args, \
-                                            0, st));                                               \
+        if (env_int_w("HF_WIDE4", 0)) {                                                           \
+            Wide4Params w4{};                                                                      \
+            w4.level_ptr = w.level_ptr;                                                            \
+            w4.row_ptr = w.row_ptr;                                                                \
+            w4.edge = w.edge;                                                                      \
+            w4.eid = w.eid;                                                                        \
+            w4.d = w.d;                                                                            \
+            w4.L = w.L;                                                                            \
+            w4.out = w.out;                                                                        \
+            w4.err = w.err;                                                                        \
+            w4.bar = w.bar;                                                                        \
+            launch_w4<FWD, EE>(g, w4, st);                                                         \
+        } else {                                                                                   \
+            const int nblk = w3_blocks<FWD, EE>(g);                                                \
+            if (nblk < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");     \
+            void *args[] = {&w};                                                                   \
+            HF_CUDA(cudaLaunchCooperativeKernel((const void *)k_wide3<FWD, EE>, nblk, W3_THREADS,  \
+                                                args, 0, st));                                     \
+        }                                                                                          \
         k_w3_final<FWD, EE><<<grid_for(g.n, 256, g.sms), 256, 0, st>>>(acc, g.n, other, slack,     \
                                                                        wns_ord);                   \
         HF_CHECK_LAUNCH();                                                                         \

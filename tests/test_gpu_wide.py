@@ -27,10 +27,10 @@ def hf():
 
 
 # S = 1 runs k_wide3 (edge units, ordered-int accumulation in place) by default; the
-# warp-unit kernel k_wide1 (HF_WIDE3=0) and the row-range kernel k_wide2 (HF_WIDE2=1)
-# stay under test
-KERNELS = {"w3": {"HF_WIDE3": "1"}, "w1": {"HF_WIDE3": "0", "HF_WIDE2": "0"},
-           "w2": {"HF_WIDE3": "0", "HF_WIDE2": "1"}}
+# staged-tile k_wide4 (HF_WIDE4=1), the warp-unit kernel k_wide1 (HF_WIDE3=0) and the
+# row-range kernel k_wide2 (HF_WIDE2=1) stay under test
+KERNELS = {"w4": {"HF_WIDE3": "1", "HF_WIDE4": "1"}, "w3": {"HF_WIDE3": "1", "HF_WIDE4": "0"},
+           "w1": {"HF_WIDE3": "0", "HF_WIDE2": "0"}, "w2": {"HF_WIDE3": "0", "HF_WIDE2": "1"}}
 
 
 def use_kernel(monkeypatch, name):
@@ -38,7 +38,7 @@ def use_kernel(monkeypatch, name):
         monkeypatch.setenv(k, v)
 
 
-@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
+@pytest.mark.parametrize("w2", ["w4", "w3", "w1", "w2"])
 @pytest.mark.parametrize("name,scale", [("C1", 1.0), ("C3", 0.05), ("C2-random", 0.01),
                                         ("C5", 0.01), ("C5", 0.1)])
 def test_wide_single(hf, name, scale, w2, monkeypatch):
@@ -48,7 +48,7 @@ def test_wide_single(hf, name, scale, w2, monkeypatch):
     check_single(hf, g.n, g.m, g.in_ptr, g.in_src, g.delay, g.at_src, g.t_req)
 
 
-@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
+@pytest.mark.parametrize("w2", ["w4", "w3", "w1", "w2"])
 def test_wide_tiny_random_dags(hf, w2, monkeypatch):
     monkeypatch.setenv("HF_WIDE", "1")
     use_kernel(monkeypatch, w2)
@@ -62,7 +62,7 @@ def test_wide_tiny_random_dags(hf, w2, monkeypatch):
                      float(mixed_delays(rng, 1)[0]))
 
 
-@pytest.mark.parametrize("w2", ["w3", "w1", "w2"])
+@pytest.mark.parametrize("w2", ["w4", "w3", "w1", "w2"])
 def test_wide_hub_fan_in(hf, w2, monkeypatch):
     """One node with 10^4 predecessors (C5's planted hub): k_wide1 folds its slices by
     atomics into one slot and its consumers read the slot; k_wide2 keeps the row in
