@@ -17,7 +17,10 @@
  *     446).  hf_last_error() returns a thread-local message for the last
  *     failure on the calling thread.  Errors detected on the device by an
  *     asynchronous _d call (non-finite scenario delay) are latched in the graph
- *     and returned by the next hf_sync() or host-pointer call.
+ *     and returned by the next hf_sync() or host-pointer call.  A dataflow wait
+ *     that outlives its watchdog (HF_WATCHDOG_SPINS poll rounds; a schedule bug,
+ *     never a legal input) is latched the same way and returned as HF_ERR_CUDA.
+ *   - Every entry point is one NVTX range named after the call (tracing).
  *   - Indices are int32, values fp32 (IEEE binary32, round-to-nearest-even, no
  *     flush-to-zero).  n, m < 2^31.  -0.0 inputs are canonicalised to +0.0;
  *     NaN / +-inf inputs are rejected with HF_ERR_INVALID_ARG (reading R9).

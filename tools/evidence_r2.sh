@@ -17,7 +17,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python tools/launches.py $O/launches_C4.csv > $O/launches_C4_summary.txt 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_flow -c 2 -o $O/flow_C4 \
     python bench.py --ncu --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-secondary > $O/ncu_flow.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_wide1 -c 2 -o $O/wide1_C5 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_wide3 -c 2 -o $O/wide3_C5 \
     python bench.py --config C5 --ncu --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_wide.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lev_kahn -c 1 -o $O/kahn_C3 \
     python bench.py --config C3 --ncu --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_kahn.log 2>&1
@@ -25,7 +25,7 @@ for c in C2-chain C2-tree C2-random; do
   timeout 600 ncu --set full --clock-control none -k regex:"k_lev_" -c 6 -o $O/lev_$c \
       python bench.py --config $c --ncu --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/ncu_lev_$c.log 2>&1
 done
-for r in flow_C4 wide1_C5 kahn_C3 lev_C2-chain lev_C2-tree lev_C2-random; do
+for r in flow_C4 wide3_C5 kahn_C3 lev_C2-chain lev_C2-tree lev_C2-random; do
   python tools/ncu_summary.py $O/$r.ncu-rep > $O/ncu_${r}_summary.txt 2>&1
 done
 python tools/ncu_stalls.py $O/flow_C4.ncu-rep k_flow 15 > $O/ncu_flow_C4_stalls.txt 2>&1
