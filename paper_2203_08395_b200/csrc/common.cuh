@@ -7,6 +7,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -90,7 +92,10 @@ struct TaskSched {
 constexpr int LO_SPLIT = 8;
 // a long row is cut into parts of LO_PE edges (part ids: exclusive scan over the
 // level-ordered rows of ceil(degree / LO_PE) for long rows, 0 otherwise)
-constexpr int LO_PE = 20;
+#ifndef LO_PE_OVR
+#define LO_PE_OVR 20
+#endif
+constexpr int LO_PE = LO_PE_OVR;
 // the level-synchronous passes cut a long row into slices of WIDE_SL edges (one
 // thread each, all loads of a slice in flight at once)
 constexpr int WIDE_SL = 8;
@@ -237,6 +242,20 @@ inline int bits_for(int64_t max_key) {
     while (b < 31 && (int64_t(1) << b) <= max_key) ++b;
     return b;
 }
+// The dynamic shared-memory limit of a kernel is one attribute per (function,
+// device): raise it to the largest size ever requested and never lower it, so that
+// launches of one kernel with different scratch sizes (e.g. batches of S = 128, then
+// 64, then 128 again) all stay within it.  Thread-safe; one driver call per new max.
+inline void ensure_dyn_smem(const void *func, int device, size_t bytes) {
+    static std::map<std::pair<const void *, int>, size_t> mx;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &cur = mx[{func, device}];
+    if (bytes <= cur) return;
+    HF_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    cur = bytes;
+}
+
 inline int grid_for(int64_t work, int block, int sms, int per_sm = 8) {
     int64_t gsz = (work + block - 1) / block;
     int64_t cap = int64_t(sms) * per_sm;

@@ -1364,11 +1364,12 @@ void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
         if (it != cache.end()) per_sm = it->second;
     }
     if (!per_sm) {
-        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ensure_dyn_smem((const void *)kern, g.device, smem);
         HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = per_sm;
     }
+    ensure_dyn_smem((const void *)kern, g.device, smem);   // (cached: a map lookup)
     if (per_sm < 1) fail(HF_ERR_CUDA, "propagation kernel does not fit on an SM");
     const int cap = env_int("HF_CTAS_PER_SM", 0);
     if (cap > 0) per_sm = std::min(per_sm, cap);
@@ -1396,7 +1397,9 @@ int occupancy_of(FlowParams &p) {
     auto it = cache.find(smem);
     if (it != cache.end()) return it->second;
     int per_sm = 0;
-    HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int dev = 0;
+    HF_CUDA(cudaGetDevice(&dev));
+    ensure_dyn_smem((const void *)kern, dev, smem);
     HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FLOW_THREADS, smem));
     cache[smem] = per_sm;
     return per_sm;
@@ -1514,9 +1517,10 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     // scratch capacity ecap = tw + LO_SPLIT edges (>= LO_PE), ncap = tw rows
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
     // measured per direction (tools/tune.py, C3 S=64): forward 12, backward 14
-    int tw = env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? (FWD ? 12 : 14) : 16));
-    tw = std::max(LO_PE - LO_SPLIT, std::min(tw, 32 * slots - LO_SPLIT));
-    p.ecap = tw + LO_SPLIT;
+    int tw = env_int(FWD ? "HF_TW_F" : "HF_TW_B",
+                     env_int("HF_TW", slots == 2 ? 32 : (G <= 2 ? (FWD ? 12 : 14) : 16)));
+    tw = std::max(4, std::min(tw, 32 * slots - LO_SPLIT));
+    p.ecap = std::max(tw + LO_SPLIT, LO_PE);   // a part task has up to LO_PE edges
     p.ncap = tw;
     p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
     p.watchdog_spins = std::max(1, env_int("HF_WATCHDOG_SPINS", 1 << 22));

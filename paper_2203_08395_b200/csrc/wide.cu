@@ -703,11 +703,12 @@ void launch_wide(Graph &g, WideParams &p, cudaStream_t st) {
         if (it != cache.end()) per_sm = it->second;
     }
     if (!per_sm) {
-        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        ensure_dyn_smem((const void *)kern, g.device, smem);
         HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WIDE_THREADS, smem));
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = per_sm;
     }
+    ensure_dyn_smem((const void *)kern, g.device, smem);
     if (per_sm < 1) fail(HF_ERR_CUDA, "wide propagation kernel does not fit on an SM");
     const int cap = env_int_w("HF_WIDE_CTAS_PER_SM", 0);
     if (cap > 0) per_sm = std::min(per_sm, cap);
@@ -1362,7 +1363,7 @@ void launch_w4(Graph &g, Wide4Params &w, cudaStream_t st) {
         if (it != cache.end()) per_sm = it->second;
     }
     if (!per_sm) {
-        HF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        ensure_dyn_smem((const void *)kern, g.device, size_t(smem));
         HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W4_THREADS, smem));
         std::lock_guard<std::mutex> lk(mu);
         cache[{(const void *)kern, g.device}] = per_sm;

@@ -742,3 +742,28 @@ def test_view_sweep_full_c3(hf, S):
     c0 = chunk * B
     assert_bits_equal(at[:, c0:c0 + B].cpu().numpy(), ato, f"at[:, {c0}:{c0 + B}]")
     assert_bits_equal(rat[:, c0:c0 + B].cpu().numpy(), rato, f"rat[:, {c0}:{c0 + B}]")
+
+
+def test_batch_scratch_size_changes_keep_the_kernel_launchable(hf):
+    """One kernel, two shared-memory sizes, in the order that used to fail: S = 128
+    (larger scratch), then S = 64 for the first time (smaller), then S = 128 again --
+    the dynamic shared-memory limit is only ever raised (common.cuh ensure_dyn_smem),
+    so every call launches and stays bit-exact."""
+    import torch
+    dev = torch.device("cuda:0")
+    g = hfgen.config("C3", 0.004)
+    G = hf.hf_graph_create(g.n, g.m, torch.from_numpy(g.in_ptr).to(dev),
+                           torch.from_numpy(g.in_src).to(dev), delay=torch.from_numpy(g.delay).to(dev),
+                           stream=torch.cuda.current_stream())
+    hf.hf_levelize(G)
+    a = torch.from_numpy(g.at_src).to(dev)
+    for S in (128, 64, 128, 64):
+        D = hfgen.scenario_delays(g, 0, S, "ms")
+        T = np.full(S, g.t_req, F32)
+        w = torch.empty(S, dtype=torch.float32, device=dev)
+        hf.hf_run_batch(G, S, torch.from_numpy(D).to(dev), hf.HF_LAYOUT_MS, torch.from_numpy(T).to(dev),
+                        a, w)
+        hf.hf_sync(G)
+        wo = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4)
+        assert_bits_equal(w.cpu().numpy(), wo, f"wns S={S}")
+    G.close()

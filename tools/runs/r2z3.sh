@@ -1,0 +1,5 @@
+set -u
+O=gpurun_out/r2z3; mkdir -p $O
+timeout 600 python tools/env_ab.py --config C4 --S 64 --reps 7 --var "" --var HF_TW=6 --var HF_TW=8 --var HF_TW=10 > $O/ab_tw.txt 2>&1
+HF_TW=8 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --timeout 120 -k "batch_small or tiny or full_c4" > $O/pytest_tw8.txt 2>&1
+echo done
