@@ -89,7 +89,10 @@ struct TaskSched {
 
 // rows with more than LO_SPLIT edges sit at the end of their level in the
 // level-ordered CSRs and are cut into part tasks by the propagation passes
-constexpr int LO_SPLIT = 8;
+#ifndef LO_SPLIT_OVR
+#define LO_SPLIT_OVR 8
+#endif
+constexpr int LO_SPLIT = LO_SPLIT_OVR;
 // a long row is cut into parts of LO_PE edges (part ids: exclusive scan over the
 // level-ordered rows of ceil(degree / LO_PE) for long rows, 0 otherwise)
 #ifndef LO_PE_OVR
