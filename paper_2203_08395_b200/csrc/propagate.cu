@@ -306,7 +306,8 @@ template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 // Only the thread bound: an explicit minimum of 1 block per SM lets ptxas spend
 // 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured); the
 // backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
-template <int V, int LPN, bool FWD, bool GA, bool EARLY>
+// ONE: the pass has one scenario chunk (S = SC): task t is descriptor t
+template <int V, int LPN, bool FWD, bool GA, bool EARLY, bool ONE>
 #if defined(FLOW_MINB_FWD) || defined(FLOW_MINB_BWD)
 #ifndef FLOW_MINB_FWD
 #define FLOW_MINB_FWD 0
@@ -372,6 +373,13 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
 
     // ---- task locator: pass-level q with tb[q] <= t < tb[q+1] (t increases) ----
     auto locate = [&](int t, int &q, int &c, int4 &dsc) {
+        if constexpr (ONE) {
+            // one scenario chunk: task bases are the descriptor offsets, task t is
+            // descriptor t (no level search, no division)
+            c = 0;
+            dsc = __ldg(p.desc + t);
+            return;
+        }
         if (__ldg(p.tb + q + 1) <= t) {
             int lo = q + 1, step = 1;
             while (lo + step < L && __ldg(p.tb + lo + step) <= t) {
@@ -646,7 +654,14 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                 const int k = k0 + r * G + g;
                 uu[r] = k < E ? s_nbr[k] : INT32_MAX;
                 if (uu[r] >= 0 && uu[r] != INT32_MAX)
+#ifdef HF_DBG_FAKE_GATHER
+                    // diagnostic build only (wrong results): gathers read always-final
+                    // rows (delay rows of a 16 MB L2-resident set): the pass without its
+                    // dependency waits -- what the instruction stream alone costs
+                    a[r] = ld_relaxed<V>(p.d + int64_t(uu[r] & 0xffff) * S + col);
+#else
                     a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);
+#endif
             }
             // neighbours cut into parts: combine of their partials (rare; HF_LASTPART:
             // never -- a long row's last part writes it like any other row)
@@ -1347,9 +1362,9 @@ int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int V, int LPN, bool FWD, bool GA, bool EARLY>
+template <int V, int LPN, bool FWD, bool GA, bool EARLY, bool ONE>
 void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
-    auto kern = k_flow<V, LPN, FWD, GA, EARLY>;
+    auto kern = k_flow<V, LPN, FWD, GA, EARLY, ONE>;
     constexpr int SC = V * LPN;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, SC, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
@@ -1386,9 +1401,9 @@ void launch_flow(Graph &g, FlowParams &p, cudaStream_t st, int cap_per_sm) {
 }
 
 // blocks per SM a kernel can keep resident alone (cached occupancy query)
-template <int V, int LPN, bool FWD, bool GA, bool EARLY>
+template <int V, int LPN, bool FWD, bool GA, bool EARLY, bool ONE>
 int occupancy_of(FlowParams &p) {
-    auto kern = k_flow<V, LPN, FWD, GA, EARLY>;
+    auto kern = k_flow<V, LPN, FWD, GA, EARLY, ONE>;
     const WarpLayout WL = warp_layout(p.ecap, p.ncap, V * LPN, FWD, GA);
     const size_t smem = size_t(wmin_bytes(p.S)) + size_t(NWARP) * WL.bytes;
     static std::map<size_t, int> cache;
@@ -1410,11 +1425,20 @@ template <bool FWD, bool GA, bool EARLY>
 int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int op) {
 #define HF_CASE(L)                                                               \
     case L:                                                                      \
-        if (op) return occupancy_of<4, L, FWD, GA, EARLY>(p);           \
-        launch_flow<4, L, FWD, GA, EARLY>(g, p, st, cap);               \
+        if (op) return occupancy_of<4, L, FWD, GA, EARLY, false>(p);    \
+        launch_flow<4, L, FWD, GA, EARLY, false>(g, p, st, cap);        \
         return 0;
     switch (LPN) {
-        HF_CASE(16)
+    case 16:
+        // one 64-column chunk (S = 64, the C4 headline): the specialised kernel
+        if (p.nch == 1 && env_int("HF_ONE", 1)) {
+            if (op) return occupancy_of<4, 16, FWD, GA, EARLY, true>(p);
+            launch_flow<4, 16, FWD, GA, EARLY, true>(g, p, st, cap);
+            return 0;
+        }
+        if (op) return occupancy_of<4, 16, FWD, GA, EARLY, false>(p);
+        launch_flow<4, 16, FWD, GA, EARLY, false>(g, p, st, cap);
+        return 0;
         HF_CASE(8)
         HF_CASE(4)
         HF_CASE(2)
@@ -1431,11 +1455,11 @@ int dispatch_mode(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st, int 
             return dispatch_ga<FWD, true, false>(g, p, LPN, st, cap, op);
         return dispatch_ga<FWD, false, EARLY>(g, p, LPN, st, cap, op);
     } else if (V == 2) {
-        if (op) return occupancy_of<2, 1, FWD, false, EARLY>(p);
-        launch_flow<2, 1, FWD, false, EARLY>(g, p, st, cap);
+        if (op) return occupancy_of<2, 1, FWD, false, EARLY, false>(p);
+        launch_flow<2, 1, FWD, false, EARLY, false>(g, p, st, cap);
     } else {
-        if (op) return occupancy_of<1, 1, FWD, false, EARLY>(p);
-        launch_flow<1, 1, FWD, false, EARLY>(g, p, st, cap);
+        if (op) return occupancy_of<1, 1, FWD, false, EARLY, false>(p);
+        launch_flow<1, 1, FWD, false, EARLY, false>(g, p, st, cap);
     }
     return 0;
 }
