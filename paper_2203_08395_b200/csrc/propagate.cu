@@ -746,7 +746,10 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                         v = ld_relaxed<V>(src);
                     }
                 }
-                if constexpr (FWD) {
+#ifndef HF_BWD_MASK
+#define HF_BWD_MASK 0
+#endif
+                if constexpr (FWD || HF_BWD_MASK) {
 #pragma unroll
                     for (int r = 0; r < RB; ++r)
                         if (mm & (1u << r)) a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);
@@ -1439,22 +1442,21 @@ int occupancy_of(FlowParams &p) {
 // op = 0: launch, op = 1: return the solo occupancy (blocks per SM)
 template <bool FWD, bool GA, bool EARLY>
 int dispatch_ga(Graph &g, FlowParams &p, int LPN, cudaStream_t st, int cap, int op) {
+    // one scenario chunk (S = V * LPN: S = 64 is the C4 headline, also S = 4..32):
+    // the specialised kernel without the task locator
+    const bool one = p.nch == 1 && env_int("HF_ONE", 1);
 #define HF_CASE(L)                                                               \
     case L:                                                                      \
-        if (op) return occupancy_of<4, L, FWD, GA, EARLY, false>(p);    \
-        launch_flow<4, L, FWD, GA, EARLY, false>(g, p, st, cap);        \
+        if (one) {                                                               \
+            if (op) return occupancy_of<4, L, FWD, GA, EARLY, true>(p);          \
+            launch_flow<4, L, FWD, GA, EARLY, true>(g, p, st, cap);              \
+            return 0;                                                            \
+        }                                                                        \
+        if (op) return occupancy_of<4, L, FWD, GA, EARLY, false>(p);             \
+        launch_flow<4, L, FWD, GA, EARLY, false>(g, p, st, cap);                 \
         return 0;
     switch (LPN) {
-    case 16:
-        // one 64-column chunk (S = 64, the C4 headline): the specialised kernel
-        if (p.nch == 1 && env_int("HF_ONE", 1)) {
-            if (op) return occupancy_of<4, 16, FWD, GA, EARLY, true>(p);
-            launch_flow<4, 16, FWD, GA, EARLY, true>(g, p, st, cap);
-            return 0;
-        }
-        if (op) return occupancy_of<4, 16, FWD, GA, EARLY, false>(p);
-        launch_flow<4, 16, FWD, GA, EARLY, false>(g, p, st, cap);
-        return 0;
+        HF_CASE(16)
         HF_CASE(8)
         HF_CASE(4)
         HF_CASE(2)
@@ -1471,11 +1473,23 @@ int dispatch_mode(Graph &g, FlowParams &p, int V, int LPN, cudaStream_t st, int 
             return dispatch_ga<FWD, true, false>(g, p, LPN, st, cap, op);
         return dispatch_ga<FWD, false, EARLY>(g, p, LPN, st, cap, op);
     } else if (V == 2) {
-        if (op) return occupancy_of<2, 1, FWD, false, EARLY, false>(p);
-        launch_flow<2, 1, FWD, false, EARLY, false>(g, p, st, cap);
+        // (S = 2: one chunk; odd multiples of 2 above: several)
+        if (p.nch == 1 && env_int("HF_ONE", 1)) {
+            if (op) return occupancy_of<2, 1, FWD, false, EARLY, true>(p);
+            launch_flow<2, 1, FWD, false, EARLY, true>(g, p, st, cap);
+        } else {
+            if (op) return occupancy_of<2, 1, FWD, false, EARLY, false>(p);
+            launch_flow<2, 1, FWD, false, EARLY, false>(g, p, st, cap);
+        }
     } else {
-        if (op) return occupancy_of<1, 1, FWD, false, EARLY, false>(p);
-        launch_flow<1, 1, FWD, false, EARLY, false>(g, p, st, cap);
+        // (S = 1, the single-graph calls: one chunk)
+        if (p.nch == 1 && env_int("HF_ONE", 1)) {
+            if (op) return occupancy_of<1, 1, FWD, false, EARLY, true>(p);
+            launch_flow<1, 1, FWD, false, EARLY, true>(g, p, st, cap);
+        } else {
+            if (op) return occupancy_of<1, 1, FWD, false, EARLY, false>(p);
+            launch_flow<1, 1, FWD, false, EARLY, false>(g, p, st, cap);
+        }
     }
     return 0;
 }
@@ -1567,7 +1581,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     tw = std::max(4, std::min(tw, 32 * slots - LO_SPLIT));
     p.ecap = std::max(tw + LO_SPLIT, LO_PE);   // a part task has up to LO_PE edges
     p.ncap = tw;
-    p.sleep_max = std::max(32, env_int("HF_SLEEP_MAX", 64));
+    p.sleep_max = std::max(32, env_int(FWD ? "HF_SLEEP_MAX" : "HF_SLEEP_MAX_B", env_int("HF_SLEEP_MAX", 64)));
     p.watchdog_spins = std::max(1, env_int("HF_WATCHDOG_SPINS", 1 << 22));
     p.poll_all = env_int("HF_POLL_ALL", 1);
     TaskSched &ts = FWD ? g.ts_f : g.ts_b;
