@@ -232,6 +232,7 @@ struct FlowParams {
     const int32_t *doff;      // [L+1]
     const int32_t *tb;        // [L+1] first global task of pass-level q
     int32_t L, S, nch;
+    int32_t nch_shift;        // log2(nch) for a power of two, else -1
     int32_t ecap, ncap;       // per-warp scratch capacity (edges, rows)
     const int32_t *part_np;   // [parts] by first part id
     float *part_buf;          // [parts][S]   (HF_LASTPART = 0)
@@ -394,10 +395,18 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
             }
             q = lo;
         }
+        // inside a pass-level the tasks are descriptor-major, chunk-minor
+        // (t = tb[q] + j * nch + c): with a power-of-two chunk count a shift and a mask,
+        // and a warp keeps one chunk when W is a multiple of nch
         const int rel = t - __ldg(p.tb + q);
-        const int ntq = __ldg(p.nt + q);
-        c = rel / ntq;
-        const int j = rel - c * ntq;
+        int j;
+        if (p.nch_shift >= 0) {
+            j = rel >> p.nch_shift;
+            c = rel & (p.nch - 1);
+        } else {
+            j = rel / p.nch;
+            c = rel - j * p.nch;
+        }
         dsc = __ldg(p.desc + __ldg(p.doff + q) + j);
     };
     // index loads of one task (no use of the results here: they land during the
@@ -1566,6 +1575,7 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     const int G = 32 / LPN;
     cx.LPN = LPN;
     p.nch = p.S / (V * LPN);
+    p.nch_shift = (p.nch & (p.nch - 1)) == 0 ? __builtin_ctz(unsigned(p.nch)) : -1;
     // task shape: weight tw (rows + edges) per task; rows longer than LO_SPLIT edges
     // (at the end of their level, levelize.cu) are cut into parts of LO_PE edges;
     // scratch capacity ecap = tw + LO_SPLIT edges (>= LO_PE), ncap = tw rows
