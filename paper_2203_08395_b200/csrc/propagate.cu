@@ -1532,7 +1532,7 @@ __global__ void k_fill_nan4(uint4 *__restrict__ p4, size_t n4, uint32_t *__restr
 }
 
 void fill_nan(Graph &g, float *buf, size_t cnt, cudaStream_t st) {
-    const int ctas = env_int("HF_FILL_CTAS", 8 * g.sms);   // 0: cudaMemsetAsync
+    const int ctas = env_int("HF_FILL_CTAS", 16 * g.sms);   // 0: cudaMemsetAsync (16 per SM: -1% phase vs 8)
     if (ctas > 0 && (reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
         k_fill_nan4<<<ctas, 256, 0, st>>>(reinterpret_cast<uint4 *>(buf), cnt / 4,
                                           reinterpret_cast<uint32_t *>(buf), cnt);
