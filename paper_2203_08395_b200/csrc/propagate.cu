@@ -697,17 +697,44 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                                 for (int j = 0; j < V; ++j) v[t].x[j] = ident<MX>();
                             }
                         }
-#pragma unroll
-                        for (int t = 0; t < PW; ++t) {
+                        if constexpr (PW == 1) {
+                            // (the four-column forward: its kernel's code is kept as it
+                            // was -- the group form below cost it 6% in codegen)
                             int ns = 32;
-                            while (has_nan<V>(v[t])) {
+                            while (has_nan<V>(v[0])) {
                                 __nanosleep(ns);
                                 ns = min(ns * 2, p.sleep_max);
-                                v[t] = ld_relaxed<V>(src + int64_t(t) * S);
+                                v[0] = ld_relaxed<V>(src);
                             }
+                        } else {
+                            // wait for the PW partials together: every round re-loads all
+                            // the missing ones (one round trip for the group; waiting on one
+                            // partial after the other paid a round trip per late partial)
+                            int ns = 32, spins = 0;
+                            for (;;) {
+                                bool miss = false;
+#pragma unroll
+                                for (int t = 0; t < PW; ++t) miss |= has_nan<V>(v[t]);
+                                if (!miss) break;
+                                if (++spins > p.watchdog_spins) {
+                                    atomicOr(p.err, ERR_WATCHDOG);
+#pragma unroll
+                                    for (int t = 0; t < PW; ++t)
+#pragma unroll
+                                        for (int j = 0; j < V; ++j) v[t].x[j] = 0.0f;
+                                    break;
+                                }
+                                __nanosleep(ns);
+                                ns = min(ns * 2, p.sleep_max);
+#pragma unroll
+                                for (int t = 0; t < PW; ++t)
+                                    if (has_nan<V>(v[t])) v[t] = ld_relaxed<V>(src + int64_t(t) * S);
+                            }
+                        }
+#pragma unroll
+                        for (int t = 0; t < PW; ++t)
 #pragma unroll
                             for (int j = 0; j < V; ++j) a[r].x[j] = combine<MX>(a[r].x[j], v[t].x[j]);
-                        }
                     }
                 }
             }
