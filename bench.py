@@ -517,7 +517,7 @@ def main():
         b_fwd, b_bwd = algorithmic_bytes(n, m, 1)
         kern_ms = (fwd_ms + bwd_ms) / K
         algo = b_fwd + b_bwd
-        kname = "forward + backward propagation kernels (k_flow; k_wide2 on wide graphs at S = 1)"
+        kname = "forward + backward propagation kernels (k_flow; on wide graphs at S = 1 the level-synchronous k_wide3 with its init and finalisation)"
     elif kind == "forward":
         edges_step = 1.0 * m * world
         algo = algorithmic_bytes(n, m, 1)[0]

@@ -13,7 +13,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_sectors_srcunit_tex_op_read.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "smsp__inst_executed.sum", "launch__occupancy_limit_registers",
-        "launch__occupancy_limit_shared_mem"]
+        "launch__occupancy_limit_shared_mem", "smsp__issue_active.avg.pct_of_peak_sustained_active"]
 
 
 def main(rep):
