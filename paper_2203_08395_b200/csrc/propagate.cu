@@ -304,22 +304,21 @@ template <int NSL> struct Idx {
 };
 template <int LPN> constexpr int idx_slots() { return LPN <= 2 ? 2 : 1; }
 
-// Only the thread bound: an explicit minimum of 1 block per SM lets ptxas spend
-// 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured); the
-// backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
-// ONE: the pass has one scenario chunk (S = SC): task t is descriptor t
-template <int V, int LPN, bool FWD, bool GA, bool EARLY, bool ONE>
-#if defined(FLOW_MINB_FWD) || defined(FLOW_MINB_BWD)
+// Launch bounds: the thread bound only.  An explicit minimum of 1 block lets ptxas
+// spend 140-152 registers (3 CTAs per SM, +5% forward / +7% backward, measured);
+// the backward experiment with 6 blocks is -DFLOW_MINB_BWD=6.
 #ifndef FLOW_MINB_FWD
 #define FLOW_MINB_FWD 0
 #endif
 #ifndef FLOW_MINB_BWD
 #define FLOW_MINB_BWD 0
 #endif
-__global__ void __launch_bounds__(FLOW_THREADS, FWD ? FLOW_MINB_FWD : FLOW_MINB_BWD) k_flow(FlowParams p) {
-#else
-__global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
-#endif
+template <int V, bool FWD, bool ONE> constexpr int flow_minb() {
+    return FWD ? FLOW_MINB_FWD : FLOW_MINB_BWD;
+}
+// ONE: the pass has one scenario chunk (S = SC): task t is descriptor t
+template <int V, int LPN, bool FWD, bool GA, bool EARLY, bool ONE>
+__global__ void __launch_bounds__(FLOW_THREADS, flow_minb<V, FWD, ONE>()) k_flow(FlowParams p) {
     // MX: the pass combines with max (late forward, early backward), else min
     constexpr bool MX = FWD != EARLY;
     constexpr int SC = V * LPN;   // columns per chunk
@@ -697,14 +696,18 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_flow(FlowParams p) {
                                 for (int j = 0; j < V; ++j) v[t].x[j] = ident<MX>();
                             }
                         }
-                        if constexpr (PW == 1) {
-                            // (the four-column forward: its kernel's code is kept as it
-                            // was -- the group form below cost it 6% in codegen)
-                            int ns = 32;
-                            while (has_nan<V>(v[0])) {
-                                __nanosleep(ns);
-                                ns = min(ns * 2, p.sleep_max);
-                                v[0] = ld_relaxed<V>(src);
+                        if constexpr (PW == 1 || !ONE) {
+                            // one partial after the other (the four-column forward, PW 1,
+                            // and the multi-chunk kernels: the group form below cost them
+                            // 6% / 3..4% in codegen -- 128 registers at several chunks)
+#pragma unroll
+                            for (int t = 0; t < PW; ++t) {
+                                int ns = 32;
+                                while (has_nan<V>(v[t])) {
+                                    __nanosleep(ns);
+                                    ns = min(ns * 2, p.sleep_max);
+                                    v[t] = ld_relaxed<V>(src + int64_t(t) * S);
+                                }
                             }
                         } else {
                             // wait for the PW partials together: every round re-loads all
