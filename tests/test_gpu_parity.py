@@ -278,14 +278,34 @@ def gpu_batch_device(hf, g, D_ms, T, s_local, want_at_rat=True):
     return out
 
 
-@pytest.mark.parametrize("S", [1, 2, 3, 8, 64])
+@pytest.mark.parametrize("S", [1, 2, 3, 4, 8, 16, 24, 32, 48, 64, 96, 192])
 def test_batch_small(hf, S):
+    # every chunk shape: the single-chunk kernels (S = 1, 2, 4, 8, 16, 32, 64: one
+    # lane-group width each), several chunks with a power-of-two count (S = 128 in the
+    # schedule test below) and with three (S = 24, 48, 96, 192: the division locator)
     g = hfgen.config("C3", 0.004)
     D = hfgen.scenario_delays(g, 0, S, "ms")
     T = np.full(S, g.t_req, F32)
     T[::2] -= 3.5
     w, at, rat = gpu_batch_device(hf, g, D, T, S)
     wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=4,
+                                 want_at_rat=True)
+    assert_bits_equal(at, ato, "at")
+    assert_bits_equal(rat, rato, "rat")
+    assert_bits_equal(w, wo, "wns")
+
+
+@pytest.mark.parametrize("S", [64, 24])
+def test_batch_long_rows(hf, S):
+    # a graph with hubs (C3 at 5%: fan-out up to 91, 503 long backward rows cut into
+    # parts): the partials of a long neighbour waited on as a group (single-chunk
+    # kernel, S = 64) and one after the other (three chunks, S = 24)
+    g = hfgen.config("C3", 0.05)
+    D = hfgen.scenario_delays(g, 0, S, "ms")
+    T = np.full(S, g.t_req, F32)
+    T[1::3] += 1.25
+    w, at, rat = gpu_batch_device(hf, g, D, T, S)
+    wo, ato, rato = oracle.batch(g.n, g.m, g.in_ptr, g.in_src, D, T, g.at_src, "ms", threads=8,
                                  want_at_rat=True)
     assert_bits_equal(at, ato, "at")
     assert_bits_equal(rat, rato, "rat")
