@@ -743,10 +743,9 @@ __global__ void __launch_bounds__(FLOW_THREADS, flow_minb<V, FWD, ONE>()) k_flow
             }
             // wait until every gathered element is final (not the NaN sentinel): every
             // lane re-loads its own missing vectors once per round (one round trip per
-            // round, back-off between rounds).  Forward: the lane's missing slots as a
-            // bitmask (~40 instructions a round instead of ~120: forward -5%); backward:
-            // the per-slot re-check (the bitmask form measured +4..7% there -- its
-            // hoisted row addresses cost the backward kernel registers)
+            // round, back-off between rounds): the lane's missing slots as a bitmask
+            // (~40 instructions a round instead of ~120: forward -5%, single-chunk
+            // backward -1%), or the per-slot re-check (multi-chunk backward)
             unsigned mm = 0;
 #pragma unroll
             for (int r = 0; r < RB; ++r)
@@ -786,9 +785,13 @@ __global__ void __launch_bounds__(FLOW_THREADS, flow_minb<V, FWD, ONE>()) k_flow
                     }
                 }
 #ifndef HF_BWD_MASK
-#define HF_BWD_MASK 0
+#define HF_BWD_MASK 1
 #endif
-                if constexpr (FWD || HF_BWD_MASK) {
+                // the bitmask rounds in the forward kernels and in the single-chunk
+                // four-column backward (-1..2%; at S = 1 +1.5%: not there); the
+                // multi-chunk backward keeps the per-slot loop (the bitmask form cost
+                // it +15% at S = 256)
+                if constexpr (FWD || (HF_BWD_MASK && ONE && V == 4)) {
 #pragma unroll
                     for (int r = 0; r < RB; ++r)
                         if (mm & (1u << r)) a[r] = ld_relaxed<V>(p.out + int64_t(uu[r]) * S + col);

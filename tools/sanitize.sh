@@ -5,7 +5,7 @@
 # those tests launch.  Output: gpurun_out/sanitize/<tool>.txt
 set -u
 O=gpurun_out/sanitize; mkdir -p $O
-SEL="golden or tiny or batch_small or isolated or multi_edges or empty or critical_path_integer or top_k_device and 0.004 or mis_ties or early_mode_tiny or config_single and C1"
+SEL="golden or tiny or batch_small or long_rows and 64 or isolated or multi_edges or empty or critical_path_integer or top_k_device and 0.004 or mis_ties or early_mode_tiny or config_single and C1"
 for tool in racecheck synccheck memcheck; do
   extra=""
   [ $tool = racecheck ] && extra="--racecheck-report all"
