@@ -1615,10 +1615,11 @@ void prepare_pass(Graph &g, FlowParams &p, int V, PassCtx &cx, bool fill_out = t
     const int slots = LPN <= 2 ? 2 : 1;   // idx_slots<LPN>()
     // measured per direction (tools/tune.py, C3 S=64): forward 12, backward 14
     // measured (C4, profiles/round2/c4_flow_variants.txt): one 64-column chunk per row
-    // (S = 64) wants smaller tasks (forward 11, backward 10: -3%); two chunks (S = 128)
+    // (S = 64) wants smaller tasks (forward 11, backward 10: -3%; with the single-chunk
+    // kernel forward 10, -2%: profiles/round2/tw_retune_ab.txt); two chunks (S = 128)
     // 12 / 14; four and more (S = 256, 1024: the level already has >= 4x the tasks)
     // larger forward tasks (20: -4..-10% forward), backward 14
-    const int tw_fb = p.nch == 1 ? (FWD ? 11 : 10) : (p.nch == 2 ? (FWD ? 12 : 14) : (FWD ? 20 : 14));
+    const int tw_fb = p.nch == 1 ? (FWD ? 10 : 10) : (p.nch == 2 ? (FWD ? 12 : 14) : (FWD ? 20 : 14));
     const int tw_dflt = slots == 2 ? 32 : (G <= 2 ? tw_fb : 16);
     int tw = env_int(FWD ? "HF_TW_F" : "HF_TW_B", env_int("HF_TW", tw_dflt));
     tw = std::max(4, std::min(tw, 32 * slots - LO_SPLIT));
