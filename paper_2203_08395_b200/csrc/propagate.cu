@@ -10,7 +10,8 @@
 //
 // Dataflow design.  One persistent cooperative launch per pass.
 //   * The pass is a list of WARP TASKS in pass order (levels ascending forward,
-//     descending backward; inside a level, scenario chunks of SC columns).  A
+//     descending backward; inside a level descriptor-major, scenario chunk of SC
+//     columns minor; with one chunk, k_flow<..., ONE> maps task t to descriptor t).  A
 //     normal task is a run of consecutive level-ordered rows (weight = edges +
 //     rows <= tw + split); a row with more than `split` edges is cut into PART
 //     tasks whose partial max/min go to part_buf.  Task t belongs to warp
@@ -31,9 +32,13 @@
 //     per SC-column chunk); backward fuses slack = rat - at and keeps per-lane
 //     minima, folded per CTA into the worst slack (ordered-int atomicMin).
 //   * Rows cut into parts are read by their consumers as the combine of their
-//     partials (each sentinel-checked; the neighbour id is encoded as
-//     -(first part id + 1), levelize.cu); their own rows are written after the
-//     pass by k_finalize_split.
+//     partials (each sentinel-checked, PW in flight, waited on as a group in the
+//     single-chunk kernels; the neighbour id is encoded as -(first part id + 1),
+//     levelize.cu); their own rows are written after the pass by k_finalize_split.
+//   * At S = 64 the passes are bound more by their instruction stream than by the
+//     dependency chain (fake-gather diagnostic, ncu issue-active),
+//     so the hot loops are written for instruction count: the poll rounds keep a
+//     per-lane bitmask of missing slots (forward, single-chunk backward).
 #include <algorithm>
 #include <map>
 #include <mutex>
