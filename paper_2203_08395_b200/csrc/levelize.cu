@@ -155,6 +155,9 @@ __device__ __forceinline__ unsigned long long lev_gtimer() {
 }
 
 constexpr int KCH = 1;    // contracted edges per frontier entry (one lane per edge)
+#ifndef KAHN_COOP_APPEND
+#define KAHN_COOP_APPEND 1
+#endif
 
 // warp-aggregated append of `cnt` entries {start + t*KCH, node} (t < cnt) per lane
 __device__ __forceinline__ void warp_append_chunks(int cnt, int start, int node, int2 *list,
@@ -189,8 +192,29 @@ __device__ __forceinline__ void warp_append_chunks64(int cnt, int start, int nod
     if (total == 0) return;
     int base = 0;
     if (lane == 31) base = int(unsigned(atomicAdd(word, (unsigned long long)total)));
-    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+    base = __shfl_sync(0xffffffffu, base, 31);
+#if KAHN_COOP_APPEND
+    // the warp writes its `total` entries together, 32 at a time: entry i belongs to
+    // the lane o with excl[o] <= i < incl[o] (binary search over the lanes' inclusive
+    // prefixes), so a hub's out-edges do not serialise on one lane
+    const int excl = incl - cnt;
+    for (int i0 = 0; i0 < total; i0 += 32) {
+        const int i = i0 + lane;
+        int o = 0;
+#pragma unroll
+        for (int b = 16; b >= 1; b >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, o + b - 1);
+            if (v <= i) o += b;
+        }
+        const int st = __shfl_sync(0xffffffffu, start, o);
+        const int ex = __shfl_sync(0xffffffffu, excl, o);
+        const int nd = __shfl_sync(0xffffffffu, node, o);
+        if (i < total) list[base + i] = make_int2(st + (i - ex) * KCH, nd);
+    }
+#else
+    base += incl - cnt;
     for (int t = 0; t < cnt; ++t) list[base + t] = make_int2(start + t * KCH, node);
+#endif
 }
 
 // Kahn over the junctions, frontier-synchronous; lev[j] = max(lev[r] + w) over the
